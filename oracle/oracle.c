@@ -1,0 +1,295 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU implementation of what the GPU path
+ * computes, written from the paper (H. Zhang, B. Meng, Y. Liang, "Sort Race",
+ * arXiv 1609.04471; cited as PAPER.md:<line>) and from the definitions in
+ * SURVEY.md §8(c).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or constant generator with paper_1609_04471_b200/csrc.
+ *
+ * Keys are widened to int64 internally (order-preserving for int32), and every
+ * element carries a 4-byte opaque payload.  Ascending order is signed numeric
+ * order.  No blocking, fusion or reordering beyond the plain
+ * definitions below.
+ *
+ * Functions and the passage each follows:
+ *   or_sort            stable top-down mergesort (north star "plain, slow,
+ *                      single-threaded CPU mergesort"; merge keeps A on ties,
+ *                      PAPER.md:99 "(f) ... any element in A no bigger than
+ *                      the first element of B" ; stability PAPER.md:280)
+ *   or_descents        |{i : a_i > a_{i+1}}|  = Run(A) - 1
+ *   or_asc_runs        maximal ascending runs, split at descents
+ *   or_desc_runs       maximal descending runs; keys-only: non-increasing,
+ *                      pairs: strictly decreasing
+ *   or_reverse         reverse a[s..e)  (Appendix A "reverse")
+ *   or_merge           stable merge of two sorted runs, A wins ties
+ *   or_merge_path      #A elements among the first d outputs of or_merge,
+ *                      by running the merge d steps (PAPER.md:100 galloping
+ *                      locates "the position in A where the current element
+ *                      in B should go")
+ *   or_splitters       stratified sample -> sort -> every o-th -> dedup;
+ *                      equality flag when a splitter occurs > gamma = 2 times
+ *                      in the sample (PAPER.md:157 pseudo-median sampling;
+ *                      PAPER.md:168 "(g) ... more than gamma = 2 elements
+ *                      equal to the pivot, use the 3-way splitting")
+ *   or_classify        bucket of x: i = #{splitters < x}; 2i+1 if x equals
+ *                      splitter i and its equality flag is set, else 2i
+ *                      (3-way split)
+ *   or_stable_partition stable counting distribution by bucket (PAPER.md:159
+ *                      (e): presortedness not disturbed)
+ *   or_count           #{x < v}, #{x <= v}  (rank) for sampled checks
+ *   or_stable_rank     #{j: k_j < k_i} + #{j < i: k_j = k_i}
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    int64_t key;
+    uint32_t val;
+} rec_t;
+
+/* ---- stable top-down mergesort ------------------------------------------------ */
+
+static void or_merge_recs(const rec_t *a, int64_t na, const rec_t *b, int64_t nb, rec_t *out) {
+    int64_t i = 0, j = 0, k = 0;
+    while (i < na && j < nb) {
+        if (a[i].key <= b[j].key) out[k++] = a[i++]; /* A wins ties: stable */
+        else out[k++] = b[j++];
+    }
+    while (i < na) out[k++] = a[i++];
+    while (j < nb) out[k++] = b[j++];
+}
+
+static void msort(rec_t *a, rec_t *tmp, int64_t lo, int64_t hi) {
+    if (hi - lo <= 1) return;
+    int64_t mid = lo + (hi - lo) / 2;
+    msort(a, tmp, lo, mid);
+    msort(a, tmp, mid, hi);
+    or_merge_recs(a + lo, mid - lo, a + mid, hi - mid, tmp + lo);
+    memcpy(a + lo, tmp + lo, (size_t)(hi - lo) * sizeof(rec_t));
+}
+
+static int sort_recs(rec_t *r, int64_t n) {
+    if (n <= 1) return 0;
+    rec_t *tmp = (rec_t *)malloc((size_t)n * sizeof(rec_t));
+    if (!tmp) return -1;
+    msort(r, tmp, 0, n);
+    free(tmp);
+    return 0;
+}
+
+/* keys: int32 (ks=4) or int64 (ks=8); vals may be NULL (keys-only sort). */
+static int64_t load_key(const void *k, int ks, int64_t i) {
+    return ks == 4 ? (int64_t)((const int32_t *)k)[i] : ((const int64_t *)k)[i];
+}
+static void store_key(void *k, int ks, int64_t i, int64_t v) {
+    if (ks == 4) ((int32_t *)k)[i] = (int32_t)v;
+    else ((int64_t *)k)[i] = v;
+}
+
+int or_sort(void *keys, uint32_t *vals, int64_t n, int ks) {
+    if (n <= 1) return 0;
+    rec_t *r = (rec_t *)malloc((size_t)n * sizeof(rec_t));
+    if (!r) return -1;
+    for (int64_t i = 0; i < n; i++) {
+        r[i].key = load_key(keys, ks, i);
+        r[i].val = vals ? vals[i] : (uint32_t)i;
+    }
+    int rc = sort_recs(r, n);
+    if (rc == 0)
+        for (int64_t i = 0; i < n; i++) {
+            store_key(keys, ks, i, r[i].key);
+            if (vals) vals[i] = r[i].val;
+        }
+    free(r);
+    return rc;
+}
+
+/* ---- presortedness ------------------------------------------- */
+
+int64_t or_descents(const void *keys, int64_t n, int ks) {
+    int64_t d = 0;
+    for (int64_t i = 0; i + 1 < n; i++)
+        if (load_key(keys, ks, i) > load_key(keys, ks, i + 1)) d++;
+    return d;
+}
+
+/* Maximal ascending runs: a new run starts after every descent a_i > a_{i+1}.
+ * Writes up to cap (start, len) pairs; returns the total number of runs. */
+int64_t or_asc_runs(const void *keys, int64_t n, int ks, int64_t *starts, int64_t *lens, int64_t cap) {
+    if (n <= 0) return 0;
+    int64_t cnt = 0, s = 0;
+    for (int64_t i = 0; i + 1 <= n; i++) {
+        int brk = (i + 1 == n) || (load_key(keys, ks, i) > load_key(keys, ks, i + 1));
+        if (brk) {
+            if (cnt < cap) { starts[cnt] = s; lens[cnt] = i + 1 - s; }
+            cnt++;
+            s = i + 1;
+        }
+    }
+    return cnt;
+}
+
+/* Maximal descending runs: a new run starts after every a_i < a_{i+1}
+ * (non-increasing runs, keys-only) or a_i <= a_{i+1} (strict = 1, pairs). */
+int64_t or_desc_runs(const void *keys, int64_t n, int ks, int strict, int64_t *starts, int64_t *lens, int64_t cap) {
+    if (n <= 0) return 0;
+    int64_t cnt = 0, s = 0;
+    for (int64_t i = 0; i + 1 <= n; i++) {
+        int brk = (i + 1 == n);
+        if (!brk) {
+            int64_t x = load_key(keys, ks, i), y = load_key(keys, ks, i + 1);
+            brk = strict ? (x <= y) : (x < y);
+        }
+        if (brk) {
+            if (cnt < cap) { starts[cnt] = s; lens[cnt] = i + 1 - s; }
+            cnt++;
+            s = i + 1;
+        }
+    }
+    return cnt;
+}
+
+void or_reverse(void *keys, uint32_t *vals, int64_t s, int64_t e, int ks) {
+    for (int64_t i = s, j = e - 1; i < j; i++, j--) {
+        int64_t t = load_key(keys, ks, i);
+        store_key(keys, ks, i, load_key(keys, ks, j));
+        store_key(keys, ks, j, t);
+        if (vals) { uint32_t u = vals[i]; vals[i] = vals[j]; vals[j] = u; }
+    }
+}
+
+/* ---- merging ------------------------------------------------ */
+
+void or_merge(const void *a, const uint32_t *va, int64_t na, const void *b, const uint32_t *vb, int64_t nb,
+              void *out, uint32_t *vout, int ks) {
+    int64_t i = 0, j = 0, k = 0;
+    while (i < na || j < nb) {
+        int take_a;
+        if (i >= na) take_a = 0;
+        else if (j >= nb) take_a = 1;
+        else take_a = load_key(a, ks, i) <= load_key(b, ks, j); /* A wins ties */
+        if (take_a) {
+            store_key(out, ks, k, load_key(a, ks, i));
+            if (vout) vout[k] = va ? va[i] : 0;
+            i++;
+        } else {
+            store_key(out, ks, k, load_key(b, ks, j));
+            if (vout) vout[k] = vb ? vb[j] : 0;
+            j++;
+        }
+        k++;
+    }
+}
+
+int64_t or_merge_path(const void *a, int64_t na, const void *b, int64_t nb, int64_t d, int ks) {
+    int64_t i = 0, j = 0;
+    for (int64_t k = 0; k < d; k++) {
+        int take_a;
+        if (i >= na) take_a = 0;
+        else if (j >= nb) take_a = 1;
+        else take_a = load_key(a, ks, i) <= load_key(b, ks, j);
+        if (take_a) i++; else j++;
+    }
+    return i;
+}
+
+/* ---- splitter partition (§4 (c),(d),(e),(g)) ----------------- */
+
+/* splitmix64 finalizer used as a counter-based jitter generator; the CUDA side
+ * implements the same published generator independently. */
+static uint64_t or_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* Sample position k (0 <= k < S) of segment [start, start+len): stratum k is
+ * [start + k*len/S, start + (k+1)*len/S); the sample is at a jittered offset. */
+int64_t or_sample_pos(int64_t start, int64_t len, int64_t S, int64_t k) {
+    int64_t lo = (k * len) / S, hi = ((k + 1) * len) / S;
+    int64_t w = hi - lo;
+    uint64_t h = or_mix64((uint64_t)start + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ULL);
+    return start + lo + (w > 0 ? (int64_t)(h % (uint64_t)w) : 0);
+}
+
+/* Splitters for one segment.  S = min(nbuckets * oversample, len) samples;
+ * candidates c_j = sample[((j+1)*S)/nbuckets], j = 0..nbuckets-2; duplicates
+ * removed (strictly increasing t_0 < ... < t_{m-1}); eq[i] = 1 when t_i occurs
+ * more than gamma = 2 times in the sample.  Returns m. */
+int32_t or_splitters(const void *keys, int64_t start, int64_t len, int32_t nbuckets, int32_t oversample,
+                     int ks, int64_t *spl, uint8_t *eq) {
+    int64_t S = (int64_t)nbuckets * oversample;
+    if (S > len) S = len;
+    if (S <= 0 || nbuckets < 2) return 0;
+    rec_t *smp = (rec_t *)malloc((size_t)S * sizeof(rec_t));
+    for (int64_t k = 0; k < S; k++) {
+        smp[k].key = load_key(keys, ks, or_sample_pos(start, len, S, k));
+        smp[k].val = (uint32_t)k;
+    }
+    sort_recs(smp, S);
+    int32_t m = 0;
+    for (int32_t j = 0; j + 1 < nbuckets; j++) {
+        int64_t c = smp[((int64_t)(j + 1) * S) / nbuckets].key;
+        if (m == 0 || spl[m - 1] != c) spl[m++] = c;
+    }
+    for (int32_t i = 0; i < m; i++) {
+        int64_t cnt = 0;
+        for (int64_t k = 0; k < S; k++) cnt += (smp[k].key == spl[i]);
+        eq[i] = cnt > 2; /* gamma = 2 */
+    }
+    free(smp);
+    return m;
+}
+
+void or_classify(const void *keys, int64_t n, int ks, const int64_t *spl, const uint8_t *eq, int32_t m,
+                 int32_t *bins) {
+    for (int64_t x = 0; x < n; x++) {
+        int64_t v = load_key(keys, ks, x);
+        int32_t i = 0;
+        while (i < m && spl[i] < v) i++; /* i = #{t_j < v}: splitters are increasing */
+        int32_t e = (i < m && spl[i] == v && eq[i]) ? 1 : 0;
+        bins[x] = 2 * i + e;
+    }
+}
+
+/* Stable distribution of (keys, vals) by bins into out; counts[nbins] filled. */
+int or_stable_partition(const int32_t *bins, int64_t n, int32_t nbins, const void *keys, const uint32_t *vals,
+                        void *out_keys, uint32_t *out_vals, int64_t *counts, int ks) {
+    int64_t *pos = (int64_t *)calloc((size_t)nbins + 1, sizeof(int64_t));
+    if (!pos) return -1;
+    for (int32_t b = 0; b < nbins; b++) counts[b] = 0;
+    for (int64_t x = 0; x < n; x++) counts[bins[x]]++;
+    for (int32_t b = 0; b < nbins; b++) pos[b + 1] = pos[b] + counts[b];
+    for (int64_t x = 0; x < n; x++) {
+        int64_t p = pos[bins[x]]++;
+        store_key(out_keys, ks, p, load_key(keys, ks, x));
+        if (out_vals) out_vals[p] = vals ? vals[x] : (uint32_t)x;
+    }
+    free(pos);
+    return 0;
+}
+
+/* ---- counts for sampled checks at sizes where a full oracle sort is too slow --- */
+
+int64_t or_count(const void *keys, int64_t n, int ks, int64_t v, int64_t *le) {
+    int64_t lt = 0, l = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t x = load_key(keys, ks, i);
+        lt += (x < v);
+        l += (x <= v);
+    }
+    *le = l;
+    return lt;
+}
+
+int64_t or_stable_rank(const void *keys, int64_t n, int ks, int64_t i) {
+    int64_t v = load_key(keys, ks, i), r = 0;
+    for (int64_t j = 0; j < n; j++) {
+        int64_t x = load_key(keys, ks, j);
+        r += (x < v) || (x == v && j < i);
+    }
+    return r;
+}

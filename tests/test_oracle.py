@@ -1,0 +1,327 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each check ties the oracle to something other than itself: brute force over
+tiny inputs, the stable-rank definition, a library routine for
+special cases (Python's stable `sorted`, numpy searchsorted), closed forms of
+the paper's constructions, and the paper's worked example
+ stored under tests/golden/.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import gen
+
+
+def _golden(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- brute force
+
+@pytest.mark.parametrize("n", range(0, 9))
+def test_all_permutations_sort_to_identity(n):
+    """north star: brute force over all permutations of n <= 8."""
+    target = np.arange(n, dtype=np.int32)
+    for p in itertools.permutations(range(n)):
+        out = oracle.sort_keys(np.array(p, dtype=np.int32))
+        assert np.array_equal(out, target), p
+
+
+def _stable_positions(keys):
+    """position(i) = #{j: k_j < k_i} + #{j < i: k_j = k_i}."""
+    n = len(keys)
+    return [sum(1 for j in range(n) if keys[j] < keys[i] or (keys[j] == keys[i] and j < i)) for i in range(n)]
+
+
+@pytest.mark.parametrize("n", range(1, 9))
+def test_all_ternary_sequences_stable_rank(n):
+    """Every sequence over {0,1,2} of length <= 8 with payload = index: the
+    oracle's output places element i at its stable rank."""
+    for seq in itertools.product(range(3), repeat=n):
+        k = np.array(seq, dtype=np.int64)
+        ok, ov = oracle.sort_pairs(k, np.arange(n, dtype=np.uint32))
+        pos = _stable_positions(seq)
+        expect_v = np.empty(n, np.uint32)
+        for i, p in enumerate(pos):
+            expect_v[p] = i
+        assert np.array_equal(ov, expect_v), seq
+        assert np.array_equal(ok, k[expect_v]), seq
+
+
+@pytest.mark.parametrize("n", range(1, 6))
+def test_ternary_brute_force_orderings(n):
+    """Enumerate all n! orderings; exactly one is key-sorted with increasing
+    index among equal keys, and it is the oracle's output (north star)."""
+    for seq in itertools.product(range(3), repeat=n):
+        ok, ov = oracle.sort_pairs(np.array(seq, np.int32), np.arange(n, dtype=np.uint32))
+        good = [perm for perm in itertools.permutations(range(n))
+                if all(seq[perm[t]] < seq[perm[t + 1]] or (seq[perm[t]] == seq[perm[t + 1]] and perm[t] < perm[t + 1])
+                       for t in range(n - 1))]
+        assert len(good) == 1
+        assert list(ov) == list(good[0])
+
+
+# ---------------------------------------------------------------- cross-checks
+
+def _insertion_sort_pairs(keys, vals):
+    """Hand-written stable insertion sort: shift while a[j-1].key > x.key (strict)."""
+    k = list(keys)
+    v = list(vals)
+    for i in range(1, len(k)):
+        xk, xv = k[i], v[i]
+        j = i
+        while j > 0 and k[j - 1] > xk:
+            k[j], v[j] = k[j - 1], v[j - 1]
+            j -= 1
+        k[j], v[j] = xk, xv
+    return k, v
+
+
+ORDERS_SMALL = ["random", "reversed", "nearly", "few_unique", "organ_pipe", "extremes", "all_equal", "runs1024"]
+
+
+@pytest.mark.parametrize("order", ORDERS_SMALL)
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_vs_insertion_sort(order, dtype):
+    n = 1500
+    k = gen.make(order, n, dtype, config=90)
+    v = np.arange(n, dtype=np.uint32)
+    ek, ev = _insertion_sort_pairs(k.tolist(), v.tolist())
+    ok, ov = oracle.sort_pairs(k, v)
+    assert ok.tolist() == ek and ov.tolist() == ev
+    assert oracle.sort_keys(k).tolist() == ek
+
+
+@pytest.mark.parametrize("order", ORDERS_SMALL + ["few100", "alternating", "sharp_teeth"])
+def test_vs_library_stable_sort(order):
+    """Python's sorted() is a stable library sort: a special case reference."""
+    n = 100_003
+    k = gen.make(order, n, np.int32, config=91)
+    v = np.arange(n, dtype=np.uint32)
+    idx = sorted(range(n), key=lambda i: int(k[i]))
+    ok, ov = oracle.sort_pairs(k, v)
+    assert np.array_equal(ov, np.array(idx, np.uint32))
+    assert np.array_equal(ok, k[idx])
+
+
+def test_sortedness_and_multiset_by_counting():
+    n = 1_000_000
+    k = gen.make("random", n, np.int32, config=92)
+    out = oracle.sort_keys(k)
+    assert np.all(out[:-1] <= out[1:])
+    u1, c1 = np.unique(k, return_counts=True)
+    u2, c2 = np.unique(out, return_counts=True)
+    assert np.array_equal(u1, u2) and np.array_equal(c1, c2)
+
+
+# ---------------------------------------------------------------- closed forms
+
+@pytest.mark.parametrize("order", ["reversed", "nearly", "swaps_1e4", "swaps_1e1", "runs1024", "sharp_teeth", "sorted"])
+def test_constructions_sort_to_ramp(order):
+    """Reversed, k-exchange, shuffled blocks, sharp teeth are permutations of
+    0..n-1 (constructions from a sorted list)."""
+    n = 300_007
+    k = gen.make(order, n, np.int32, config=93)
+    assert np.array_equal(oracle.sort_keys(k), np.arange(n, dtype=np.int32))
+
+
+def test_few_unique_closed_form():
+    n = 200_000
+    k = gen.make("few_unique", n, np.int32, config=94)
+    vals = sorted(set(k.tolist()))
+    assert len(vals) == 10
+    expect = np.concatenate([np.full(int((k == v).sum()), v, np.int32) for v in vals])
+    assert np.array_equal(oracle.sort_keys(k), expect)
+
+
+def test_pairs_index_payload_invariants():
+    """configs[3]: payload = original index pins the stable output completely."""
+    n = 300_000
+    k = gen.make("few100", n, np.int32, config=95)
+    ok, ov = oracle.sort_pairs(k, gen.index_payload(n))
+    assert np.array_equal(np.sort(ov), np.arange(n, dtype=np.uint32))
+    assert np.array_equal(ok, k[ov])
+    same = ok[:-1] == ok[1:]
+    assert np.all(ok[:-1] <= ok[1:])
+    assert np.all(ov[:-1][same] < ov[1:][same])
+
+
+# ---------------------------------------------------------------- golden fixtures
+
+def test_F1_worked_example(golden_dir):
+    g = _golden(golden_dir, "F1_worked_example.json")
+    k = np.array(g["keys"], np.int32)
+    assert oracle.descents(k) == g["descents"] == g["run"] - 1
+    asc = oracle.asc_runs(k)
+    assert list(asc[0]) == g["asc_run_first"]
+    desc = oracle.desc_runs(k, strict=False)
+    assert list(desc[-1]) == g["desc_run_last_start_len"]
+    r = k.copy()
+    oracle.reverse(r, 5, 16)
+    assert r.tolist() == g["after_reversal_of_5_16"]
+    assert oracle.sort_keys(k).tolist() == g["sorted"]
+    a = np.array(g["merge_A"], np.int32)
+    b = np.array(g["merge_B"], np.int32)
+    for d, i in g["merge_path"].items():
+        assert oracle.merge_path(a, b, int(d)) == i
+    assert oracle.merge(a, b).tolist() == g["sorted"]
+
+
+@pytest.mark.parametrize("name", ["F2_pairs_find_run.json", "F3_organ_pipe_ties.json", "F6_all_equal_pairs.json"])
+def test_pair_fixtures(golden_dir, name):
+    g = _golden(golden_dir, name)
+    ok, ov = oracle.sort_pairs(np.array(g["keys"], np.int32), np.array(g["vals"], np.uint32))
+    assert ok.tolist() == g["sorted_keys"] and ov.tolist() == g["sorted_vals"]
+    if "asc_runs" in g:
+        k = np.array(g["keys"], np.int32)
+        assert [list(r) for r in oracle.asc_runs(k)] == g["asc_runs"]
+        assert [list(r) for r in oracle.desc_runs(k, strict=True)] == g["desc_runs_strict"]
+        assert [list(r) for r in oracle.desc_runs(k, strict=False)] == g["desc_runs_nonstrict"]
+
+
+@pytest.mark.parametrize("name", ["F4_bsd_adversarial.json", "F5_signed_extremes.json"])
+def test_key_fixtures(golden_dir, name):
+    g = _golden(golden_dir, name)
+    k = np.array(g["keys"], np.int32)
+    assert oracle.sort_keys(k).tolist() == g["sorted"]
+    if "descents" in g:
+        assert oracle.descents(k) == g["descents"]
+    assert gen.bsd_adversarial(3, np.int32).tolist() == _golden(golden_dir, "F4_bsd_adversarial.json")["keys"]
+
+
+def test_F7_reversed(golden_dir):
+    for n in _golden(golden_dir, "F7_reversed.json")["sizes"]:
+        k = gen.reversed_ramp(n, np.int32)
+        assert oracle.descents(k) == n - 1  # Run(A) = n
+        assert oracle.desc_runs(k, strict=True) == [(0, n)]
+        assert np.array_equal(oracle.sort_keys(k), np.arange(n, dtype=np.int32))
+
+
+# ---------------------------------------------------------------- presortedness
+
+@pytest.mark.parametrize("seed", range(20))
+def test_runs_are_maximal_monotone_partitions(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 200))
+    k = rng.integers(0, 4, n).astype(np.int32)
+    for runs, ok_pair in [(oracle.asc_runs(k), lambda x, y: x <= y),
+                          (oracle.desc_runs(k, strict=False), lambda x, y: x >= y),
+                          (oracle.desc_runs(k, strict=True), lambda x, y: x > y)]:
+        pos = 0
+        for s, l in runs:
+            assert s == pos and l >= 1
+            seg = k[s:s + l].tolist()
+            assert all(ok_pair(seg[t], seg[t + 1]) for t in range(l - 1))
+            if s + l < n:  # maximal: cannot extend by one
+                assert not ok_pair(int(k[s + l - 1]), int(k[s + l]))
+            pos += l
+        assert pos == n
+    assert len(oracle.asc_runs(k)) == oracle.descents(k) + 1  # Run(A) = D + 1
+
+
+def test_even_teeth_mono_equals_k():
+    """for k <= n/3 a k-even teeth has Mono = k; with distinct
+    values inside a tooth, its maximal monotone runs alternate direction."""
+    k = gen.even_teeth(1200, 8, np.int32)
+    d = oracle.desc_runs(k, strict=True)
+    a = oracle.asc_runs(k)
+    # 4 strictly descending teeth of 150; 4 ascending teeth that absorb the
+    # equal neighbours at tooth boundaries (1,1 and 150,150), so 150..152 long
+    assert sum(1 for _, l in d if l == 150) == 4
+    assert sorted(l for _, l in a if l >= 150) == [151, 152, 152, 152]
+
+
+# ---------------------------------------------------------------- merge / merge path
+
+@pytest.mark.parametrize("seed", range(30))
+def test_merge_is_stable_union(seed):
+    rng = np.random.default_rng(seed)
+    a = np.sort(rng.integers(0, 5, int(rng.integers(0, 40)))).astype(np.int32)
+    b = np.sort(rng.integers(0, 5, int(rng.integers(0, 40)))).astype(np.int32)
+    va = np.arange(a.size, dtype=np.uint32)
+    vb = np.arange(a.size, a.size + b.size, dtype=np.uint32)
+    out, vout = oracle.merge(a, b, va, vb)
+    # concatenation sorted stably by key == stable merge with A winning ties
+    cat = np.concatenate([a, b])
+    idx = sorted(range(cat.size), key=lambda i: int(cat[i]))
+    assert out.tolist() == cat[idx].tolist() and vout.tolist() == idx
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_merge_path_split_invariant(seed):
+    """For every diagonal d the split i (j = d - i) satisfies A[i-1] <= B[j]
+    and B[j-1] < A[i]: the set of first-d outputs (A wins ties)."""
+    rng = np.random.default_rng(100 + seed)
+    a = np.sort(rng.integers(0, 6, int(rng.integers(0, 25)))).astype(np.int64)
+    b = np.sort(rng.integers(0, 6, int(rng.integers(0, 25)))).astype(np.int64)
+    for d in range(a.size + b.size + 1):
+        i = oracle.merge_path(a, b, d)
+        j = d - i
+        assert 0 <= i <= a.size and 0 <= j <= b.size
+        if i > 0 and j < b.size:
+            assert a[i - 1] <= b[j]
+        if j > 0 and i < a.size:
+            assert b[j - 1] < a[i]
+
+
+# ---------------------------------------------------------------- partition pieces
+
+@pytest.mark.parametrize("seed", range(10))
+def test_classify_matches_searchsorted(seed):
+    rng = np.random.default_rng(seed)
+    keys = rng.integers(-50, 50, 5000).astype(np.int32)
+    spl = np.unique(rng.integers(-60, 60, int(rng.integers(1, 40)))).astype(np.int32)
+    eq = rng.integers(0, 2, spl.size).astype(np.uint8)
+    bins = oracle.classify(keys, spl, eq)
+    i = np.searchsorted(spl, keys, side="left")  # #{t < x}
+    hit = (i < spl.size) & (spl[np.minimum(i, spl.size - 1)] == keys) & (eq[np.minimum(i, spl.size - 1)] == 1)
+    assert np.array_equal(bins, 2 * i + hit)
+    # bucket order is key order: concatenating buckets in id order is sorted by bucket
+    assert np.all(np.diff(bins[np.argsort(keys, kind="stable")]) >= 0)
+
+
+def test_stable_partition_matches_stable_library_sort():
+    rng = np.random.default_rng(7)
+    n = 20000
+    keys = rng.integers(0, 1000, n).astype(np.int64)
+    bins = rng.integers(0, 37, n).astype(np.int32)
+    ok, ov, counts = oracle.stable_partition(bins, 37, keys, np.arange(n, dtype=np.uint32))
+    idx = sorted(range(n), key=lambda t: int(bins[t]))
+    assert ov.tolist() == idx and ok.tolist() == keys[idx].tolist()
+    assert counts.tolist() == np.bincount(bins, minlength=37).tolist()
+
+
+@pytest.mark.parametrize("order", ["random", "few_unique", "organ_pipe", "all_equal", "nearly"])
+def test_splitters_properties(order):
+    n = 200_000
+    k = gen.make(order, n, np.int32, config=96)
+    B, o = 256, 8
+    spl, eq = oracle.splitters(k, 0, n, B, o)
+    S = B * o
+    assert 1 <= spl.size <= B - 1
+    assert np.all(np.diff(spl.astype(np.int64)) > 0)  # strictly increasing (dedup)
+    pos = [oracle.sample_pos(0, n, S, t) for t in range(S)]
+    for t, p in enumerate(pos):  # one sample per stratum
+        assert (t * n) // S <= p < ((t + 1) * n) // S
+    smp = np.sort(k[pos])  # library sort of the sample: order statistics
+    cand = [smp[((j + 1) * S) // B] for j in range(B - 1)]
+    assert spl.tolist() == sorted(set(int(c) for c in cand))
+    for t, f in zip(spl, eq):
+        assert f == (int((smp == t).sum()) > 2)  # gamma = 2
+    if order == "few_unique":  # all 10 values become equality splitters
+        assert spl.size == 10 and eq.all()
+    if order == "all_equal":
+        assert spl.size == 1 and eq.all()
+
+
+def test_count_and_stable_rank():
+    k = np.array([5, 3, 5, 1, 3, 5], np.int64)
+    assert oracle.count(k, 3) == (1, 3)
+    assert oracle.count(k, 5) == (3, 6)
+    assert [oracle.stable_rank(k, i) for i in range(6)] == _stable_positions(k.tolist())
