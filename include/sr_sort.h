@@ -1,0 +1,164 @@
+/*
+ * sr_sort.h -- C ABI of libsr_sort.so, a B200 (sm_100a) adaptive comparison
+ * sort after H. Zhang, B. Meng, Y. Liang, "Sort Race" (arXiv 1609.04471).
+ * Citations "PAPER.md:N" refer to lines of that paper's text (§ / table /
+ * appendix given alongside).
+ *
+ * All functions are extern "C"; no C++ exception crosses the ABI.  Every
+ * pointer named keys / vals / out* is a DEVICE pointer (cudaMalloc, torch
+ * tensor data_ptr, managed memory) unless the name says host_.  `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).  Sizes are
+ * element counts.
+ *
+ * Problem statement: "comparison based, internal sorting" of large in-memory
+ * arrays with the qsort interface sort(arr, n, es, cmp)
+ * (Appendix A); the comparator is fixed to
+ * ascending signed integer order, so `dtype` replaces es+cmp.
+ *
+ * Error behaviour (all entry points): arguments are validated before any
+ * device work; on SR_ERR_INVALID_ARGUMENT / _UNSUPPORTED_DTYPE / _SIZE /
+ * _ALIGNMENT / _OUT_OF_MEMORY the caller's buffers are untouched.  A CUDA
+ * failure after the first kernel returns SR_ERR_CUDA, leaves the contents
+ * unspecified and puts the CUDA message in sr_last_error().
+ */
+#ifndef SR_SORT_H
+#define SR_SORT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SR_INT32 = 0, SR_INT64 = 1 }; /* key dtype; values are 4-byte opaque payloads */
+
+enum {
+  SR_OK = 0,
+  SR_ERR_INVALID_ARGUMENT = 1, /* NULL with n >= 2, n < 0, host pointer, overlapping keys/vals */
+  SR_ERR_UNSUPPORTED_DTYPE = 2,
+  SR_ERR_SIZE = 3,             /* n > 2^31 - 1 */
+  SR_ERR_ALIGNMENT = 4,        /* keys not aligned to the key size or vals to 4 bytes */
+  SR_ERR_OUT_OF_MEMORY = 5,    /* workspace allocation failed (buffers untouched) */
+  SR_ERR_CUDA = 6,
+  SR_ERR_INTERNAL = 7          /* planner invariant violated (reported, never silent) */
+};
+
+/* Route chosen by the planner (H3).  PAPER.md:284: quicksort unless stability
+ * or presortedness calls for mergesort. */
+enum {
+  SR_ROUTE_NONE = 0,      /* n <= 1 */
+  SR_ROUTE_SORTED = 1,    /* D = 0: is_sorted exit, no write */
+  SR_ROUTE_REVERSED = 2,  /* one descending run: reversal only */
+  SR_ROUTE_MERGE = 3,     /* natural runs + merge levels (§3, Appendix A) */
+  SR_ROUTE_PARTITION = 4, /* splitter partition with equality buckets (§4, Appendix B) */
+  SR_ROUTE_TILE = 5       /* n <= one CTA tile: tile sort only (PAPER.md:155 alpha cutoff) */
+};
+
+/* ------------------------------------------------------------------ sort */
+
+/* Sort keys[0..n) ascending in place.  dtype: SR_INT32 / SR_INT64.  keys must
+ * be aligned to the key size.  Work is enqueued on `stream`; the call blocks
+ * the host on small statistics readbacks (one for sorted / reversed /
+ * single-level inputs) and returns before the GPU finishes; synchronise the
+ * stream before reading keys.  Scratch: about n*(key bytes) + O(n/8) bytes,
+ * stream-ordered from the device memory pool, released before return.
+ * Equal keys are indistinguishable, so the result is unique. */
+int32_t sr_sort_keys(void *keys, int64_t n, int32_t dtype, void *stream);
+
+/* Stable key-value sort: keys ascending; among equal keys the input order of
+ * (key, val) pairs is kept; vals[i] travels with keys[i]
+ * and is never compared.  vals: 4-byte elements, 4-byte aligned, must not
+ * overlap keys.  Scratch about n*(key bytes + 4). */
+int32_t sr_sort_pairs(void *keys, void *vals, int64_t n, int32_t dtype, void *stream);
+
+/* End-to-end variants with HOST buffers (pinned or pageable): copies the
+ * input host->device on `stream`, sorts, copies back, and synchronises the
+ * stream before returning.  host_vals may be NULL for sr_sort_host (keys only).
+ */
+int32_t sr_sort_host(void *host_keys, void *host_vals, int64_t n, int32_t dtype, void *stream);
+
+/* ------------------------------------------------------------------ introspection */
+
+typedef struct {
+  int32_t route;            /* SR_ROUTE_* */
+  int32_t levels;           /* partition levels, or merge levels */
+  int64_t n;
+  int64_t descents;         /* D = Run(A) - 1 */
+  int64_t asc_breaks;       /* descending-run breaks */
+  int64_t long_runs;        /* long natural runs found (either direction) */
+  int64_t desc_runs_reversed;
+  int64_t equal_keys;       /* keys placed by equality buckets */
+  int64_t bytes_planned;    /* algorithmic HBM bytes of all launched kernels */
+  int64_t workspace_bytes;
+  int32_t launches;         /* kernels launched by the call */
+  int32_t host_syncs;       /* host<->device statistics readbacks */
+} sr_plan;
+
+/* Plan of the last sort call made by this host thread.  SR_OK or
+ * SR_ERR_INVALID_ARGUMENT when out is NULL. */
+int32_t sr_last_plan(sr_plan *out);
+
+const char *sr_status_string(int32_t status);
+const char *sr_last_error(void); /* thread-local; "" when none */
+
+enum {
+  SR_OPT_FORCE_ROUTE = 0, /* 0 auto, SR_ROUTE_MERGE or SR_ROUTE_PARTITION (tests, ablations) */
+  SR_OPT_PROFILE = 1,     /* 1: time every kernel with CUDA events (see sr_last_profile) */
+  SR_OPT_MERGE_ROUTE = 2  /* 0: never choose the merge route automatically */
+};
+/* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
+int32_t sr_set_option(int32_t key, int64_t value);
+
+/* With SR_OPT_PROFILE on: per-kernel names, device ms and algorithmic bytes of
+ * the last call on this thread (synchronises its stream).  Returns the number
+ * of kernels (<= cap written). */
+int32_t sr_last_profile(const char **names, float *ms, int64_t *bytes, int32_t cap);
+
+/* ------------------------------------------------------------------ step-level entry points
+ * One per hot-path row; used by the parity tests.  All are
+ * synchronous (they synchronise `stream` before returning) and take device
+ * pointers for array data and host pointers for small results. */
+
+typedef struct {
+  int64_t n, descents, asc_breaks;
+  int64_t n_asc_runs, n_desc_runs, asc_cover, desc_cover;
+} sr_presort_stats;
+
+/* H1: presortedness scan with tile size `tile` (power of two, 1024..65536);
+ * runs of length >= tile are reported.  strict = 1 uses strictly descending
+ * runs (pairs), 0 non-increasing runs (keys).  host_runs (may be NULL): up to
+ * cap rows of {start, len, dir(0 asc / 1 desc), 0}; asc runs first. */
+int32_t sr_presort_scan(const void *keys, int64_t n, int32_t dtype, int32_t strict, int32_t tile,
+                        sr_presort_stats *host_stats, int64_t *host_runs, int64_t cap, void *stream);
+
+/* H2: reverse keys[s..e) (and vals when non-NULL) in place. */
+int32_t sr_reverse_range(void *keys, void *vals, int64_t n, int32_t dtype, int64_t s, int64_t e, void *stream);
+
+/* H4: stable sort of every tile [t*tile, (t+1)*tile) independently, tile <= 8192. */
+int32_t sr_tile_sort(void *keys, void *vals, int64_t n, int32_t dtype, int32_t tile, void *stream);
+
+/* H5: merge-path split i(d) = #A among the first d outputs of the stable
+ * merge of sorted a[0..na) and b[0..nb) (A wins ties), for host_diags[0..nd). */
+int32_t sr_merge_path(const void *a, int64_t na, const void *b, int64_t nb, int32_t dtype,
+                      const int64_t *host_diags, int64_t *host_out, int64_t nd, void *stream);
+
+/* H6: stable merge of sorted (a, va) and (b, vb) into (out, vout); va/vb/vout
+ * may be NULL for keys only. */
+int32_t sr_merge(const void *a, const void *va, int64_t na, const void *b, const void *vb, int64_t nb,
+                 void *out, void *vout, int32_t dtype, void *stream);
+
+/* H7: splitters of keys[0..n) for nbuckets (power of two, 2..1024) buckets:
+ * host_spl[0..m) (int64), host_eq[0..m) equality flags; returns m via *m. */
+int32_t sr_splitters(const void *keys, int64_t n, int32_t dtype, int32_t nbuckets, int64_t *host_spl,
+                     uint8_t *host_eq, int32_t *m, void *stream);
+
+/* H8-H10: one partition level: splitters (as sr_splitters), bucket histogram,
+ * count-matrix scan and stable scatter of (keys, vals) into (out, vout) in
+ * bucket order.  Equality buckets' keys are written too (filled) so that out
+ * is the complete stable partition.  host_counts[0..2*nbuckets+1). */
+int32_t sr_partition_level(const void *keys, const void *vals, int64_t n, int32_t dtype, int32_t nbuckets,
+                           void *out, void *vout, int64_t *host_counts, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SR_SORT_H */

@@ -1,0 +1,257 @@
+// presort.cuh -- H1 presortedness scan (K1), run resolve (K2), H2 run reversal (K3).
+//
+// H1 follows §4(f) "If n >= alpha, test if the array is already sorted; if
+// yes, exit" (Appendix B is_sorted PAPER.md:385) and §3(a)
+// scanning for runs (Appendix A).  One read of
+// the keys yields D = |{i : a_i > a_{i+1}}| = Run(A) - 1, the
+// descending-run breaks, and the long (>= L_min) natural runs of either
+// direction.  With L_min >= tile size a long run always touches a tile edge,
+// so per-tile first/last break positions are enough to recover every long run.
+#pragma once
+#include "common.cuh"
+#include "types.cuh"
+
+namespace sr {
+
+// Branchless lower_bound over the padded splitter array (P2-1 entries, pads =
+// +inf): i = #{t_j < x}.  Bucket id 2i+1 when x equals an equality splitter
+// (3-way split, switched on per splitter by the gamma test
+// of PAPER.md:168), else 2i.
+template <typename K>
+__device__ __forceinline__ int classify_key(K x, const K* spl, const uint8_t* eqf, int m, int P2) {
+  int i = 0;
+  for (int step = P2 >> 1; step > 0; step >>= 1)
+    if (spl[i + step - 1] < x) i += step;
+  return 2 * i + ((i < m && spl[i] == x && eqf[i]) ? 1 : 0);
+}
+
+__host__ __device__ __forceinline__ int pow2_above(int m) {  // smallest power of 2 >= m+1
+  int p = 1;
+  while (p < m + 1) p <<= 1;
+  return p;
+}
+
+template <typename K>
+__device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_spl, uint8_t* s_eq,
+                                                    int& P2) {
+  P2 = pow2_above(m);
+  for (int i = threadIdx.x; i < P2 - 1; i += blockDim.x) {
+    s_spl[i] = i < m ? spl[i] : KeyTraits<K>::max_key();
+    s_eq[i] = i < m ? eqf[i] : 0;
+  }
+}
+
+// Warp-aggregated shared-memory histogram increment.
+__device__ __forceinline__ void hist_add(uint32_t* hist, int bin, bool valid) {
+  unsigned mask = __ballot_sync(0xffffffffu, valid);
+  if (valid) {
+    unsigned peers = __match_any_sync(mask, bin);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+  }
+}
+
+// K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
+// break rule: a_i <= a_{i+1} (pairs: only strictly descending runs may be
+// reversed, "the reversely sorted subsequence cannot contain equal
+// elements") or a_i < a_{i+1} (keys-only: non-increasing runs).
+// FUSE additionally classifies every key against the level-1 splitters and
+// writes the tile's bucket histogram (H8 fused into the H1 read).
+template <typename K, bool STRICT, bool FUSE, int NT>
+__global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys, int64_t n, int tile,
+                                                      TileSummary* __restrict__ sums, const K* __restrict__ spl,
+                                                      const uint8_t* __restrict__ eqf, const int* __restrict__ mcount,
+                                                      uint32_t* __restrict__ mat, int nbins, int G) {
+  constexpr int U = 4;
+  __shared__ K s_spl[FUSE ? kMaxBuckets : 1];
+  __shared__ uint8_t s_eq[FUSE ? kMaxBuckets : 1];
+  __shared__ uint32_t s_hist[FUSE ? kMaxBins : 1];
+  __shared__ int32_t s_red[NT / 32 + 1];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * tile;
+  const int64_t t1 = t0 + tile < n ? t0 + tile : n;
+  int m = 0, P2 = 1;
+  if (FUSE) {
+    m = mcount[0];
+    load_splitters_smem(spl, eqf, m, s_spl, s_eq, P2);
+    for (int b = tid; b < nbins; b += NT) s_hist[b] = 0;
+    __syncthreads();
+  }
+  int cd = 0, ca = 0;
+  int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
+  for (int64_t base = t0; base < t1; base += NT * U) {
+    K x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int64_t i = base + u * NT + tid;
+      x[u] = i < n ? keys[i] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int64_t i = base + u * NT + tid;
+      K y = __shfl_down_sync(0xffffffffu, x[u], 1);
+      if (lane == 31 && i + 1 < n) y = keys[i + 1];
+      if (i < t1 && i + 1 < n) {
+        if (y < x[u]) { cd++; fd = min(fd, (int)i); ld = max(ld, (int)i); }
+        bool brk = STRICT ? !(y < x[u]) : (x[u] < y);
+        if (brk) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }
+      }
+      if (FUSE) {
+        bool valid = i < t1;
+        int bin = valid ? classify_key<K>(x[u], s_spl, s_eq, m, P2) : 0;
+        hist_add(s_hist, bin, valid);
+      }
+    }
+  }
+  cd = block_reduce_sum<NT>(cd, s_red);
+  ca = block_reduce_sum<NT>(ca, s_red);
+  fd = block_reduce_min<NT>(fd, s_red);
+  ld = block_reduce_max<NT>(ld, s_red);
+  fa = block_reduce_min<NT>(fa, s_red);
+  la = block_reduce_max<NT>(la, s_red);
+  if (tid == 0) {
+    TileSummary s;
+    s.ndesc = cd; s.nab = ca; s.fdesc = fd; s.ldesc = ld; s.fab = fa; s.lab = la; s.pad0 = 0; s.pad1 = 0;
+    sums[blockIdx.x] = s;
+  }
+  if (FUSE) {
+    __syncthreads();
+    for (int b = tid; b < nbins; b += NT) mat[(int64_t)b * G + blockIdx.x] = s_hist[b];
+  }
+}
+
+// K2: resolve tile summaries into D, the long runs of both directions and
+// their covers (single CTA; loops over the tiles with a carried prefix).
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ keys, int64_t n,
+                                                         const TileSummary* __restrict__ sums, int G, int64_t lmin,
+                                                         RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
+                                                         DevStats* __restrict__ st) {
+  __shared__ int32_t s_incl[2][NT];
+  __shared__ int64_t s_red64[NT / 32 + 1];
+  __shared__ int32_t s_red[NT / 32 + 1];
+  const int tid = threadIdx.x;
+  int32_t carryD = -1, carryA = -1;
+  int64_t D = 0, A = 0, nasc = 0, ndsc = 0, covA = 0, covD = 0;
+  for (int c0 = 0; c0 < G; c0 += NT) {
+    const int t = c0 + tid;
+    TileSummary s;
+    if (t < G) s = sums[t];
+    else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; }
+    D += s.ndesc;
+    A += s.nab;
+    int32_t iD = block_inclusive_max<NT>(s.ldesc, s_red, -1);
+    int32_t iA = block_inclusive_max<NT>(s.lab, s_red, -1);
+    s_incl[0][tid] = iD;
+    s_incl[1][tid] = iA;
+    __syncthreads();
+    int32_t prevD = tid > 0 ? s_incl[0][tid - 1] : -1;
+    int32_t prevA = tid > 0 ? s_incl[1][tid - 1] : -1;
+    prevD = max(prevD, carryD);
+    prevA = max(prevA, carryA);
+    // ascending run ending at this tile's first descent
+    int64_t lenA = (s.ndesc > 0) ? (int64_t)s.fdesc - prevD : 0;
+    int fA = (t < G && s.ndesc > 0 && lenA >= lmin) ? 1 : 0;
+    int64_t lenDd = (s.nab > 0) ? (int64_t)s.fab - prevA : 0;
+    int fDd = (t < G && s.nab > 0 && lenDd >= lmin) ? 1 : 0;
+    int32_t totA, totD;
+    int32_t exA = block_exclusive_sum<NT>(fA, s_red, &totA);
+    int32_t exD = block_exclusive_sum<NT>(fDd, s_red, &totD);
+    if (fA) {
+      RunDesc r;
+      r.start = prevD + 1; r.len = lenA;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
+      asc[nasc + exA] = r;
+    }
+    if (fDd) {
+      RunDesc r;
+      r.start = prevA + 1; r.len = lenDd;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
+      desc[ndsc + exD] = r;
+    }
+    covA += fA ? lenA : 0;
+    covD += fDd ? lenDd : 0;
+    nasc += totA;
+    ndsc += totD;
+    carryD = max(carryD, s_incl[0][NT - 1]);
+    carryA = max(carryA, s_incl[1][NT - 1]);
+    __syncthreads();
+  }
+  D = block_reduce_sum<NT>(D, s_red64);
+  A = block_reduce_sum<NT>(A, s_red64);
+  covA = block_reduce_sum<NT>(covA, s_red64);
+  covD = block_reduce_sum<NT>(covD, s_red64);
+  if (tid == 0) {
+    // final runs after the last break
+    int64_t lastLen = n - 1 - (int64_t)carryD;
+    if (n > 0 && lastLen >= lmin) {
+      RunDesc r;
+      r.start = carryD + 1; r.len = lastLen;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+      asc[nasc++] = r;
+      covA += lastLen;
+    }
+    int64_t lastLenD = n - 1 - (int64_t)carryA;
+    if (n > 0 && lastLenD >= lmin) {
+      RunDesc r;
+      r.start = carryA + 1; r.len = lastLenD;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+      desc[ndsc++] = r;
+      covD += lastLenD;
+    }
+    st->n = n;
+    st->descents = D;
+    st->asc_breaks = A;
+    st->n_asc_runs = nasc;
+    st->n_desc_runs = ndsc;
+    st->asc_cover = covA;
+    st->desc_cover = covD;
+  }
+}
+
+// K3: in-place reversal of ranges [start, start+len) (H2; PAPER.md:93 and
+// Appendix A reverse()).  Block b maps to (range, chunk)
+// through the host-built chunk prefix; each chunk swaps NT*U mirrored pairs
+// with coalesced front and back accesses.
+template <typename K, bool HAS_V, int NT>
+__global__ void __launch_bounds__(NT) k_reverse(K* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                 const RunDesc* __restrict__ ranges,
+                                                 const int64_t* __restrict__ chunk_prefix, int nranges) {
+  constexpr int U = 8;
+  constexpr int CH = NT * U;
+  __shared__ int s_r;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = nranges - 1;
+    while (lo < hi) {  // last r with chunk_prefix[r] <= blockIdx.x
+      int mid = (lo + hi + 1) >> 1;
+      if (chunk_prefix[mid] <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    s_r = lo;
+  }
+  __syncthreads();
+  const int r = s_r;
+  const int64_t s = ranges[r].start, len = ranges[r].len;
+  const int64_t half = len / 2;
+  const int64_t c0 = ((int64_t)blockIdx.x - chunk_prefix[r]) * CH;
+  K a[U], b[U];
+  uint32_t va[U], vb[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    int64_t p = c0 + u * NT + threadIdx.x;
+    if (p < half) {
+      a[u] = keys[s + p];
+      b[u] = keys[s + len - 1 - p];
+      if (HAS_V) { va[u] = vals[s + p]; vb[u] = vals[s + len - 1 - p]; }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    int64_t p = c0 + u * NT + threadIdx.x;
+    if (p < half) {
+      keys[s + p] = b[u];
+      keys[s + len - 1 - p] = a[u];
+      if (HAS_V) { vals[s + p] = vb[u]; vals[s + len - 1 - p] = va[u]; }
+    }
+  }
+}
+
+}  // namespace sr

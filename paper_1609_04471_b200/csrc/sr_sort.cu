@@ -1,0 +1,932 @@
+// sr_sort.cu -- host planner (H3, H12) and C ABI of libsr_sort.so.
+//
+// Route choice follows the paper's recommendation: "quicksort,
+// especially our hybrid quicksort, if stable sorting is not required. Only
+// when ... the input contains some kind of presortedness and the memory is not
+// a concern, then mergesort".  Here both routes are stable, so the planner
+// picks by a byte-cost model over the measured run statistics:
+//   D == 0                -> SORTED (is_sorted exit)
+//   no descending breaks  -> REVERSED (one reversal, PAPER.md:93 / :172)
+//   long natural runs     -> MERGE if its simulated bytes beat PARTITION
+//   otherwise             -> PARTITION (levels until every bucket <= kCap)
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sr_sort.h"
+#include "merge.cuh"
+#include "partition.cuh"
+#include "presort.cuh"
+
+using namespace sr;
+
+namespace {
+
+// ------------------------------------------------------------------ options / thread state
+int g_force_route = 0;
+int g_profile = 0;
+int g_merge_route = 1;
+
+struct ProfEntry {
+  const char* name;
+  cudaEvent_t a, b;
+  int64_t bytes;
+};
+
+struct ThreadState {
+  sr_plan plan{};
+  std::string err;
+  std::vector<ProfEntry> prof;
+  cudaStream_t prof_stream = nullptr;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  ~ThreadState() {
+    for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+thread_local ThreadState t_state;
+
+struct SrError {
+  int32_t code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int32_t code, const std::string& msg) { throw SrError{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); fail(SR_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e)); }
+  if (e != cudaSuccess) fail(SR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* pinned(size_t bytes) {
+  ThreadState& ts = t_state;
+  if (ts.pinned_bytes < bytes) {
+    if (ts.pinned) cudaFreeHost(ts.pinned);
+    size_t sz = std::max<size_t>(bytes, 1 << 20);
+    check_cuda(cudaHostAlloc(&ts.pinned, sz, cudaHostAllocDefault), "cudaHostAlloc");
+    ts.pinned_bytes = sz;
+  }
+  return ts.pinned;
+}
+
+std::once_flag g_pool_once;
+void init_pool() {
+  std::call_once(g_pool_once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  });
+}
+
+template <typename T>
+T ceil_div(T a, T b) { return (a + b - 1) / b; }
+
+int64_t pow2ceil(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// ------------------------------------------------------------------ per-call context
+struct Ctx {
+  cudaStream_t st;
+  sr_plan& plan;
+  std::vector<void*> allocs;
+  bool profile;
+  explicit Ctx(cudaStream_t s) : st(s), plan(t_state.plan), profile(g_profile != 0) {
+    plan = sr_plan{};
+    if (profile) {
+      for (auto& e : t_state.prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+      t_state.prof.clear();
+      t_state.prof_stream = s;
+    }
+  }
+  ~Ctx() {
+    for (void* p : allocs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  T* alloc(int64_t count) {
+    if (count <= 0) count = 1;
+    void* p = nullptr;
+    size_t bytes = (size_t)count * sizeof(T);
+    bytes = (bytes + 255) & ~size_t(255);
+    check_cuda(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+    allocs.push_back(p);
+    plan.workspace_bytes += (int64_t)bytes;
+    return reinterpret_cast<T*>(p);
+  }
+  template <typename F>
+  void launch(const char* name, int64_t bytes, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profile) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+    f();
+    check_cuda(cudaGetLastError(), name);
+    if (profile) {
+      cudaEventRecord(b, st);
+      t_state.prof.push_back({name, a, b, bytes});
+    }
+    plan.launches++;
+    plan.bytes_planned += bytes;
+  }
+  void memset0(void* p, size_t bytes) { check_cuda(cudaMemsetAsync(p, 0, bytes, st), "cudaMemsetAsync"); }
+  template <typename T>
+  void upload(T* dst, const std::vector<T>& src) {
+    if (src.empty()) return;
+    check_cuda(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+  }
+  // Readback of `bytes` from device into pinned memory + synchronise (the planner's host sync).
+  void* readback(const void* dev, size_t bytes) {
+    void* h = pinned(bytes);
+    check_cuda(cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, st), "readback");
+    check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    plan.host_syncs++;
+    return h;
+  }
+};
+
+template <typename Kern>
+void set_smem(Kern k, size_t bytes) {
+  static_assert(sizeof(Kern) > 0, "");
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// ------------------------------------------------------------------ tunables
+constexpr int kScanNT = 256, kScanIPT = 16;              // K9
+constexpr int kFinNT = 512, kFinVT = 16;                 // K11 (kCap = 8192)
+constexpr int kSplNT = 512, kSplVT = 16;                 // K7 (S <= 8192)
+constexpr int kScatNT = 256, kScatVT = 16;               // K10
+constexpr int kMergeNT = 256, kMergeVT = 16;             // K6
+constexpr int kMergeNV = kMergeNT * kMergeVT;
+static_assert(kFinNT * kFinVT == kCap, "finishing tile must equal kCap");
+
+int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
+  int64_t t = pow2ceil(std::max<int64_t>(1, n / 512));
+  return std::min<int64_t>(65536, std::max<int64_t>(8192, t));
+}
+int choose_buckets(int64_t len) {
+  int64_t b = pow2ceil(ceil_div<int64_t>(len, 2048));
+  return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
+}
+
+// ------------------------------------------------------------------ the sort
+template <typename K, bool HAS_V>
+struct Sorter {
+  Ctx& c;
+  K* keys;
+  uint32_t* vals;
+  int64_t n;
+  K* wk = nullptr;
+  uint32_t* wv = nullptr;
+  static constexpr int64_t kw = sizeof(K);
+  static constexpr int64_t vw = HAS_V ? 4 : 0;
+
+  Sorter(Ctx& ctx, K* k, uint32_t* v, int64_t nn) : c(ctx), keys(k), vals(v), n(nn) {}
+
+  void ensure_ws() {
+    if (!wk) {
+      wk = c.alloc<K>(n);
+      if (HAS_V) wv = c.alloc<uint32_t>(n);
+    }
+  }
+
+  // ---- finishing kernel over a device item list
+  void finish(const Item* items, const int64_t* count_ptr, int64_t begin, int64_t max_items, int64_t bytes) {
+    if (max_items <= 0) return;
+    using BS = BlockSort<K, HAS_V, kFinNT, kFinVT>;
+    size_t smem = sizeof(K) * BS::KEYS_SMEM + (HAS_V ? 4 * BS::VALS_SMEM : 0);
+    auto kern = k_finish<K, HAS_V, kFinNT, kFinVT>;
+    set_smem(kern, smem);
+    int grid = (int)std::min<int64_t>(max_items, 148 * 8);
+    K* kk = keys;
+    uint32_t* vv = vals;
+    const K* wkk = wk;
+    const uint32_t* wvv = wv;
+    c.launch("finish", bytes, [&] { kern<<<grid, kFinNT, smem, c.st>>>(items, count_ptr, begin, kk, vv, wkk, wvv); });
+  }
+
+  void reverse_ranges(const std::vector<RunDesc>& ranges) {
+    if (ranges.empty()) return;
+    constexpr int NT = 256;
+    constexpr int64_t CH = NT * 8;
+    std::vector<int64_t> pre(ranges.size());
+    int64_t tot = 0, bytes = 0;
+    for (size_t i = 0; i < ranges.size(); i++) {
+      pre[i] = tot;
+      tot += std::max<int64_t>(1, ceil_div<int64_t>(ranges[i].len / 2, CH));
+      bytes += 2 * ranges[i].len * (kw + vw);
+    }
+    RunDesc* d_r = c.alloc<RunDesc>(ranges.size());
+    int64_t* d_p = c.alloc<int64_t>(pre.size());
+    c.upload(d_r, ranges);
+    c.upload(d_p, pre);
+    K* kk = keys;
+    uint32_t* vv = vals;
+    int nr = (int)ranges.size();
+    c.launch("reverse", bytes, [&] { k_reverse<K, HAS_V, NT><<<(unsigned)tot, NT, 0, c.st>>>(kk, vv, d_r, d_p, nr); });
+  }
+
+  // ---- one partition level over `segs` of buffer src (0 primary, 1 ws); writes the other buffer.
+  struct LevelOut {
+    DevStats st;
+    std::vector<OvfSeg> ovf;
+  };
+
+  // Level-1 state prepared before the route decision (fused with H1).
+  struct Level {
+    std::vector<SegDesc> segs;
+    SegDesc* d_segs = nullptr;
+    int* d_chunk_seg = nullptr;
+    K* d_spl = nullptr;
+    uint8_t* d_eq = nullptr;
+    int* d_m = nullptr;
+    uint32_t* d_mat = nullptr;
+    int64_t mat_entries = 0;
+    int64_t total_chunks = 0;
+    int64_t chunk_size = 0;
+    int64_t total_bins = 0;
+    DevStats* d_st = nullptr;
+    unsigned long long* d_status = nullptr;
+    int* d_tile_counter = nullptr;
+    int64_t scan_tiles = 0;
+    Item* d_items = nullptr;
+    OvfSeg* d_ovf = nullptr;
+    int src = 0;
+  };
+
+  void level_alloc(Level& L, const std::vector<OvfSeg>& parts, int64_t chunk_size, int src, int forced_b = 0) {
+    L.src = src;
+    L.chunk_size = chunk_size;
+    int64_t chunk_base = 0, mat = 0, lp = 0, bins = 0;
+    std::vector<int> chunk_seg;
+    for (size_t s = 0; s < parts.size(); s++) {
+      SegDesc d;
+      d.start = parts[s].start;
+      d.len = parts[s].len;
+      d.nbuckets = forced_b ? forced_b : choose_buckets(d.len);
+      d.nbins = 2 * d.nbuckets + 1;
+      d.nchunks = (int32_t)ceil_div<int64_t>(d.len, chunk_size);
+      d.chunk_base = (int32_t)chunk_base;
+      d.mat_base = mat;
+      d.len_prefix = lp;
+      for (int g = 0; g < d.nchunks; g++) chunk_seg.push_back((int)s);
+      chunk_base += d.nchunks;
+      mat += (int64_t)d.nbins * d.nchunks;
+      lp += d.len;
+      bins += d.nbins;
+      L.segs.push_back(d);
+    }
+    L.total_chunks = chunk_base;
+    L.mat_entries = mat;
+    L.total_bins = bins;
+    const int64_t S = (int64_t)parts.size();
+    L.d_segs = c.alloc<SegDesc>(S);
+    L.d_chunk_seg = c.alloc<int>(chunk_base);
+    L.d_spl = c.alloc<K>(S * kMaxBuckets);
+    L.d_eq = c.alloc<uint8_t>(S * kMaxBuckets);
+    L.d_m = c.alloc<int>(S);
+    L.d_mat = c.alloc<uint32_t>(mat);
+    L.scan_tiles = ceil_div<int64_t>(mat, kScanNT * kScanIPT);
+    // control block: stats | tile counter | scan status
+    size_t ctrl = sizeof(DevStats) + 256 + sizeof(unsigned long long) * (size_t)L.scan_tiles;
+    unsigned char* cb = c.alloc<unsigned char>((int64_t)ctrl);
+    c.memset0(cb, ctrl);
+    L.d_st = reinterpret_cast<DevStats*>(cb);
+    L.d_tile_counter = reinterpret_cast<int*>(cb + sizeof(DevStats));
+    L.d_status = reinterpret_cast<unsigned long long*>(cb + sizeof(DevStats) + 256);
+    L.d_items = c.alloc<Item>(bins);
+    L.d_ovf = c.alloc<OvfSeg>(bins);
+    c.upload(L.d_segs, L.segs);
+    c.upload(L.d_chunk_seg, chunk_seg);
+  }
+
+  const K* buf_k(int b) const { return b ? wk : keys; }
+  const uint32_t* buf_v(int b) const { return b ? wv : vals; }
+
+  void level_splitters(Level& L) {
+    using BS = BlockSort<K, false, kSplNT, kSplVT>;
+    size_t smem = sizeof(K) * BS::KEYS_SMEM;
+    auto kern = k_splitters<K, kSplNT, kSplVT>;
+    set_smem(kern, smem);
+    const K* src = buf_k(L.src);
+    int S = (int)L.segs.size();
+    int64_t bytes = 0;
+    for (auto& s : L.segs) bytes += std::min<int64_t>(s.len, (int64_t)s.nbuckets * kOversample) * kw;
+    c.launch("splitters", bytes,
+             [&] { kern<<<S, kSplNT, smem, c.st>>>(src, L.d_segs, kOversample, L.d_spl, L.d_eq, L.d_m); });
+  }
+
+  void level_count(Level& L) {
+    const K* src = buf_k(L.src);
+    int64_t keys_in = 0;
+    for (auto& s : L.segs) keys_in += s.len;
+    c.launch("count", keys_in * kw + L.mat_entries * 4, [&] {
+      k_count<K, 256><<<(unsigned)L.total_chunks, 256, 0, c.st>>>(src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl,
+                                                                 L.d_eq, L.d_m, L.d_mat);
+    });
+  }
+
+  void level_scan_plan(Level& L) {
+    int64_t cnt = L.mat_entries;
+    c.launch("scan", cnt * 8, [&] {
+      k_scan_u32<kScanNT, kScanIPT><<<(unsigned)L.scan_tiles, kScanNT, 0, c.st>>>(L.d_mat, cnt, L.d_status,
+                                                                                 L.d_tile_counter);
+    });
+    int S = (int)L.segs.size();
+    int dst = 1 - L.src;
+    c.launch("plan", L.total_bins * 8, [&] {
+      k_plan<K, 1024><<<S, 1024, 0, c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_ovf, L.d_st);
+    });
+  }
+
+  void level_scatter(Level& L, const DevStats& hs) {
+    const bool skip = !HAS_V && hs.noneq_total == 0;  // keys-only, everything in equality buckets
+    if (skip) return;
+    using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
+    size_t smem = sizeof(SM);
+    auto kern = k_scatter<K, HAS_V, kScatNT, kScatVT>;
+    set_smem(kern, smem);
+    ensure_ws();
+    const K* sk = buf_k(L.src);
+    const uint32_t* sv = buf_v(L.src);
+    K* dk = L.src ? keys : wk;
+    uint32_t* dv = L.src ? vals : wv;
+    int64_t keys_in = 0;
+    for (auto& s : L.segs) keys_in += s.len;
+    int64_t bytes = keys_in * (kw + vw) + hs.noneq_total * kw + keys_in * vw + L.mat_entries * 4;
+    c.launch("scatter", bytes, [&] {
+      kern<<<(unsigned)L.total_chunks, kScatNT, smem, c.st>>>(sk, sv, dk, dv, L.d_segs, L.d_chunk_seg, L.chunk_size,
+                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat);
+    });
+  }
+
+  void level_finish(Level& L, const DevStats& hs) {
+    // sort items read+write the range buckets; fills write keys (+ move vals)
+    int64_t bytes = 2 * (hs.noneq_total - hs.ovf_keys) * (kw + vw) + hs.eq_keys * kw + (L.src == 0 ? 2 : 0) * hs.eq_keys * vw;
+    finish(L.d_items, &L.d_st->n_items, 0, hs.n_items, bytes);
+    c.plan.equal_keys += hs.eq_keys;
+  }
+
+  // Partition levels >= 2 (segments from the previous level's oversized buckets).
+  void run_levels(std::vector<OvfSeg> parts, int src) {
+    int level = 2;
+    while (!parts.empty()) {
+      if (level > 12) fail(SR_ERR_INTERNAL, "partition did not converge");
+      int64_t tot = 0;
+      for (auto& p : parts) tot += p.len;
+      int64_t cs = std::min<int64_t>(65536, std::max<int64_t>(4096, pow2ceil(std::max<int64_t>(1, tot / 512))));
+      Level L;
+      level_alloc(L, parts, cs, src);
+      level_splitters(L);
+      level_count(L);
+      level_scan_plan(L);
+      DevStats hs = *reinterpret_cast<DevStats*>(c.readback(L.d_st, sizeof(DevStats)));
+      if (hs.error) fail(SR_ERR_INTERNAL, "plan kernel inconsistency");
+      std::vector<OvfSeg> next;
+      if (hs.n_ovf > 0) {
+        const OvfSeg* h = reinterpret_cast<const OvfSeg*>(c.readback(L.d_ovf, sizeof(OvfSeg) * hs.n_ovf));
+        next.assign(h, h + hs.n_ovf);
+        for (auto& o : next)
+          for (auto& p : parts)
+            if (o.start == p.start && o.len == p.len) fail(SR_ERR_INTERNAL, "partition made no progress");
+      }
+      level_scatter(L, hs);
+      level_finish(L, hs);
+      c.plan.levels = level;
+      parts.swap(next);
+      src = 1 - src;
+      level++;
+    }
+  }
+
+  // ---- merge route (natural runs, reversal, tile sort, half-down merge levels)
+  struct Seg {
+    int64_t start, len;
+    int kind;  // 0 asc run, 1 desc run (reversed), 2 gap tile
+  };
+
+  // Simulated half-down merge tree (Appendix A).
+  struct Node {
+    int64_t start, len;
+    int left = -1, right = -1;
+    int depth = 0;
+    int buf = 0;
+  };
+
+  static std::vector<Node> half_down_tree(const std::vector<std::pair<int64_t, int64_t>>& runs, int& root) {
+    std::vector<Node> nodes;
+    std::vector<int> stack;
+    auto merge_top = [&]() {
+      int b = stack.back();
+      stack.pop_back();
+      int a = stack.back();
+      stack.pop_back();
+      Node m;
+      m.start = nodes[a].start;
+      m.len = nodes[a].len + nodes[b].len;
+      m.left = a;
+      m.right = b;
+      m.depth = 1 + std::max(nodes[a].depth, nodes[b].depth);
+      nodes.push_back(m);
+      stack.push_back((int)nodes.size() - 1);
+    };
+    for (auto& r : runs) {
+      Node l;
+      l.start = r.first;
+      l.len = r.second;
+      nodes.push_back(l);
+      stack.push_back((int)nodes.size() - 1);
+      // "merge two runs if the current run > 1/2 of its predecessor"
+      while (stack.size() > 1 && nodes[stack.back()].len > (nodes[stack[stack.size() - 2]].len >> 1)) merge_top();
+    }
+    while (stack.size() > 1) merge_top();  // "merge all runs into one, from last to first"
+    root = stack.empty() ? -1 : stack.back();
+    return nodes;
+  }
+
+  // bytes of the merge schedule (merges + harmonising copies + final copy)
+  static int64_t schedule_bytes(std::vector<Node>& nodes, int root, int64_t elem_bytes) {
+    int64_t b = 0;
+    std::vector<int> order(nodes.size());
+    for (size_t i = 0; i < nodes.size(); i++) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return nodes[x].depth < nodes[y].depth; });
+    for (int i : order) {
+      Node& nd = nodes[i];
+      if (nd.left < 0) { nd.buf = 0; continue; }
+      Node& A = nodes[nd.left];
+      Node& B = nodes[nd.right];
+      int in = A.buf;
+      if (A.buf != B.buf) {
+        in = A.len >= B.len ? A.buf : B.buf;
+        b += 2 * std::min(A.len, B.len) * elem_bytes;
+      }
+      nd.buf = 1 - in;
+      b += 2 * nd.len * elem_bytes;
+    }
+    if (root >= 0 && nodes[root].buf == 1) b += 2 * nodes[root].len * elem_bytes;
+    return b;
+  }
+
+  std::vector<Seg> build_segments(const std::vector<RunDesc>& asc, const std::vector<RunDesc>& desc) {
+    std::vector<Seg> runs;
+    for (auto& r : asc) runs.push_back({r.start, r.len, 0});
+    // descending runs trimmed against ascending runs (a shared
+    // boundary element goes to the ascending run; a sub-range of a descending
+    // run is still descending)
+    size_t ai = 0;
+    for (auto& r : desc) {
+      int64_t s = r.start, e = r.start + r.len;
+      while (ai < asc.size() && asc[ai].start + asc[ai].len <= s) ai++;
+      for (size_t k = ai; k < asc.size() && asc[k].start < e; k++) {
+        int64_t as = asc[k].start, ae = asc[k].start + asc[k].len;
+        if (as <= s && ae > s) s = ae;
+        else if (as > s && as < e) e = as;
+      }
+      if (e - s >= 2) runs.push_back({s, e - s, 1});
+    }
+    std::sort(runs.begin(), runs.end(), [](const Seg& a, const Seg& b) { return a.start < b.start; });
+    std::vector<Seg> segs;
+    int64_t pos = 0;
+    auto gap = [&](int64_t s, int64_t e) {
+      for (int64_t p = s; p < e; p += kCap) segs.push_back({p, std::min<int64_t>(kCap, e - p), 2});
+    };
+    for (auto& r : runs) {
+      if (r.start > pos) gap(pos, r.start);
+      int64_t s = std::max(pos, r.start);
+      if (r.start + r.len > s) segs.push_back({s, r.start + r.len - s, r.kind});
+      pos = std::max(pos, r.start + r.len);
+    }
+    if (pos < n) gap(pos, n);
+    return segs;
+  }
+
+  int64_t merge_route_bytes(const std::vector<Seg>& segs) {
+    int64_t b = 0;
+    std::vector<std::pair<int64_t, int64_t>> runs;
+    for (auto& s : segs) {
+      if (s.kind != 0) b += 2 * s.len * (kw + vw);
+      runs.push_back({s.start, s.len});
+    }
+    int root;
+    auto nodes = half_down_tree(runs, root);
+    return b + schedule_bytes(nodes, root, kw + vw);
+  }
+
+  void run_merge_route(const std::vector<Seg>& segs0) {
+    // H2: reverse descending runs in place
+    std::vector<RunDesc> rev;
+    std::vector<Item> tiles;
+    for (auto& s : segs0) {
+      if (s.kind == 1) rev.push_back({s.start, s.len, 0, 0});
+      if (s.kind == 2) {
+        Item it;
+        it.start = s.start;
+        it.len = (int32_t)s.len;
+        it.kind = kItemSort;
+        it.key = 0;
+        tiles.push_back(it);
+      }
+    }
+    c.plan.desc_runs_reversed = (int64_t)rev.size();
+    reverse_ranges(rev);
+    // H4: sort gap tiles in place
+    if (!tiles.empty()) {
+      Item* d_items = c.alloc<Item>(tiles.size());
+      int64_t* d_cnt = c.alloc<int64_t>(1);
+      c.upload(d_items, tiles);
+      std::vector<int64_t> cnt{(int64_t)tiles.size()};
+      c.upload(d_cnt, cnt);
+      int64_t gl = 0;
+      for (auto& t : tiles) gl += t.len;
+      finish(d_items, d_cnt, 0, (int64_t)tiles.size(), 2 * gl * (kw + vw));
+    }
+    // post-reversal boundary check: coalesce runs whose boundary is ordered
+    // (trimmed merges); a fully ordered set is the
+    // "sorted after reversal" exit.
+    std::vector<int64_t> bpos;
+    for (size_t i = 1; i < segs0.size(); i++) bpos.push_back(segs0[i].start);
+    std::vector<std::pair<int64_t, int64_t>> runs;
+    if (!bpos.empty()) {
+      int64_t nb = (int64_t)bpos.size();
+      int64_t* d_pos = c.alloc<int64_t>(nb);
+      uint8_t* d_flags = c.alloc<uint8_t>(nb + 8);
+      unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.alloc<unsigned long long>(1));
+      c.memset0(d_bad, 8);
+      c.upload(d_pos, bpos);
+      const K* kk = keys;
+      c.launch("boundary", nb * 2 * kw, [&] {
+        k_boundary_check<K><<<(unsigned)ceil_div<int64_t>(nb, 256), 256, 0, c.st>>>(kk, d_pos, nb, d_flags, d_bad);
+      });
+      const uint8_t* flags = reinterpret_cast<const uint8_t*>(c.readback(d_flags, (size_t)nb));
+      int64_t s = segs0[0].start, l = segs0[0].len;
+      for (int64_t i = 0; i < nb; i++) {
+        const Seg& g = segs0[i + 1];
+        if (flags[i]) { runs.push_back({s, l}); s = g.start; l = g.len; }
+        else l += g.len;
+      }
+      runs.push_back({s, l});
+    } else {
+      runs.push_back({0, n});
+    }
+    if (runs.size() == 1) { c.plan.levels = 0; return; }
+    // H6: half-down merge tree, executed level by level
+    int root;
+    auto nodes = half_down_tree(runs, root);
+    schedule_bytes(nodes, root, kw + vw);  // assigns buffers
+    ensure_ws();
+    int maxd = nodes[root].depth;
+    for (int d = 1; d <= maxd; d++) {
+      std::vector<CopyJob> copies;
+      std::vector<MergeJob> jobs;
+      int64_t cta = 0, ccta = 0, mbytes = 0, cbytes = 0;
+      for (auto& nd : nodes) {
+        if (nd.depth != d || nd.left < 0) continue;
+        Node& A = nodes[nd.left];
+        Node& B = nodes[nd.right];
+        int in = A.buf;
+        if (A.buf != B.buf) {
+          in = A.len >= B.len ? A.buf : B.buf;
+          Node& mv = (A.buf == in) ? B : A;
+          CopyJob cj{mv.start, mv.len, ccta, in == 1 ? 0 : 1, 0};  // dir 0: primary->ws
+          copies.push_back(cj);
+          ccta += ceil_div<int64_t>(mv.len, 256 * 8);
+          cbytes += 2 * mv.len * (kw + vw);
+        }
+        MergeJob j{nd.start, A.len, B.len, cta, in, 0};
+        jobs.push_back(j);
+        cta += ceil_div<int64_t>(nd.len, kMergeNV);
+        mbytes += 2 * nd.len * (kw + vw);
+      }
+      if (!copies.empty()) run_copies(copies, ccta, cbytes);
+      run_merges(jobs, cta, mbytes);
+    }
+    if (nodes[root].buf == 1) {
+      std::vector<CopyJob> cj{{0, n, 0, 1, 0}};
+      run_copies(cj, ceil_div<int64_t>(n, 256 * 8), 2 * n * (kw + vw));
+    }
+    c.plan.levels = maxd;
+  }
+
+  void run_copies(const std::vector<CopyJob>& jobs, int64_t ctas, int64_t bytes) {
+    CopyJob* d = c.alloc<CopyJob>(jobs.size());
+    c.upload(d, jobs);
+    int nj = (int)jobs.size();
+    K* kk = keys;
+    uint32_t* vv = vals;
+    K* w = wk;
+    uint32_t* wvv = wv;
+    c.launch("copy", bytes, [&] { k_copy<K, HAS_V, 256><<<(unsigned)ctas, 256, 0, c.st>>>(kk, vv, w, wvv, d, nj); });
+  }
+
+  void run_merges(const std::vector<MergeJob>& jobs, int64_t ctas, int64_t bytes) {
+    MergeJob* d = c.alloc<MergeJob>(jobs.size());
+    int64_t* splits = c.alloc<int64_t>(ctas + 1);
+    c.upload(d, jobs);
+    int nj = (int)jobs.size();
+    const K* kk = keys;
+    const K* w = wk;
+    c.launch("merge_partition", ctas * 2 * 20 * kw, [&] {
+      k_merge_partition<K, kMergeNV><<<(unsigned)ceil_div<int64_t>(ctas, 256), 256, 0, c.st>>>(kk, w, d, nj, ctas, splits);
+    });
+    size_t smem = sizeof(K) * padded_size<K>(kMergeNV) + (HAS_V ? 4 * padded_size<uint32_t>(kMergeNV) : 0);
+    auto kern = k_merge<K, HAS_V, kMergeNT, kMergeVT>;
+    set_smem(kern, smem);
+    K* pk = keys;
+    uint32_t* pv = vals;
+    K* wkk = wk;
+    uint32_t* wvv = wv;
+    c.launch("merge", bytes, [&] { kern<<<(unsigned)ctas, kMergeNT, smem, c.st>>>(pk, pv, wkk, wvv, d, nj, splits); });
+  }
+
+  // ---- top level
+  void run() {
+    c.plan.n = n;
+    const int64_t T = choose_tile(n);
+    const int64_t G = ceil_div<int64_t>(n, T);
+    const bool part = n > kCap;
+    Level L1;
+    if (part) {
+      std::vector<OvfSeg> whole{{0, n}};
+      level_alloc(L1, whole, T, 0);
+      level_splitters(L1);
+    }
+    TileSummary* d_sums = c.alloc<TileSummary>(G);
+    RunDesc* d_asc = c.alloc<RunDesc>(G + 1);
+    RunDesc* d_desc = c.alloc<RunDesc>(G + 1);
+    DevStats* d_pst = part ? L1.d_st : c.alloc<DevStats>(1);
+    if (!part) c.memset0(d_pst, sizeof(DevStats));
+    const K* kk = keys;
+    const int nbins1 = part ? L1.segs[0].nbins : 0;
+    c.launch("presort_scan", n * kw + (part ? (int64_t)nbins1 * G * 4 : 0), [&] {
+      if (part) {
+        if (HAS_V)
+          k_presort_scan<K, true, true, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq,
+                                                                           L1.d_m, L1.d_mat, nbins1, (int)G);
+        else
+          k_presort_scan<K, false, true, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq,
+                                                                            L1.d_m, L1.d_mat, nbins1, (int)G);
+      } else {
+        if (HAS_V)
+          k_presort_scan<K, true, false, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, nullptr, nullptr,
+                                                                            nullptr, nullptr, 0, (int)G);
+        else
+          k_presort_scan<K, false, false, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, nullptr, nullptr,
+                                                                             nullptr, nullptr, 0, (int)G);
+      }
+    });
+    c.launch("presort_resolve", G * (int64_t)sizeof(TileSummary), [&] {
+      k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst);
+    });
+    if (part) level_scan_plan(L1);
+    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(d_pst, sizeof(DevStats)));
+    c.plan.descents = hs.descents;
+    c.plan.asc_breaks = hs.asc_breaks;
+    c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
+    if (hs.error) fail(SR_ERR_INTERNAL, "plan kernel inconsistency");
+
+    const int force = g_force_route;
+    if (hs.descents == 0) {  // is_sorted exit
+      c.plan.route = SR_ROUTE_SORTED;
+      return;
+    }
+    if (hs.asc_breaks == 0 && force != SR_ROUTE_PARTITION && force != SR_ROUTE_MERGE) {
+      // one descending run over the whole array (strict for pairs): reverse
+      c.plan.route = SR_ROUTE_REVERSED;
+      c.plan.desc_runs_reversed = 1;
+      reverse_ranges({RunDesc{0, n, 0, 0}});
+      return;
+    }
+    if (!part && force != SR_ROUTE_MERGE) {
+      c.plan.route = SR_ROUTE_TILE;
+      std::vector<Item> one{Item{0, 0, (int32_t)n, kItemSort}};
+      Item* d_items = c.alloc<Item>(1);
+      int64_t* d_cnt = c.alloc<int64_t>(1);
+      std::vector<int64_t> cnt{1};
+      c.upload(d_items, one);
+      c.upload(d_cnt, cnt);
+      finish(d_items, d_cnt, 0, 1, 2 * n * (kw + vw));
+      return;
+    }
+    // MERGE vs PARTITION by planned bytes
+    bool use_merge = force == SR_ROUTE_MERGE;
+    std::vector<Seg> segs;
+    if (force == SR_ROUTE_MERGE || (force == 0 && g_merge_route && hs.asc_cover + hs.desc_cover >= n / 2)) {
+      std::vector<RunDesc> asc, desc;
+      if (hs.n_asc_runs) {
+        const RunDesc* h = reinterpret_cast<const RunDesc*>(c.readback(d_asc, sizeof(RunDesc) * hs.n_asc_runs));
+        asc.assign(h, h + hs.n_asc_runs);
+      }
+      if (hs.n_desc_runs) {
+        const RunDesc* h = reinterpret_cast<const RunDesc*>(c.readback(d_desc, sizeof(RunDesc) * hs.n_desc_runs));
+        desc.assign(h, h + hs.n_desc_runs);
+      }
+      segs = build_segments(asc, desc);
+      if (!use_merge) {
+        int64_t mb = merge_route_bytes(segs);
+        int64_t N = n * (kw + vw);
+        int64_t pb = 4 * N + (n > 4 * 1024 * 1024 ? 3 * N : 0);
+        use_merge = mb < pb;
+      }
+    }
+    if (use_merge) {
+      c.plan.route = SR_ROUTE_MERGE;
+      if (segs.empty()) segs = build_segments({}, {});
+      run_merge_route(segs);
+      return;
+    }
+    // PARTITION
+    c.plan.route = SR_ROUTE_PARTITION;
+    c.plan.levels = 1;
+    if (!part) fail(SR_ERR_INTERNAL, "partition route without level 1");
+    std::vector<OvfSeg> next;
+    if (hs.n_ovf > 0) {
+      const OvfSeg* h = reinterpret_cast<const OvfSeg*>(c.readback(L1.d_ovf, sizeof(OvfSeg) * hs.n_ovf));
+      next.assign(h, h + hs.n_ovf);
+    }
+    level_scatter(L1, hs);
+    level_finish(L1, hs);
+    run_levels(next, 1);
+  }
+};
+
+// ------------------------------------------------------------------ validation
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int32_t validate(const void* keys, const void* vals, int64_t n, int32_t dtype, bool pairs) {
+  if (n < 0) return SR_ERR_INVALID_ARGUMENT;
+  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (n > INT32_MAX) return SR_ERR_SIZE;
+  if (n <= 1) return SR_OK;
+  const int64_t kw = dtype == SR_INT32 ? 4 : 8;
+  if (!keys || (pairs && !vals)) return SR_ERR_INVALID_ARGUMENT;
+  if ((uintptr_t)keys % kw) return SR_ERR_ALIGNMENT;
+  if (pairs && (uintptr_t)vals % 4) return SR_ERR_ALIGNMENT;
+  if (!is_device_ptr(keys) || (pairs && !is_device_ptr(vals))) return SR_ERR_INVALID_ARGUMENT;
+  if (pairs) {
+    uintptr_t k0 = (uintptr_t)keys, k1 = k0 + n * kw, v0 = (uintptr_t)vals, v1 = v0 + n * 4;
+    if (k0 < v1 && v0 < k1) return SR_ERR_INVALID_ARGUMENT;
+  }
+  return SR_OK;
+}
+
+template <typename F>
+int32_t guarded(F&& f) {
+  t_state.err.clear();
+  try {
+    f();
+    return SR_OK;
+  } catch (const SrError& e) {
+    t_state.err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_state.err = "host allocation failed";
+    return SR_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    t_state.err = "unknown internal error";
+    return SR_ERR_INTERNAL;
+  }
+}
+
+int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream, bool pairs) {
+  int32_t v = validate(keys, vals, n, dtype, pairs);
+  if (v != SR_OK) {
+    t_state.err = sr_status_string(v);
+    return v;
+  }
+  return guarded([&] {
+    Ctx c((cudaStream_t)stream);
+    c.plan.n = n;
+    if (n <= 1) return;
+    init_pool();
+    if (dtype == SR_INT32) {
+      if (pairs) Sorter<int32_t, true>(c, (int32_t*)keys, (uint32_t*)vals, n).run();
+      else Sorter<int32_t, false>(c, (int32_t*)keys, nullptr, n).run();
+    } else {
+      if (pairs) Sorter<int64_t, true>(c, (int64_t*)keys, (uint32_t*)vals, n).run();
+      else Sorter<int64_t, false>(c, (int64_t*)keys, nullptr, n).run();
+    }
+  });
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int32_t sr_sort_keys(void* keys, int64_t n, int32_t dtype, void* stream) {
+  return sort_impl(keys, nullptr, n, dtype, stream, false);
+}
+
+int32_t sr_sort_pairs(void* keys, void* vals, int64_t n, int32_t dtype, void* stream) {
+  return sort_impl(keys, vals, n, dtype, stream, true);
+}
+
+int32_t sr_sort_host(void* host_keys, void* host_vals, int64_t n, int32_t dtype, void* stream) {
+  if (n < 0) return SR_ERR_INVALID_ARGUMENT;
+  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (n > INT32_MAX) return SR_ERR_SIZE;
+  if (n <= 1) return SR_OK;
+  if (!host_keys) return SR_ERR_INVALID_ARGUMENT;
+  const int64_t kw = dtype == SR_INT32 ? 4 : 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  void *dk = nullptr, *dv = nullptr;
+  int32_t rc = guarded([&] {
+    check_cuda(cudaMallocAsync(&dk, n * kw, st), "cudaMallocAsync");
+    if (host_vals) check_cuda(cudaMallocAsync(&dv, n * 4, st), "cudaMallocAsync");
+    check_cuda(cudaMemcpyAsync(dk, host_keys, n * kw, cudaMemcpyHostToDevice, st), "h2d");
+    if (host_vals) check_cuda(cudaMemcpyAsync(dv, host_vals, n * 4, cudaMemcpyHostToDevice, st), "h2d");
+  });
+  if (rc == SR_OK) rc = host_vals ? sr_sort_pairs(dk, dv, n, dtype, stream) : sr_sort_keys(dk, n, dtype, stream);
+  if (rc == SR_OK) {
+    rc = guarded([&] {
+      check_cuda(cudaMemcpyAsync(host_keys, dk, n * kw, cudaMemcpyDeviceToHost, st), "d2h");
+      if (host_vals) check_cuda(cudaMemcpyAsync(host_vals, dv, n * 4, cudaMemcpyDeviceToHost, st), "d2h");
+    });
+  }
+  if (dk) cudaFreeAsync(dk, st);
+  if (dv) cudaFreeAsync(dv, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (rc == SR_OK && e != cudaSuccess) {
+    t_state.err = cudaGetErrorString(e);
+    rc = SR_ERR_CUDA;
+  }
+  return rc;
+}
+
+int32_t sr_last_plan(sr_plan* out) {
+  if (!out) return SR_ERR_INVALID_ARGUMENT;
+  *out = t_state.plan;
+  return SR_OK;
+}
+
+const char* sr_status_string(int32_t s) {
+  switch (s) {
+    case SR_OK: return "ok";
+    case SR_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SR_ERR_UNSUPPORTED_DTYPE: return "unsupported dtype";
+    case SR_ERR_SIZE: return "size out of range";
+    case SR_ERR_ALIGNMENT: return "misaligned pointer";
+    case SR_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case SR_ERR_CUDA: return "CUDA error";
+    case SR_ERR_INTERNAL: return "internal error";
+    default: return "unknown status";
+  }
+}
+
+const char* sr_last_error(void) { return t_state.err.c_str(); }
+
+int32_t sr_set_option(int32_t key, int64_t value) {
+  switch (key) {
+    case SR_OPT_FORCE_ROUTE:
+      if (value != 0 && value != SR_ROUTE_MERGE && value != SR_ROUTE_PARTITION) return SR_ERR_INVALID_ARGUMENT;
+      g_force_route = (int)value;
+      return SR_OK;
+    case SR_OPT_PROFILE:
+      g_profile = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_MERGE_ROUTE:
+      g_merge_route = value ? 1 : 0;
+      return SR_OK;
+    default:
+      return SR_ERR_INVALID_ARGUMENT;
+  }
+}
+
+int32_t sr_last_profile(const char** names, float* ms, int64_t* bytes, int32_t cap) {
+  ThreadState& ts = t_state;
+  if (ts.prof.empty()) return 0;
+  cudaStreamSynchronize(ts.prof_stream);
+  int32_t k = 0;
+  for (auto& e : ts.prof) {
+    if (k < cap) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e.a, e.b);
+      if (names) names[k] = e.name;
+      if (ms) ms[k] = t;
+      if (bytes) bytes[k] = e.bytes;
+    }
+    k++;
+  }
+  return k;
+}
+
+}  // extern "C"
+
+#include "debug_api.cuh"

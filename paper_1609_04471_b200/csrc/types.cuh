@@ -1,0 +1,70 @@
+// types.cuh -- descriptors shared by the host planner and the kernels.
+#pragma once
+#include <cstdint>
+
+namespace sr {
+
+// Per-tile presortedness summary (H1/K1).  Positions are global indices i of
+// the adjacent pair (a_i, a_{i+1}); -1 / INT32_MAX when absent.
+struct TileSummary {
+  int32_t ndesc;   // #{i in tile : a_i > a_{i+1}}
+  int32_t nab;     // #{i in tile : descending-run break}
+  int32_t fdesc, ldesc;
+  int32_t fab, lab;
+  int32_t pad0, pad1;
+};
+
+// A long natural run [start, start+len) and its end keys as stored in the
+// input (before any reversal).  dir: 0 ascending, 1 descending.
+struct RunDesc {
+  int64_t start, len;
+  int64_t kfirst, klast;
+};
+
+// Device-side statistics block, copied to the host once per planning step.
+struct DevStats {
+  int64_t n;
+  int64_t descents;     // D = Run(A) - 1
+  int64_t asc_breaks;   // descending-run breaks
+  int64_t n_asc_runs, n_desc_runs;    // long runs (>= L_min)
+  int64_t asc_cover, desc_cover;      // keys covered by long runs
+  // partition level (plan kernel)
+  int64_t noneq_total;  // keys in range (non-equality) buckets
+  int64_t n_items;      // finish items emitted (cumulative counter)
+  int64_t n_ovf;        // oversized range buckets for the next level
+  int64_t ovf_keys;
+  int64_t eq_keys;
+  int64_t error;        // device-detected inconsistency (must stay 0)
+  int64_t pad[3];
+};
+
+// One segment of a partition level (H7-H10).
+struct SegDesc {
+  int64_t start, len;     // in the level's source buffer (global indices)
+  int64_t mat_base;       // first count-matrix entry of this segment
+  int64_t len_prefix;     // sum of len of earlier segments in this level
+  int32_t nbuckets;       // B_s (power of two, <= kMaxBuckets)
+  int32_t nbins;          // 2*B_s + 1 matrix rows (bucket-major)
+  int32_t chunk_base;     // first global chunk index
+  int32_t nchunks;        // G_s
+};
+
+// Work item for the finishing kernel (H11/H4 segmented).
+enum : int32_t { kItemSort = 0, kItemFill = 1 };
+struct Item {
+  int64_t start;
+  int64_t key;    // fill value for kItemFill
+  int32_t len;
+  int32_t kind;   // kItemSort / kItemFill | (buf << 4): buf 1 = workspace side
+};
+
+struct OvfSeg {
+  int64_t start, len;
+};
+
+constexpr int kMaxBuckets = 1024;           // B_max per level
+constexpr int kMaxBins = 2 * kMaxBuckets + 1;
+constexpr int kOversample = 8;              // o: S = B*o <= 8192 samples
+constexpr int kCap = 8192;                  // finishing tile (NT=512, VT=16)
+
+}  // namespace sr

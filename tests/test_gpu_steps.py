@@ -1,0 +1,158 @@
+"""Step-level parity (-m gpu): each hot-path row through its C-ABI
+entry point against the oracle function that follows the same passage."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1609_04471_b200 as sr
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a).copy()).cuda()
+
+
+# ---------------------------------------------------------------- H1 presortedness scan
+
+@pytest.mark.parametrize("strict", [False, True])
+@pytest.mark.parametrize("order,n,tile", [
+    ("alternating", 1 << 20, 4096), ("sharp_teeth", 3 * 65536 + 17, 8192), ("runs1024", 200_000, 1024),
+    ("reversed", 123_457, 1024), ("random", 500_000, 4096), ("sorted", 100_000, 1024), ("all_equal", 70_001, 2048),
+    ("organ_pipe", 99_999, 1024), ("even_teeth", 400_000, 4096), ("last1pct", 300_000, 1024),
+])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h1_presort_scan(order, n, tile, strict, dtype):
+    k = gen.make(order, n, dtype, config=20)
+    st, runs = sr.presort_scan(cuda(k), strict=strict, tile=tile)
+    assert st["descents"] == oracle.descents(k)  # Run(A) - 1
+    asc = [(s, l) for s, l in oracle.asc_runs(k) if l >= tile]
+    desc = [(s, l) for s, l in oracle.desc_runs(k, strict=strict) if l >= tile]
+    assert [(s, l) for s, l, d in runs if d == 0] == asc
+    assert [(s, l) for s, l, d in runs if d == 1] == desc
+    assert st["asc_breaks"] == len(oracle.desc_runs(k, strict=strict)) - 1
+    assert st["asc_cover"] == sum(l for _, l in asc) and st["desc_cover"] == sum(l for _, l in desc)
+
+
+def test_h1_worked_example():
+    k = np.array([1, 15, 18, 19, 20, 16, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2], np.int32)
+    st, runs = sr.presort_scan(cuda(k), tile=1024)
+    assert st["descents"] == 11 and runs == []
+
+
+# ---------------------------------------------------------------- H2 reversal
+
+@pytest.mark.parametrize("n,s,e", [(10, 0, 10), (100_001, 5, 99_000), (1 << 20, 0, 1 << 20), (33, 3, 4), (5000, 17, 4097)])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h2_reverse(n, s, e, dtype):
+    k = gen.make("random", n, dtype, config=21)
+    v = gen.index_payload(n)
+    dk, dv = cuda(k), cuda(v.view(np.int32))
+    sr.reverse_range(dk, s, e, vals=dv)
+    oracle.reverse(k, s, e, v)
+    assert np.array_equal(dk.cpu().numpy(), k)
+    assert np.array_equal(dv.cpu().numpy().view(np.uint32), v)
+
+
+# ---------------------------------------------------------------- H4 tile sort
+
+@pytest.mark.parametrize("tile", [1, 2, 7, 16, 100, 1000, 4096, 8191, 8192])
+@pytest.mark.parametrize("order", ["random", "few_unique", "reversed", "organ_pipe", "extremes"])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h4_tile_sort_stable(tile, order, dtype):
+    n = 3 * 8192 + 1234
+    k = gen.make(order, n, dtype, config=22)
+    v = gen.index_payload(n)
+    dk, dv = cuda(k), cuda(v.view(np.int32))
+    sr.tile_sort(dk, tile, vals=dv)
+    gk, gv = dk.cpu().numpy(), dv.cpu().numpy().view(np.uint32)
+    for s in range(0, n, tile):
+        ek, ev = oracle.sort_pairs(k[s:s + tile], v[s:s + tile])
+        assert np.array_equal(gk[s:s + tile], ek) and np.array_equal(gv[s:s + tile], ev)
+        if tile < 100 and s > 2000:
+            break
+    dk2 = cuda(k)
+    sr.tile_sort(dk2, tile)
+    assert np.array_equal(dk2.cpu().numpy()[:tile], oracle.sort_keys(k[:tile]))
+
+
+# ---------------------------------------------------------------- H5 merge path
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h5_merge_path(seed, dtype):
+    rng = np.random.default_rng(seed)
+    na, nb = int(rng.integers(0, 3000)), int(rng.integers(0, 3000))
+    hi = [3, 50, 10**9][seed % 3]
+    a = np.sort(rng.integers(0, hi, na)).astype(dtype)
+    b = np.sort(rng.integers(0, hi, nb)).astype(dtype)
+    diags = list(range(0, na + nb + 1, max(1, (na + nb) // 97))) + [na + nb]
+    got = sr.merge_path(cuda(a), cuda(b), diags)
+    assert got.tolist() == [oracle.merge_path(a, b, d) for d in diags]
+
+
+def test_h5_worked_example():
+    a = np.array([1, 15, 18, 19, 20], np.int32)
+    b = np.array([2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 16], np.int32)
+    assert sr.merge_path(cuda(a), cuda(b), [0, 1, 11, 12, 16]).tolist() == [0, 1, 1, 2, 5]
+
+
+# ---------------------------------------------------------------- H6 merge
+
+@pytest.mark.parametrize("na,nb", [(0, 5), (5, 0), (1, 1), (4096, 4096), (100_000, 3), (3, 100_000), (250_001, 123_457)])
+@pytest.mark.parametrize("hi", [4, 10**9])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h6_merge_stable(na, nb, hi, dtype):
+    rng = np.random.default_rng(na * 7 + nb)
+    a = np.sort(rng.integers(0, hi, na)).astype(dtype)
+    b = np.sort(rng.integers(0, hi, nb)).astype(dtype)
+    va = np.arange(na, dtype=np.uint32)
+    vb = np.arange(na, na + nb, dtype=np.uint32)
+    out, vout = sr.merge(cuda(a), cuda(b), cuda(va.view(np.int32)), cuda(vb.view(np.int32)))
+    ek, ev = oracle.merge(a, b, va, vb)
+    assert np.array_equal(out.cpu().numpy(), ek)
+    assert np.array_equal(vout.cpu().numpy().view(np.uint32), ev)
+    out2 = sr.merge(cuda(a), cuda(b))
+    assert np.array_equal(out2.cpu().numpy(), ek)
+
+
+def test_h6_trimmed_pair_is_copy():
+    a = np.arange(0, 50_000, dtype=np.int32)
+    b = np.arange(50_000, 90_000, dtype=np.int32)
+    assert np.array_equal(sr.merge(cuda(a), cuda(b)).cpu().numpy(), np.arange(90_000, dtype=np.int32))
+
+
+# ---------------------------------------------------------------- H7 splitters
+
+@pytest.mark.parametrize("order", ["random", "few_unique", "all_equal", "organ_pipe", "nearly", "few100", "extremes"])
+@pytest.mark.parametrize("nb", [2, 64, 1024])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h7_splitters(order, nb, dtype):
+    n = 300_007
+    k = gen.make(order, n, dtype, config=23)
+    gs, ge = sr.splitters(cuda(k), nb)
+    es, ee = oracle.splitters(k, 0, n, nb, 8)
+    assert gs.tolist() == es.astype(np.int64).tolist()
+    assert ge.tolist() == ee.tolist()
+
+
+# ---------------------------------------------------------------- H8-H10 partition level
+
+@pytest.mark.parametrize("order", ["random", "few_unique", "few100", "nearly", "all_equal", "organ_pipe", "extremes"])
+@pytest.mark.parametrize("nb", [2, 256, 1024])
+@pytest.mark.parametrize("pairs", [False, True])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_h8_h10_partition_level(order, nb, pairs, dtype):
+    n = 200_003
+    k = gen.make(order, n, dtype, config=24)
+    v = gen.index_payload(n)
+    ok, ov, counts = sr.partition_level(cuda(k), nb, vals=cuda(v.view(np.int32)) if pairs else None)
+    spl, eq = oracle.splitters(k, 0, n, nb, 8)
+    bins = oracle.classify(k, spl, eq)
+    ek, ev, ec = oracle.stable_partition(bins, 2 * nb + 1, k, v)
+    assert counts.tolist() == ec.tolist()
+    assert np.array_equal(ok.cpu().numpy(), ek)
+    if pairs:
+        assert np.array_equal(ov.cpu().numpy().view(np.uint32), ev)
