@@ -207,12 +207,15 @@ static uint64_t or_mix64(uint64_t z) {
 }
 
 /* Sample position k (0 <= k < S) of segment [start, start+len): stratum k is
- * [start + k*len/S, start + (k+1)*len/S); the sample is at a jittered offset. */
+ * [start + k*len/S, start + (k+1)*len/S); the sample sits at offset
+ * floor(h * w / 2^64) inside it (h = the k-th jitter draw, w = stratum width),
+ * i.e. a uniformly jittered position (SURVEY Q8 / DESIGN.md reading R8). */
 int64_t or_sample_pos(int64_t start, int64_t len, int64_t S, int64_t k) {
     int64_t lo = (k * len) / S, hi = ((k + 1) * len) / S;
     int64_t w = hi - lo;
     uint64_t h = or_mix64((uint64_t)start + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ULL);
-    return start + lo + (w > 0 ? (int64_t)(h % (uint64_t)w) : 0);
+    uint64_t off = (uint64_t)(((unsigned __int128)h * (uint64_t)w) >> 64);
+    return start + lo + (int64_t)off;
 }
 
 /* Splitters for one segment.  S = min(nbuckets * oversample, len) samples;

@@ -43,12 +43,28 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 // Stratified jittered sample position k of segment [start, start+len) with S
-// strata ("jittered regular positions ... deterministic").
-__host__ __device__ __forceinline__ int64_t sample_position(int64_t start, int64_t len, int64_t S, int64_t k) {
-  int64_t lo = (k * len) / S, hi = ((k + 1) * len) / S;
-  int64_t w = hi - lo;
+// strata ("jittered regular positions ... deterministic"): stratum
+// k is [k*len/S, (k+1)*len/S), offset = floor(h*w / 2^64) for the k-th jitter
+// draw h and stratum width w.  log2S >= 0 selects the shift form of the
+// division (S a power of two).
+__host__ __device__ __forceinline__ int64_t sample_position(int64_t start, int64_t len, int64_t S, int64_t k,
+                                                          int log2S = -1) {
+  int64_t lo, hi;
+  if (log2S >= 0) {
+    lo = (k * len) >> log2S;
+    hi = ((k + 1) * len) >> log2S;
+  } else {
+    lo = (k * len) / S;
+    hi = ((k + 1) * len) / S;
+  }
+  uint64_t w = (uint64_t)(hi - lo);
   uint64_t h = mix64((uint64_t)start + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ULL);
-  return start + lo + (w > 0 ? (int64_t)(h % (uint64_t)w) : 0);
+#ifdef __CUDA_ARCH__
+  uint64_t off = __umul64hi(h, w);
+#else
+  uint64_t off = (uint64_t)(((unsigned __int128)h * w) >> 64);
+#endif
+  return start + lo + (int64_t)off;
 }
 
 // ---- warp / block scans ----------------------------------------------------
