@@ -28,7 +28,7 @@
  *                      by running the merge d steps (PAPER.md:100 galloping
  *                      locates "the position in A where the current element
  *                      in B should go")
- *   or_splitters       stratified sample -> sort -> every o-th -> dedup;
+ *   or_splitters       stratified sample -> sort -> every o-th order statistic;
  *                      equality flag when a splitter occurs > gamma = 2 times
  *                      in the sample (PAPER.md:157 pseudo-median sampling;
  *                      PAPER.md:168 "(g) ... more than gamma = 2 elements
@@ -219,9 +219,11 @@ int64_t or_sample_pos(int64_t start, int64_t len, int64_t S, int64_t k) {
 }
 
 /* Splitters for one segment.  S = min(nbuckets * oversample, len) samples;
- * candidates c_j = sample[((j+1)*S)/nbuckets], j = 0..nbuckets-2; duplicates
- * removed (strictly increasing t_0 < ... < t_{m-1}); eq[i] = 1 when t_i occurs
- * more than gamma = 2 times in the sample.  Returns m. */
+ * splitter t_j = the ((j+1)*S/nbuckets)-th smallest sample, j = 0..nbuckets-2
+ * (equal values may repeat: classification by lower_bound sends every key to
+ * the first of equal splitters, the repeats delimit empty buckets);
+ * eq[j] = 1 when t_j occurs more than gamma = 2 times in the sample.
+ * Returns m = nbuckets - 1. */
 int32_t or_splitters(const void *keys, int64_t start, int64_t len, int32_t nbuckets, int32_t oversample,
                      int ks, int64_t *spl, uint8_t *eq) {
     int64_t S = (int64_t)nbuckets * oversample;
@@ -234,10 +236,7 @@ int32_t or_splitters(const void *keys, int64_t start, int64_t len, int32_t nbuck
     }
     sort_recs(smp, S);
     int32_t m = 0;
-    for (int32_t j = 0; j + 1 < nbuckets; j++) {
-        int64_t c = smp[((int64_t)(j + 1) * S) / nbuckets].key;
-        if (m == 0 || spl[m - 1] != c) spl[m++] = c;
-    }
+    for (int32_t j = 0; j + 1 < nbuckets; j++) spl[m++] = smp[((int64_t)(j + 1) * S) / nbuckets].key;
     for (int32_t i = 0; i < m; i++) {
         int64_t cnt = 0;
         for (int64_t k = 0; k < S; k++) cnt += (smp[k].key == spl[i]);

@@ -286,6 +286,26 @@ def test_classify_matches_searchsorted(seed):
     assert np.all(np.diff(bins[np.argsort(keys, kind="stable")]) >= 0)
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_classify_with_repeated_splitters(seed):
+    """Repeated splitter values: every key equal to a repeated splitter goes to
+    the first copy (lower_bound); the buckets between the copies stay empty."""
+    rng = np.random.default_rng(50 + seed)
+    keys = rng.integers(-20, 20, 5000).astype(np.int64)
+    spl = np.sort(rng.integers(-25, 25, int(rng.integers(1, 60)))).astype(np.int64)
+    vals, first = np.unique(spl, return_index=True)
+    flag_of = {int(v): int(rng.integers(0, 2)) for v in vals}
+    eq = np.array([flag_of[int(v)] for v in spl], np.uint8)
+    bins = oracle.classify(keys, spl, eq)
+    i = np.searchsorted(spl, keys, side="left")
+    hit = (i < spl.size) & (spl[np.minimum(i, spl.size - 1)] == keys) & (eq[np.minimum(i, spl.size - 1)] == 1)
+    assert np.array_equal(bins, 2 * i + hit)
+    used = set(bins.tolist())
+    for j in range(1, spl.size):  # no key lands between two copies of a value
+        if spl[j] == spl[j - 1]:
+            assert 2 * j not in used and 2 * j + 1 not in used
+
+
 def test_stable_partition_matches_stable_library_sort():
     rng = np.random.default_rng(7)
     n = 20000
@@ -304,20 +324,20 @@ def test_splitters_properties(order):
     B, o = 256, 8
     spl, eq = oracle.splitters(k, 0, n, B, o)
     S = B * o
-    assert 1 <= spl.size <= B - 1
-    assert np.all(np.diff(spl.astype(np.int64)) > 0)  # strictly increasing (dedup)
+    assert spl.size == B - 1
+    assert np.all(np.diff(spl.astype(np.int64)) >= 0)  # non-decreasing (repeats delimit empty buckets)
     pos = [oracle.sample_pos(0, n, S, t) for t in range(S)]
     for t, p in enumerate(pos):  # one sample per stratum
         assert (t * n) // S <= p < ((t + 1) * n) // S
     smp = np.sort(k[pos])  # library sort of the sample: order statistics
     cand = [smp[((j + 1) * S) // B] for j in range(B - 1)]
-    assert spl.tolist() == sorted(set(int(c) for c in cand))
+    assert spl.tolist() == [int(c) for c in cand]
     for t, f in zip(spl, eq):
         assert f == (int((smp == t).sum()) > 2)  # gamma = 2
     if order == "few_unique":  # all 10 values become equality splitters
-        assert spl.size == 10 and eq.all()
+        assert len(set(spl.tolist())) == 10 and eq.all()
     if order == "all_equal":
-        assert spl.size == 1 and eq.all()
+        assert len(set(spl.tolist())) == 1 and eq.all()
 
 
 def test_count_and_stable_rank():
