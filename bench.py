@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py -- Mkeys/s of the B200 adaptive sort on BASELINE.json's workloads.
+
+Default workload (N=1): configs[1] ("C2"): n = 2,000,000 int32 keys, four
+orders (random, reversely sorted, nearly sorted = n/100 swaps, few unique = 10
+values).  One STEP = one sort of one instance of each of the four orders
+(8,000,000 keys).  value = keys sorted / summed device time of the sorts.
+
+Timing: every sort is bracketed by CUDA events on the sort's stream.  Before
+each sort the input is restored from a pristine device copy and L2 is flushed
+by writing a 512 MiB buffer (both untimed, outside the events); the K timed
+steps are bracketed by barrier + synchronize on both sides and the max over
+ranks is taken.  e2e: the same metric through sr_sort_host (HOST pinned
+buffers; H2D copy, sort, D2H copy and stream sync inside the events).
+
+--impl reference runs the CPU oracle (the reference arm for this tier: a plain
+single-threaded mergesort, oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import gen  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+WORKLOADS = {
+    # name: (n, dtype, orders, config index for seeds)
+    "c2": (2_000_000, np.int32, ["random", "reversed", "nearly", "few_unique"], 1),
+    "c1": (1_000_000, np.int32, ["random"], 0),
+    "c5a": (268_435_456, np.int32, ["random"], 4),
+    "c5b": (268_435_456, np.int32, ["nearly1000"], 4),
+    "c5c": (134_217_728, np.int64, ["random"], 4),
+    "c3": (16_777_216, np.int32, ["swaps_1e4", "swaps_1e3", "swaps_1e2", "swaps_1e1", "runs1024", "last1pct",
+                                  "alternating"], 2),
+    "c4": (16_777_216, np.int32, ["few100"], 3),
+}
+
+
+def make_input(order, n, dtype, config, instance):
+    if order == "nearly1000":
+        return gen.swaps(n, n // 1000, dtype, gen.seed_for(config, 2, instance))
+    return gen.make(order, n, dtype, config=config, instance=instance)
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, wl):
+    """Reference arm: the CPU oracle on a bounded sample of the workload."""
+    import oracle
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n, dtype, orders, cfg = WORKLOADS[wl]
+    budget = float(os.environ.get("SR_REF_BUDGET_S", "20"))
+    # bounded sample: the first `m` keys of each order's instance, m chosen so a step is ~budget/(steps+warmup) s
+    per_step = budget / max(1, args.steps + args.warmup)
+    m = min(n, max(10_000, int(per_step / (len(orders) * 1.2e-7) )))  # ~120 ns/key oracle estimate
+    inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
+    for _ in range(args.warmup):
+        for a in inputs:
+            oracle.sort_keys(a)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for a in inputs:
+            oracle.sort_keys(a)
+    dt = (time.perf_counter() - t0) / args.steps
+    keys = m * len(orders)
+    v = keys / dt / 1e6
+    line = {"impl": "reference", "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types)", "value": round(v, 3),
+            "unit": "Mkeys/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": np.dtype(dtype).name.replace("int", "i"), "data": "synthetic",
+            "config": {"workload": wl, "n": n, "orders": orders, "sample_keys_per_order": m},
+            "cpu_baseline": {"value": round(v, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {m} keys of instance 0 of each order, single-threaded C mergesort"},
+            "e2e": {"value": round(v, 3), "unit": "Mkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """The oracle as it stands, single-threaded, on a bounded sample (whole instances while within budget)."""
+    import oracle
+    n, dtype, orders, cfg = WORKLOADS[wl]
+    m = n if n <= 4_000_000 else 4_000_000
+    inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
+    keys = 0
+    t_sort = 0.0
+    rounds = 0
+    while t_sort < budget_s and rounds < 10:
+        for a in inputs:
+            t0 = time.perf_counter()
+            oracle.sort_keys(a)
+            t_sort += time.perf_counter() - t0
+            keys += a.size
+        rounds += 1
+    sample = (f"{rounds} x instance 0 of each of {orders}, " + (f"n={n}" if m == n else f"first {m} keys of n={n}"))
+    return {"value": round(keys / t_sort / 1e6, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
+            "sample": sample, "host_cpus": os.cpu_count()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    wl = args.workload
+
+    if args.impl == "reference":
+        run_reference(args, wl)
+        return
+
+    import torch
+    import paper_1609_04471_b200 as sr
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    n, dtype, orders, cfg = WORKLOADS[wl]
+    tdt = torch.int32 if dtype == np.int32 else torch.int64
+    kw = np.dtype(dtype).itemsize
+
+    # inputs: instance = rank * (steps+warmup) + step  (weak scaling: independent problems per rank)
+    total = args.steps + args.warmup
+    big = n >= 50_000_000
+    ninst = 1 if big else total
+    pristine = {}
+    host_inputs = {}
+    for o in orders:
+        for i in range(ninst):
+            a = make_input(o, n, dtype, cfg, rank * total + i)
+            pristine[(o, i)] = torch.from_numpy(a).to(dev)
+            if i == 0:
+                host_inputs[o] = a
+    work = torch.empty(n, dtype=tdt, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def one_sort(o, i, ev=None):
+        work.copy_(pristine[(o, i % ninst)])
+        flush.fill_(i)
+        if ev:
+            ev[0].record(stream)
+        sr.sort_keys(work)
+        if ev:
+            ev[1].record(stream)
+        return sr.last_plan()
+
+    for w in range(args.warmup):
+        for o in orders:
+            one_sort(o, w)
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in orders]
+           for _ in range(args.steps)]
+    plans = []
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            for j, o in enumerate(orders):
+                plans.append((o, one_sort(o, args.warmup + s, evs[s][j])))
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if ws > 1:
+        torch.distributed.barrier()
+    per_order_ms = {o: [evs[s][j][0].elapsed_time(evs[s][j][1]) for s in range(args.steps)] for j, o in enumerate(orders)}
+    step_ms = [sum(evs[s][j][0].elapsed_time(evs[s][j][1]) for j in range(len(orders))) for s in range(args.steps)]
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    keys_all = n * len(orders) * args.steps * ws
+    value = keys_all / (total_ms / 1e3) / 1e6
+    launches = sum(p["launches"] for _, p in plans)
+    bytes_planned = sum(p["bytes_planned"] for _, p in plans) / args.steps
+
+    # ---- e2e through the host API (pinned host buffers, copies inside the events)
+    e2e = None
+    if not args.no_e2e:
+        pin = {o: torch.from_numpy(host_inputs[o]).pin_memory() for o in orders}
+        hbuf = torch.empty(n, dtype=tdt).pin_memory()
+        hb = hbuf.numpy()
+        e2e_ms = 0.0
+        for s in range(args.warmup + args.steps):
+            for o in orders:
+                hbuf.copy_(pin[o])
+                flush.fill_(s)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                sr.sort_host(hb, None, stream.cuda_stream)
+                b.record(stream)
+                b.synchronize()
+                if s >= args.warmup:
+                    e2e_ms += a.elapsed_time(b)
+        if ws > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": round(keys_all / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mkeys/s",
+               "h2d_bytes_per_step": n * kw * len(orders), "d2h_bytes_per_step": n * kw * len(orders),
+               "ms_per_step": round(e2e_ms / args.steps, 4)}
+
+    # ---- per-kernel device times (profile pass over the same inputs, CUDA events on the sort stream)
+    sr.set_option(sr.OPT_PROFILE, 1)
+    kern = {}
+    for s in range(args.steps):
+        for o in orders:
+            one_sort(o, args.warmup + s)
+            for name, ms, by in sr.last_profile():
+                d = kern.setdefault(name, {"ms": 0.0, "bytes": 0, "launches": 0})
+                d["ms"] += ms
+                d["bytes"] += by
+                d["launches"] += 1
+    sr.set_option(sr.OPT_PROFILE, 0)
+    hbm, hbm_src = peaks()
+    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    avg_ms = d["ms"] / d["launches"]
+    bytes_per_launch = d["bytes"] / d["launches"]
+    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    kern_total = sum(v["ms"] for v in kern.values())
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                "share_of_kernel_time": round(d["ms"] / kern_total, 3),
+                "kernels": {k: {"ms_per_launch": round(v["ms"] / v["launches"], 4),
+                                "GBps": round(v["bytes"] / v["launches"] / (v["ms"] / v["launches"] / 1e3) / 1e9, 1),
+                                "launches_per_step": v["launches"] / args.steps} for k, v in kern.items()}}
+    step_ms_mean = total_ms / args.steps
+    route_of = {o: p["route_name"] for o, p in plans[:len(orders)]}
+
+    line = {
+        "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types); achieved HBM GB/s vs peak",
+        "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_ms_mean, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "i32" if dtype == np.int32 else "i64", "data": "synthetic",
+        "config": {"workload": wl, "n": n, "orders": orders, "keys_per_step_per_gpu": n * len(orders),
+                   "l2": "flushed (512 MiB write) before every sort; restore+flush outside the events",
+                   "parallelism": f"independent instances per rank x{ws}",
+                   "per_order_ms_mean": {o: round(statistics.mean(v), 4) for o, v in per_order_ms.items()},
+                   "total_of_order_means_ms": round(sum(statistics.mean(v) for v in per_order_ms.values()), 4),
+                   "routes": route_of, "wall_s": round(t_wall, 3)},
+        "whole_step_hbm": {"bytes_planned_per_step": int(bytes_planned),
+                           "GBps": round(bytes_planned / (step_ms_mean / 1e3) / 1e9, 1),
+                           "frac_of_peak": round(bytes_planned / (step_ms_mean / 1e3) / 1e9 / hbm, 4),
+                           "ideal_pass_frac": round(2 * n * kw * len(orders) / (step_ms_mean / 1e3) / 1e9 / hbm, 4)},
+        "roofline": roofline,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,129 @@
+// bitonic.cuh -- H4 tile sort for keys only: a register / warp-shuffle bitonic
+// network over up to NT*VT keys of one CTA.
+//
+// Same role as block_sort.cuh (the "minrun" tile sort of §3(b), PAPER.md:94;
+// the alpha cutoff of §4(a)), but organised for sm_100a's
+// latency profile: every stage is a set of VT independent compare-exchanges
+// per thread (no dependent shared-memory chains as in a serial merge).
+// Partners within a thread use registers, partners within a warp use
+// __shfl_xor_sync, and only partners in another warp go through shared memory
+// (double-buffered, one barrier per stage).  All runs are kept ascending: the
+// first stage of every merge level compares mirrored positions ("flip"), the
+// following half-cleaner stages compare i and i^j.  Equal keys are
+// indistinguishable, so the missing stability is unobservable for keys-only
+// sorts; pairs use the stable merge sort of block_sort.cuh.
+#pragma once
+#include "block_sort.cuh"
+#include "common.cuh"
+
+namespace sr {
+
+template <typename K, int NT, int VT>
+struct BitonicSort {
+  static constexpr int NV = NT * VT;
+  static constexpr int SMEM = 2 * NV;  // double buffer for cross-warp stages
+  static_assert((VT & (VT - 1)) == 0 && VT >= 2, "VT must be a power of two");
+  static_assert(NT % 32 == 0, "");
+
+  __device__ __forceinline__ static K kmin(K a, K b) { return min(a, b); }
+  __device__ __forceinline__ static K kmax(K a, K b) { return max(a, b); }
+
+  // partner values of a cross-thread stage are in b[]; flip pairs r with VT-1-r
+  __device__ __forceinline__ static void combine(K (&k)[VT], const K (&b)[VT], bool lower, bool flip) {
+#pragma unroll
+    for (int r = 0; r < VT; r++) {
+      K o = flip ? b[VT - 1 - r] : b[r];
+      k[r] = lower ? kmin(k[r], o) : kmax(k[r], o);
+    }
+  }
+
+  __device__ __forceinline__ static void shfl_stage(K (&k)[VT], int mask, bool lower, bool flip) {
+    K b[VT];
+#pragma unroll
+    for (int r = 0; r < VT; r++) b[r] = __shfl_xor_sync(0xffffffffu, k[r], mask);
+    combine(k, b, lower, flip);
+  }
+
+  __device__ __forceinline__ static void reg_half_cleaners(K (&k)[VT]) {
+#pragma unroll
+    for (int j = VT / 2; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < VT; r++) {
+        if ((r & j) == 0) {
+          K x = k[r], y = k[r | j];
+          k[r] = kmin(x, y);
+          k[r | j] = kmax(x, y);
+        }
+      }
+    }
+  }
+
+  // Sort ks[0, count) ascending in place (count <= NV); ks must hold SMEM
+  // elements.  All NT threads must call.
+  __device__ static void sort(K* ks, int count) {
+    const int t = threadIdx.x;
+    const int need = (count + VT - 1) / VT;
+    int nta = 32;
+    while (nta < need) nta <<= 1;
+    const bool act = t < nta;
+    K k[VT];
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < VT; i++) {
+        int p = t * VT + i;
+        k[i] = p < count ? ks[p] : KeyTraits<K>::max_key();
+      }
+      batcher_network<VT>([&](int a, int b) {
+        K x = k[a], y = k[b];
+        k[a] = kmin(x, y);
+        k[b] = kmax(x, y);
+      });
+    }
+    int parity = 0;
+    __syncthreads();  // everyone has read ks before the first cross-warp stage writes it
+    for (int kk = 2 * VT; kk <= nta * VT; kk <<= 1) {
+      const int tk = kk / VT;  // threads per merged run
+      // flip stage: partner thread t ^ (tk-1), register VT-1-r
+      {
+        const int m = tk - 1;
+        const bool lower = (t & (tk >> 1)) == 0;
+        if (m < 32) {
+          if (act) shfl_stage(k, m, lower, true);
+        } else {
+          K* buf = ks + parity * NV;
+          if (act) BlockSort<K, false, NT, VT>::store_vec(buf + t * VT, k);
+          __syncthreads();
+          if (act) {
+            K b[VT];
+            BlockSort<K, false, NT, VT>::load_vec(buf + (t ^ m) * VT, b);
+            combine(k, b, lower, true);
+          }
+          parity ^= 1;
+        }
+      }
+      // half-cleaners across threads: j = kk/4 .. VT
+      for (int jt = tk >> 2; jt >= 1; jt >>= 1) {
+        const bool lower = (t & jt) == 0;
+        if (jt < 32) {
+          if (act) shfl_stage(k, jt, lower, false);
+        } else {
+          K* buf = ks + parity * NV;
+          if (act) BlockSort<K, false, NT, VT>::store_vec(buf + t * VT, k);
+          __syncthreads();
+          if (act) {
+            K b[VT];
+            BlockSort<K, false, NT, VT>::load_vec(buf + (t ^ jt) * VT, b);
+            combine(k, b, lower, false);
+          }
+          parity ^= 1;
+        }
+      }
+      if (act) reg_half_cleaners(k);
+    }
+    __syncthreads();
+    if (act) BlockSort<K, false, NT, VT>::store_vec(ks + t * VT, k);
+    __syncthreads();
+  }
+};
+
+}  // namespace sr

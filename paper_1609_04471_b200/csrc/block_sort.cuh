@@ -1,15 +1,20 @@
 // block_sort.cuh -- H4 tile sort: a stable ascending sort of up to NT*VT items
-// held in (padded) shared memory by one CTA.
+// held in shared memory by one CTA.
 //
 // Paper anchor: §3(b) "If a run in the input is shorter than the minimal length
 // for a run, insertion sort is called to create a longer run" (PAPER.md:94,
 // Appendix A isort) and §4(a) the alpha cutoff.
 // On the GPU the "minrun" is a whole CTA tile: each thread sorts VT keys in
-// registers with odd-even transposition (swap only on strict '>', so it is
-// stable), then log2(NT) merge-path levels in shared memory merge the
-// per-thread runs; merges take from the left run on ties, so the
-// whole tile sort is stable and pairs keep input order among equal keys.
+// registers, then log2(NT) merge-path levels in shared memory merge the
+// per-thread runs.  Merges take from the left run on ties.
+//   keys only: the register sort is Batcher's odd-even merge network on
+//              min/max (equal keys are indistinguishable, so stability is moot);
+//   pairs:     odd-even transposition (swap only on strict '>'), stable, and
+//              every merge tracks source positions to gather the payloads,
+//   so the pair sort keeps input order among equal keys.
 #pragma once
+#include <utility>
+
 #include "common.cuh"
 
 namespace sr {
@@ -30,38 +35,158 @@ __device__ __forceinline__ int merge_path_search(LoadA a, int a_len, LoadB b, in
   return lo;
 }
 
+// Batcher's odd-even merge sort network over N register slots, tabulated at
+// compile time so every compare-exchange addresses registers by constants.
+template <int N>
+struct BatcherNet {
+  static constexpr int count() {
+    int c = 0;
+    for (int p = 1; p < N; p += p)
+      for (int k = p; k > 0; k /= 2)
+        for (int j = k % p; j + k < N; j += k + k)
+          for (int i = 0; i < k && i + j + k < N; i++)
+            if ((i + j) / (p + p) == (i + j + k) / (p + p)) c++;
+    return c;
+  }
+  static constexpr int C = count();
+  struct Table {
+    int a[C > 0 ? C : 1];
+    int b[C > 0 ? C : 1];
+  };
+  static constexpr Table make() {
+    Table t{};
+    int c = 0;
+    for (int p = 1; p < N; p += p)
+      for (int k = p; k > 0; k /= 2)
+        for (int j = k % p; j + k < N; j += k + k)
+          for (int i = 0; i < k && i + j + k < N; i++)
+            if ((i + j) / (p + p) == (i + j + k) / (p + p)) { t.a[c] = i + j; t.b[c] = i + j + k; c++; }
+    return t;
+  }
+  static constexpr int a(int c) { return make().a[c]; }
+  static constexpr int b(int c) { return make().b[c]; }
+};
+
+template <int N, typename CE, int... I>
+__device__ __forceinline__ void batcher_apply(CE& ce, std::integer_sequence<int, I...>) {
+  (ce(std::integral_constant<int, BatcherNet<N>::a(I)>::value, std::integral_constant<int, BatcherNet<N>::b(I)>::value),
+   ...);
+}
+
+template <int N, typename CE>
+__device__ __forceinline__ void batcher_network(CE&& ce) {
+  batcher_apply<N>(ce, std::make_integer_sequence<int, BatcherNet<N>::C>{});
+}
+
 template <typename K, bool HAS_V, int NT, int VT>
 struct BlockSort {
   static constexpr int NV = NT * VT;
-  static constexpr int KEYS_SMEM = padded_size<K>(NV);
-  static constexpr int VALS_SMEM = HAS_V ? padded_size<uint32_t>(NV) : 1;
+  // slack after NV: the branch-free serial merge may read one element past a list
+  static constexpr int KEYS_SMEM = NV + VT;
+  static constexpr int VALS_SMEM = HAS_V ? NV + VT : 1;
+  static_assert((VT & (VT - 1)) == 0, "VT must be a power of two");
 
-  // Stable in-register sort of VT items (odd-even transposition sort).
   __device__ __forceinline__ static void thread_sort(K (&k)[VT], uint32_t (&v)[VT]) {
+    if (!HAS_V) {
+      batcher_network<VT>([&](int a, int b) {
+        K x = k[a], y = k[b];
+        k[a] = x < y ? x : y;
+        k[b] = x < y ? y : x;
+      });
+    } else {
 #pragma unroll
-    for (int r = 0; r < VT; r++) {
+      for (int r = 0; r < VT; r++) {
 #pragma unroll
-      for (int i = (r & 1); i + 1 < VT; i += 2) {
-        if (k[i + 1] < k[i]) {  // strict: equal keys never swap
-          K tk = k[i]; k[i] = k[i + 1]; k[i + 1] = tk;
-          if (HAS_V) { uint32_t tv = v[i]; v[i] = v[i + 1]; v[i + 1] = tv; }
+        for (int i = (r & 1); i + 1 < VT; i += 2) {
+          bool sw = k[i + 1] < k[i];  // strict: equal keys never swap (stable)
+          K a = k[i], b = k[i + 1];
+          uint32_t va = v[i], vb = v[i + 1];
+          k[i] = sw ? b : a;
+          k[i + 1] = sw ? a : b;
+          v[i] = sw ? vb : va;
+          v[i + 1] = sw ? va : vb;
         }
       }
     }
   }
 
-  __device__ __forceinline__ static void store_regs(K* ks, uint32_t* vs, const K (&k)[VT], const uint32_t (&v)[VT]) {
+  // Blocked store/load of VT consecutive elements as 16-byte vectors, built
+  // element by element so the register arrays never need an address.
+  __device__ __forceinline__ static uint32_t lo32(int32_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t lo32(uint32_t x) { return x; }
+  template <typename T>
+  __device__ __forceinline__ static void store_vec(T* base, const T (&x)[VT]) {
+    uint4* p = reinterpret_cast<uint4*>(base);
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int i = 0; i < VT / 4; i++)
+        p[i] = make_uint4((uint32_t)x[4 * i], (uint32_t)x[4 * i + 1], (uint32_t)x[4 * i + 2], (uint32_t)x[4 * i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VT / 2; i++) {
+        uint64_t a = (uint64_t)x[2 * i], b = (uint64_t)x[2 * i + 1];
+        p[i] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+      }
+    }
+  }
+  template <typename T>
+  __device__ __forceinline__ static void load_vec(const T* base, T (&x)[VT]) {
+    const uint4* p = reinterpret_cast<const uint4*>(base);
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int i = 0; i < VT / 4; i++) {
+        uint4 q = p[i];
+        x[4 * i] = (T)q.x; x[4 * i + 1] = (T)q.y; x[4 * i + 2] = (T)q.z; x[4 * i + 3] = (T)q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VT / 2; i++) {
+        uint4 q = p[i];
+        x[2 * i] = (T)(((uint64_t)q.y << 32) | q.x);
+        x[2 * i + 1] = (T)(((uint64_t)q.w << 32) | q.z);
+      }
+    }
+  }
+
+  // One merge level: thread t of a cooperative group of `coop` threads merges
+  // VT outputs of two adjacent sorted lists of (coop/2)*VT items.
+  __device__ __forceinline__ static void merge_level(const K* ks, const uint32_t* vs, int coop, K (&k)[VT],
+                                                     uint32_t (&v)[VT]) {
     const int t = threadIdx.x;
+    const int list = (coop >> 1) * VT;
+    const int a0 = (t & ~(coop - 1)) * VT;
+    const int diag = (t & (coop - 1)) * VT;
+    const K* A = ks + a0;
+    const K* B = A + list;
+    int lo = diag - list > 0 ? diag - list : 0;
+    int hi = diag < list ? diag : list;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (!(B[diag - 1 - mid] < A[mid])) lo = mid + 1; else hi = mid;
+    }
+    int ai = lo, bi = diag - lo;
+    K ak = A[ai], bk = B[bi];  // over-reads stay inside the slack
+    int src[VT];
 #pragma unroll
     for (int i = 0; i < VT; i++) {
-      ks[pad_idx<K>(t * VT + i)] = k[i];
-      if (HAS_V) vs[pad_idx<uint32_t>(t * VT + i)] = v[i];
+      const bool p = (bi >= list) || (ai < list && !(bk < ak));
+      k[i] = p ? ak : bk;
+      if (HAS_V) src[i] = p ? a0 + ai : a0 + list + bi;
+      ai += p;
+      bi += !p;
+      const K nx = *(p ? A + ai : B + bi);
+      ak = p ? nx : ak;
+      bk = p ? bk : nx;
+    }
+    if (HAS_V) {
+#pragma unroll
+      for (int i = 0; i < VT; i++) v[i] = vs[src[i]];
     }
   }
 
   // Sort items [0, count) of ks (and vs) in place; count <= NV.  Only the
-  // smallest power-of-two number of threads that covers count works, so a
-  // short segment costs O(count log count).  All NT threads must call this.
+  // smallest power-of-two number of threads covering count takes part, so a
+  // short range costs O(count log count).  All NT threads must call this.
   __device__ static void sort(K* ks, uint32_t* vs, int count) {
     const int t = threadIdx.x;
     const int need = (count + VT - 1) / VT;
@@ -71,52 +196,33 @@ struct BlockSort {
     K k[VT];
     uint32_t v[VT];
     if (act) {
+      if ((t + 1) * VT <= count) {
+        load_vec(ks + t * VT, k);
+        if (HAS_V) load_vec(vs + t * VT, v);
+      } else {
 #pragma unroll
-      for (int i = 0; i < VT; i++) {
-        int p = t * VT + i;
-        bool ok = p < count;
-        k[i] = ok ? ks[pad_idx<K>(p)] : KeyTraits<K>::max_key();  // +inf padding stays last (stable)
-        v[i] = (HAS_V && ok) ? vs[pad_idx<uint32_t>(p)] : 0u;
+        for (int i = 0; i < VT; i++) {
+          int p = t * VT + i;
+          k[i] = p < count ? ks[p] : KeyTraits<K>::max_key();  // +inf padding stays last (stable)
+          v[i] = (HAS_V && p < count) ? vs[p] : 0u;
+        }
       }
       thread_sort(k, v);
     }
     __syncthreads();
     for (int coop = 2; coop <= nta; coop <<= 1) {
-      if (act) store_regs(ks, vs, k, v);
-      __syncthreads();
       if (act) {
-        const int list = (coop >> 1) * VT;
-        const int a0 = (t / coop) * coop * VT;
-        const int b0 = a0 + list;
-        const int diag = (t % coop) * VT;
-        int mp = merge_path_search<K>([&](int i) { return ks[pad_idx<K>(a0 + i)]; }, list,
-                                      [&](int i) { return ks[pad_idx<K>(b0 + i)]; }, list, diag);
-        int ai = a0 + mp, bi = b0 + diag - mp;
-        const int aend = a0 + list, bend = b0 + list;
-        K ak = ai < aend ? ks[pad_idx<K>(ai)] : K(0);
-        K bk = bi < bend ? ks[pad_idx<K>(bi)] : K(0);
-        int src[VT];
-#pragma unroll
-        for (int i = 0; i < VT; i++) {
-          bool take_a = (bi >= bend) || (ai < aend && !(bk < ak));
-          k[i] = take_a ? ak : bk;
-          src[i] = take_a ? ai : bi;
-          if (take_a) {
-            ++ai;
-            if (ai < aend) ak = ks[pad_idx<K>(ai)];
-          } else {
-            ++bi;
-            if (bi < bend) bk = ks[pad_idx<K>(bi)];
-          }
-        }
-        if (HAS_V) {
-#pragma unroll
-          for (int i = 0; i < VT; i++) v[i] = vs[pad_idx<uint32_t>(src[i])];
-        }
+        store_vec(ks + t * VT, k);
+        if (HAS_V) store_vec(vs + t * VT, v);
       }
       __syncthreads();
+      if (act) merge_level(ks, vs, coop, k, v);
+      __syncthreads();
     }
-    if (act) store_regs(ks, vs, k, v);
+    if (act) {
+      store_vec(ks + t * VT, k);
+      if (HAS_V) store_vec(vs + t * VT, v);
+    }
     __syncthreads();
   }
 };

@@ -29,13 +29,13 @@ void presort_scan_t(Ctx& c, const K* keys, int64_t n, int strict, int tile, sr_p
   c.launch("presort_scan", n * sizeof(K), [&] {
     if (strict)
       k_presort_scan<K, true, false, 256><<<(unsigned)G, 256, 0, c.st>>>(keys, n, tile, d_sums, nullptr, nullptr,
-                                                                         nullptr, nullptr, 0, (int)G);
+                                                                         nullptr, nullptr, 0, (int)G, nullptr);
     else
       k_presort_scan<K, false, false, 256><<<(unsigned)G, 256, 0, c.st>>>(keys, n, tile, d_sums, nullptr, nullptr,
-                                                                          nullptr, nullptr, 0, (int)G);
+                                                                          nullptr, nullptr, 0, (int)G, nullptr);
   });
   c.launch("presort_resolve", G * 32, [&] {
-    k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(keys, n, d_sums, (int)G, tile, d_asc, d_desc, d_st);
+    k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(keys, n, d_sums, (int)G, tile, d_asc, d_desc, d_st, 0, 1);
   });
   DevStats hs = *reinterpret_cast<DevStats*>(c.readback(d_st, sizeof(DevStats)));
   hs_out->n = hs.n;
@@ -125,7 +125,7 @@ void partition_level_t(Ctx& c, const K* keys, const uint32_t* vals, int64_t n, i
   if (hs.error) fail(SR_ERR_INTERNAL, "plan kernel inconsistency");
   DevStats forced = hs;
   forced.noneq_total = 1;  // never skip: the step must write every range key
-  s.level_scatter(L, forced);
+  s.level_scatter(L, &forced);
   // fill the equality buckets' keys (the scatter moves only their payloads)
   std::vector<Item> items(hs.n_items);
   if (hs.n_items)
@@ -141,8 +141,14 @@ void partition_level_t(Ctx& c, const K* keys, const uint32_t* vals, int64_t n, i
     c.upload(d_cnt, cnt);
     s.finish(d_items, d_cnt, 0, (int64_t)fills.size(), 0);
   }
-  // bucket counts from the scanned matrix (first chunk column of every bin)
   const SegDesc& sd = L.segs[0];
+  if (L.atomic) {  // keys only: bucket totals
+    std::vector<uint32_t> tot(sd.nbins);
+    check_cuda(cudaMemcpy(tot.data(), L.d_tot, tot.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    for (int b = 0; b < 2 * nbk + 1; b++) counts[b] = b < sd.nbins ? tot[b] : 0;
+    return;
+  }
+  // bucket counts from the scanned matrix (first chunk column of every bin)
   std::vector<uint32_t> mat((size_t)sd.nbins * sd.nchunks);
   check_cuda(cudaMemcpy(mat.data(), L.d_mat, mat.size() * 4, cudaMemcpyDeviceToHost), "d2h");
   for (int b = 0; b < 2 * nbk + 1; b++) {

@@ -18,6 +18,7 @@
 //       -> buckets <= kCap are finished by the CTA tile
 //      sort (K11) with an is_sorted skip.
 #pragma once
+#include "bitonic.cuh"
 #include "block_sort.cuh"
 #include "common.cuh"
 #include "presort.cuh"
@@ -86,60 +87,90 @@ __device__ void smem_scan(T* a, int L, T identity, Op op, bool exclusive, bool r
 }
 
 // ---------------------------------------------------------------------------
-// K7: splitters for every segment of a level (one CTA per segment).
-template <typename K, int NT, int VT>
-__global__ void __launch_bounds__(NT) k_splitters(const K* __restrict__ src, const SegDesc* __restrict__ segs,
-                                                   int oversample, K* __restrict__ spl_out,
-                                                   uint8_t* __restrict__ eq_out, int* __restrict__ m_out) {
-  using BS = BlockSort<K, false, NT, VT>;
+// K7: splitters for every segment of a level, in two kernels.
+//
+// K7a ranks the S-key sample without sorting it: rank(i) = #{j : (s_j, j) <
+// (s_i, i)}, the position of sample i in the stably sorted sample.  Grid =
+// (S/NT) x J x segments; each CTA gathers one of J chunks of the sample into
+// shared memory and every thread counts, for its own sample key, the chunk
+// keys ordered before it (<= for j < i, < for j > i), then adds the partial
+// count to rank[i].  O(S^2) compare+add pairs spread over the whole GPU, no
+// serial merge levels.
+template <typename K, int NT, int J>
+__global__ void __launch_bounds__(NT) k_sample_rank(const K* __restrict__ src, const SegDesc* __restrict__ segs,
+                                                     int oversample, uint32_t* __restrict__ rank,
+                                                     K* __restrict__ sample, const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
+  __shared__ K s_chunk[kMaxSample / J + 4];
+  const SegDesc seg = segs[blockIdx.z];
+  int64_t S64 = (int64_t)seg.nbuckets * oversample;
+  if (S64 > seg.len) S64 = seg.len;
+  if (S64 > kMaxSample) S64 = kMaxSample;
+  const int S = (int)S64;
+  const int i0 = blockIdx.x * NT;
+  if (i0 >= S) return;
+  const int log2S = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
+  const int cj = (S + J - 1) / J;
+  const int j0 = blockIdx.y * cj;
+  const int j1 = j0 + cj < S ? j0 + cj : S;
+  if (j0 >= j1) return;
+  const int len = j1 - j0;
+  for (int jj = threadIdx.x; jj < len; jj += NT)
+    s_chunk[jj] = src[sample_position(seg.start, seg.len, S, j0 + jj, log2S)];
+  const int i = i0 + threadIdx.x;
+  K x = i < S ? src[sample_position(seg.start, seg.len, S, i, log2S)] : K(0);
+  if (blockIdx.y == 0 && i < S) sample[seg.sample_base + i] = x;
+  __syncthreads();
+  if (i < S) {
+    const int split = i - j0 < 0 ? 0 : (i - j0 > len ? len : i - j0);  // chunk keys before i: [0, split)
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+    int jj = 0;
+    for (; jj + 4 <= split; jj += 4) {
+      r0 += s_chunk[jj] <= x; r1 += s_chunk[jj + 1] <= x; r2 += s_chunk[jj + 2] <= x; r3 += s_chunk[jj + 3] <= x;
+    }
+    for (; jj < split; jj++) r0 += s_chunk[jj] <= x;
+    jj = (i >= j0 && i < j1) ? split + 1 : split;
+    for (; jj + 4 <= len; jj += 4) {
+      r0 += s_chunk[jj] < x; r1 += s_chunk[jj + 1] < x; r2 += s_chunk[jj + 2] < x; r3 += s_chunk[jj + 3] < x;
+    }
+    for (; jj < len; jj++) r0 += s_chunk[jj] < x;
+    const uint32_t r = r0 + r1 + r2 + r3;
+    atomicAdd(&rank[seg.sample_base + i], r);
+  }
+}
+
+// K7b: one CTA per segment places the sample at its ranks (the sorted sample),
+// then splitter t_j = sorted[((j+1)*S)/B], j = 0..B-2, with the equality flag
+// set when t_j occurs more than gamma = 2 times in the sample,
+// i.e. when three consecutive sorted samples around position r equal t_j.
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT) k_select_splitters(const SegDesc* __restrict__ segs, int oversample,
+                                                          const uint32_t* __restrict__ rank,
+                                                          const K* __restrict__ sample, K* __restrict__ spl_out,
+                                                          uint8_t* __restrict__ eq_out, int* __restrict__ m_out,
+                                                          const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* ks = reinterpret_cast<K*>(smem_raw);
-  __shared__ int32_t s_red[NT / 32 + 1];
-  __shared__ int s_m;
+  K* sorted = reinterpret_cast<K*>(smem_raw);
   const SegDesc seg = segs[blockIdx.x];
   const int B = seg.nbuckets;
   int64_t S64 = (int64_t)B * oversample;
   if (S64 > seg.len) S64 = seg.len;
-  if (S64 > BS::NV) S64 = BS::NV;
+  if (S64 > kMaxSample) S64 = kMaxSample;
   const int S = (int)S64;
-  for (int k = threadIdx.x; k < S; k += NT) ks[pad_idx<K>(k)] = src[sample_position(seg.start, seg.len, S, k)];
+  for (int i = threadIdx.x; i < S; i += NT) sorted[rank[seg.sample_base + i]] = sample[seg.sample_base + i];
   __syncthreads();
-  BS::sort(ks, nullptr, S);
-  // candidates c_j = sample[((j+1)*S)/B], j = 0..B-2; keep the first of equal runs
-  const int ncand = B - 1;
-  const int j0 = threadIdx.x * 2;
-  K c[2];
-  int f[2];
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    int j = j0 + u;
-    f[u] = 0;
-    if (j < ncand) {
-      c[u] = ks[pad_idx<K>((int)(((int64_t)(j + 1) * S) / B))];
-      f[u] = (j == 0) ? 1 : (ks[pad_idx<K>((int)(((int64_t)j * S) / B))] != c[u]);
-    }
-  }
-  int32_t tot;
-  int32_t ex = block_exclusive_sum<NT>(f[0] + f[1], s_red, &tot);
   K* out = spl_out + (int64_t)blockIdx.x * kMaxBuckets;
   uint8_t* eo = eq_out + (int64_t)blockIdx.x * kMaxBuckets;
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    if (f[u]) {
-      // occurrences of c in the sorted sample: upper_bound - lower_bound
-      int lo = 0, hi = S;
-      while (lo < hi) { int mid = (lo + hi) >> 1; if (ks[pad_idx<K>(mid)] < c[u]) lo = mid + 1; else hi = mid; }
-      int lb = lo;
-      hi = S;
-      while (lo < hi) { int mid = (lo + hi) >> 1; if (c[u] < ks[pad_idx<K>(mid)]) hi = mid; else lo = mid + 1; }
-      out[ex] = c[u];
-      eo[ex] = (lo - lb) > 2 ? 1 : 0;  // gamma = 2
-      ex++;
-    }
+  for (int j = threadIdx.x; j < B - 1; j += NT) {
+    const int r = (int)(((int64_t)(j + 1) * S) / B);
+    const K t = sorted[r];
+    const bool m1 = r >= 1 && sorted[r - 1] == t, m2 = r >= 2 && sorted[r - 2] == t;
+    const bool p1 = r + 1 < S && sorted[r + 1] == t, p2 = r + 2 < S && sorted[r + 2] == t;
+    out[j] = t;
+    eo[j] = ((m1 && m2) || (m1 && p1) || (p1 && p2)) ? 1 : 0;  // count > gamma = 2
   }
-  if (threadIdx.x == 0) s_m = tot;
-  __syncthreads();
-  if (threadIdx.x == 0) m_out[blockIdx.x] = s_m;
+  if (threadIdx.x == 0) m_out[blockIdx.x] = B - 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -148,8 +179,10 @@ template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const SegDesc* __restrict__ segs,
                                                const int* __restrict__ chunk_seg, int64_t chunk_size,
                                                const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
-                                               const int* __restrict__ m_all, uint32_t* __restrict__ mat) {
-  constexpr int U = 4;
+                                               const int* __restrict__ m_all, uint32_t* __restrict__ mat,
+                                               uint32_t* __restrict__ tot, const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
+  constexpr int U = 8;
   __shared__ K s_spl[kMaxBuckets];
   __shared__ uint8_t s_eq[kMaxBuckets];
   __shared__ uint32_t s_hist[kMaxBins];
@@ -158,8 +191,7 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
   const SegDesc seg = segs[s];
   const int g = c - seg.chunk_base;
   const int m = m_all[s];
-  int P2;
-  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, s_spl, s_eq, P2);
+  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, s_spl, s_eq);
   for (int b = threadIdx.x; b < seg.nbins; b += NT) s_hist[b] = 0;
   __syncthreads();
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
@@ -171,16 +203,18 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
       int64_t i = base + u * NT + threadIdx.x;
       x[u] = i < c1 ? src[i] : K(0);
     }
+    int bin[U];
+    classify_keys<K, U>(x, bin, s_spl, s_eq, m);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      int64_t i = base + u * NT + threadIdx.x;
-      bool valid = i < c1;
-      int bin = valid ? classify_key<K>(x[u], s_spl, s_eq, m, P2) : 0;
-      hist_add(s_hist, bin, valid);
-    }
+    for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], base + u * NT + threadIdx.x < c1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < seg.nbins; b += NT) mat[seg.mat_base + (int64_t)b * seg.nchunks + g] = s_hist[b];
+  if (tot) {  // keys only: per-segment bucket totals at bin base seg.mat_base
+    for (int b = threadIdx.x; b < seg.nbins; b += NT)
+      if (s_hist[b]) atomicAdd(&tot[seg.mat_base + b], s_hist[b]);
+  } else {
+    for (int b = threadIdx.x; b < seg.nbins; b += NT) mat[seg.mat_base + (int64_t)b * seg.nchunks + g] = s_hist[b];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -188,10 +222,12 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
 // status[] and *tile_counter must be zero before launch.
 template <int NT, int IPT>
 __global__ void __launch_bounds__(NT) k_scan_u32(uint32_t* __restrict__ data, int64_t count,
-                                                  unsigned long long* __restrict__ status, int* __restrict__ tile_counter) {
+                                                  unsigned long long* __restrict__ status, int* __restrict__ tile_counter,
+                                                  const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
   __shared__ int s_tile;
   __shared__ uint32_t s_red[NT / 32 + 1];
-  __shared__ uint32_t s_stage[NT * IPT];
+  __shared__ uint32_t s_stage[NT * IPT + NT * IPT / 32 + 1];
   __shared__ uint32_t s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
   __syncthreads();
@@ -199,44 +235,47 @@ __global__ void __launch_bounds__(NT) k_scan_u32(uint32_t* __restrict__ data, in
   const int64_t base = (int64_t)tile * NT * IPT;
   for (int i = threadIdx.x; i < NT * IPT; i += NT) {
     int64_t p = base + i;
-    s_stage[i] = p < count ? data[p] : 0u;
+    s_stage[pad_idx<uint32_t>(i)] = p < count ? data[p] : 0u;
   }
   __syncthreads();
   uint32_t v[IPT];
   uint32_t sum = 0;
 #pragma unroll
-  for (int i = 0; i < IPT; i++) { v[i] = s_stage[threadIdx.x * IPT + i]; sum += v[i]; }
+  for (int i = 0; i < IPT; i++) { v[i] = s_stage[pad_idx<uint32_t>(threadIdx.x * IPT + i)]; sum += v[i]; }
   uint32_t agg;
   uint32_t ex = block_exclusive_sum<NT>(sum, s_red, &agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-parallel look-back: lanes inspect 32 predecessors at a time
     volatile unsigned long long* vs = status;
+    const int lane = threadIdx.x;
+    if (lane == 0) vs[tile] = ((tile == 0 ? 2ull : 1ull) << 32) | agg;
     uint32_t prefix = 0;
-    if (tile == 0) {
-      vs[0] = (2ull << 32) | agg;
-    } else {
-      vs[tile] = (1ull << 32) | agg;
-      int j = tile - 1;
-      while (true) {
-        unsigned long long sv = vs[j];
-        unsigned flag = (unsigned)(sv >> 32);
-        if (flag == 0) continue;
-        prefix += (uint32_t)sv;
-        if (flag == 2) break;
-        j--;
-      }
-      __threadfence();
-      vs[tile] = (2ull << 32) | (uint32_t)(prefix + agg);
+    int j = tile - 1;
+    while (j >= 0) {
+      const int idx = j - lane;
+      unsigned long long sv = idx >= 0 ? vs[idx] : (2ull << 32);
+      unsigned flag = (unsigned)(sv >> 32);
+      if (__any_sync(0xffffffffu, flag == 0)) continue;  // a predecessor has not published yet
+      unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+      int stop = incl ? __ffs(incl) - 1 : 31;
+      uint32_t val = lane <= stop ? (uint32_t)sv : 0u;
+      prefix += warp_reduce_sum(val);
+      if (incl) break;
+      j -= 32;
     }
-    s_prefix = prefix;
+    if (lane == 0) {
+      if (tile > 0) vs[tile] = (2ull << 32) | (uint32_t)(prefix + agg);
+      s_prefix = prefix;
+    }
   }
   __syncthreads();
   uint32_t run = s_prefix + ex;
 #pragma unroll
-  for (int i = 0; i < IPT; i++) { s_stage[threadIdx.x * IPT + i] = run; run += v[i]; }
+  for (int i = 0; i < IPT; i++) { s_stage[pad_idx<uint32_t>(threadIdx.x * IPT + i)] = run; run += v[i]; }
   __syncthreads();
   for (int i = threadIdx.x; i < NT * IPT; i += NT) {
     int64_t p = base + i;
-    if (p < count) data[p] = s_stage[i];
+    if (p < count) data[p] = s_stage[pad_idx<uint32_t>(i)];
   }
 }
 
@@ -252,39 +291,72 @@ __global__ void __launch_bounds__(NT) k_scan_u32(uint32_t* __restrict__ data, in
 //      union of consecutive buckets equals sorting each one).
 enum : uint8_t { kBinEmpty = 0, kBinFill = 1, kBinOvf = 2, kBinBig = 3, kBinSmall = 4 };
 
+struct PlanSmem {
+  int32_t p[kMaxBins + 1];
+  int32_t epoch[kMaxBins];
+  int32_t prev[kMaxBins];
+  int32_t next[kMaxBins + 1];
+  uint8_t type[kMaxBins];
+};
+
+// Per-thread slot reservation in one of the item lists: block scan + one
+// global atomic per block.
+template <int NT>
+__device__ __forceinline__ int64_t reserve_slots(int mine, unsigned long long* counter, int32_t* s_red, long long* s_base) {
+  int32_t tot;
+  int32_t ex = block_exclusive_sum<NT>(mine, s_red, &tot);
+  if (threadIdx.x == 0) *s_base = tot ? (long long)atomicAdd(counter, (unsigned long long)tot) : 0;
+  __syncthreads();
+  int64_t r = *s_base + ex;
+  __syncthreads();
+  return r;
+}
+
 template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ mat,
                                               const K* __restrict__ spl_all, const int* __restrict__ m_all,
-                                              int buf, Item* __restrict__ items, OvfSeg* __restrict__ ovf,
-                                              DevStats* __restrict__ st) {
-  __shared__ int32_t s_p[kMaxBins + 1];
-  __shared__ uint8_t s_type[kMaxBins];
-  __shared__ int32_t s_epoch[kMaxBins];
-  __shared__ int32_t s_prev[kMaxBins];
-  __shared__ int32_t s_next[kMaxBins + 1];
+                                              int buf, Item* __restrict__ items, Item* __restrict__ items_big,
+                                              OvfSeg* __restrict__ ovf, DevStats* __restrict__ st,
+                                              const uint32_t* __restrict__ tot, uint32_t* __restrict__ cursor,
+                                              const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanSmem& sm = *reinterpret_cast<PlanSmem*>(smem_raw);
   __shared__ int32_t s_red[NT / 32 + 1];
   __shared__ long long s_red64[NT / 32 + 1];
+  __shared__ long long s_base;
   const SegDesc seg = segs[blockIdx.x];
   const int nb = seg.nbins;
   const int G = seg.nchunks;
   const int64_t send = seg.start + seg.len;
-  constexpr int H = kCap / 2;
-  for (int b = threadIdx.x; b < nb; b += NT)
-    s_p[b] = (int32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * G] - seg.len_prefix));
-  if (threadIdx.x == 0) s_p[nb] = (int32_t)send;
+  constexpr int H = kPack;
+  if (tot) {
+    // keys only: bucket starts = seg.start + exclusive scan of the totals
+    for (int b = threadIdx.x; b < nb; b += NT) sm.p[b] = (int32_t)tot[seg.mat_base + b];
+    __syncthreads();
+    smem_scan<NT>(sm.p, nb, 0, [](int32_t a, int32_t b) { return a + b; }, true, false, s_red);
+    for (int b = threadIdx.x; b < nb; b += NT) {
+      sm.p[b] += (int32_t)seg.start;
+      cursor[seg.mat_base + b] = (uint32_t)sm.p[b];
+    }
+  } else {
+    for (int b = threadIdx.x; b < nb; b += NT)
+      sm.p[b] = (int32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * G] - seg.len_prefix));
+  }
+  if (threadIdx.x == 0) sm.p[nb] = (int32_t)send;
   __syncthreads();
   long long noneq = 0, eqk = 0, ovk = 0;
   for (int b = threadIdx.x; b < nb; b += NT) {
-    int c = s_p[b + 1] - s_p[b];
+    int c = sm.p[b + 1] - sm.p[b];
     uint8_t ty;
     if (b & 1) ty = c > 0 ? kBinFill : kBinEmpty;
     else if (c == 0) ty = kBinEmpty;
     else if (c > kCap) ty = kBinOvf;
-    else if (c > H) ty = kBinBig;
+    else if (c > kPack) ty = kBinBig;
     else ty = kBinSmall;
-    s_type[b] = ty;
-    s_epoch[b] = (ty == kBinFill || ty == kBinOvf || ty == kBinBig) ? 1 : 0;
-    s_prev[b] = ty == kBinSmall ? b : -1;
+    sm.type[b] = ty;
+    sm.epoch[b] = (ty == kBinFill || ty == kBinOvf || ty == kBinBig) ? 1 : 0;
+    sm.prev[b] = ty == kBinSmall ? b : -1;
     if (b & 1) eqk += c; else noneq += c;
     if (ty == kBinOvf) ovk += c;
   }
@@ -292,48 +364,65 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
   auto add = [](int32_t a, int32_t b) { return a + b; };
   auto mx = [](int32_t a, int32_t b) { return a > b ? a : b; };
   auto mn = [](int32_t a, int32_t b) { return a < b ? a : b; };
-  smem_scan<NT>(s_epoch, nb, 0, add, true, false, s_red);   // separators before b
-  smem_scan<NT>(s_prev, nb, -1, mx, true, false, s_red);    // last small bin before b
+  smem_scan<NT>(sm.epoch, nb, 0, add, true, false, s_red);   // separators before b
+  smem_scan<NT>(sm.prev, nb, -1, mx, true, false, s_red);    // last small bin before b
   // chunk heads and boundaries
   for (int b = threadIdx.x; b < nb; b += NT) {
     bool head = false;
-    if (s_type[b] == kBinSmall) {
-      int pv = s_prev[b];
-      head = pv < 0 || s_epoch[pv] != s_epoch[b] ||
-             (s_p[pv] - (int32_t)seg.start) / H != (s_p[b] - (int32_t)seg.start) / H;
+    if (sm.type[b] == kBinSmall) {
+      int pv = sm.prev[b];
+      head = pv < 0 || sm.epoch[pv] != sm.epoch[b] ||
+             (sm.p[pv] - (int32_t)seg.start) / H != (sm.p[b] - (int32_t)seg.start) / H;
     }
-    uint8_t ty = s_type[b];
+    uint8_t ty = sm.type[b];
     bool bound = head || ty == kBinFill || ty == kBinOvf || ty == kBinBig;
-    s_next[b] = bound ? s_p[b] : (int32_t)send;
-    if (head) s_type[b] = kBinSmall | 0x80;
+    sm.next[b] = bound ? sm.p[b] : (int32_t)send;
+    if (head) sm.type[b] = kBinSmall | 0x80;
   }
   __syncthreads();
-  smem_scan<NT>(s_next, nb, (int32_t)send, mn, false, true, s_red);  // suffix min
+  smem_scan<NT>(sm.next, nb, (int32_t)send, mn, false, true, s_red);  // suffix min
+  // item lengths per bin (0 = no item); fills split into kFillChunk pieces
+  constexpr int IPT = (kMaxBins + NT - 1) / NT;
+  int n_small = 0, n_big = 0, n_ovf = 0;
+  for (int k = 0; k < IPT; k++) {
+    int b = threadIdx.x + k * NT;
+    if (b >= nb) break;
+    uint8_t ty = sm.type[b];
+    int c = sm.p[b + 1] - sm.p[b];
+    int len = ty == (kBinSmall | 0x80) ? ((b + 1 < nb ? sm.next[b + 1] : (int32_t)send) - sm.p[b])
+                                       : (ty == kBinBig ? c : 0);
+    if (len) (len <= kSmallItem ? n_small : n_big)++;
+    if (ty == kBinFill) n_small += (c + kFillChunk - 1) / kFillChunk;
+    if (ty == kBinOvf) n_ovf++;
+  }
+  int64_t o_small = reserve_slots<NT>(n_small, (unsigned long long*)&st->n_items, s_red, &s_base);
+  int64_t o_big = reserve_slots<NT>(n_big, (unsigned long long*)&st->n_items_big, s_red, &s_base);
+  int64_t o_ovf = reserve_slots<NT>(n_ovf, (unsigned long long*)&st->n_ovf, s_red, &s_base);
   const int m = m_all[blockIdx.x];
   const K* spl = spl_all + (int64_t)blockIdx.x * kMaxBuckets;
-  for (int b = threadIdx.x; b < nb; b += NT) {
-    uint8_t ty = s_type[b];
-    int c = s_p[b + 1] - s_p[b];
-    if (ty == (kBinSmall | 0x80)) {
-      int end = b + 1 < nb ? s_next[b + 1] : (int32_t)send;
-      unsigned long long slot = atomicAdd((unsigned long long*)&st->n_items, 1ull);
-      Item it; it.start = s_p[b]; it.len = end - s_p[b]; it.kind = kItemSort | (buf << 4); it.key = 0;
-      items[slot] = it;
-    } else if (ty == kBinBig) {
-      unsigned long long slot = atomicAdd((unsigned long long*)&st->n_items, 1ull);
-      Item it; it.start = s_p[b]; it.len = c; it.kind = kItemSort | (buf << 4); it.key = 0;
-      items[slot] = it;
+  for (int k = 0; k < IPT; k++) {
+    int b = threadIdx.x + k * NT;
+    if (b >= nb) break;
+    uint8_t ty = sm.type[b];
+    int c = sm.p[b + 1] - sm.p[b];
+    int len = ty == (kBinSmall | 0x80) ? ((b + 1 < nb ? sm.next[b + 1] : (int32_t)send) - sm.p[b])
+                                       : (ty == kBinBig ? c : 0);
+    if (len) {
+      Item it;
+      it.start = sm.p[b]; it.len = len; it.kind = kItemSort | (buf << 4); it.key = 0;
+      if (len <= kSmallItem) items[o_small++] = it; else items_big[o_big++] = it;
     } else if (ty == kBinFill) {
-      unsigned long long slot = atomicAdd((unsigned long long*)&st->n_items, 1ull);
       int i = (b - 1) / 2;
-      Item it; it.start = s_p[b]; it.len = c; it.kind = kItemFill | (buf << 4);
-      it.key = i < m ? (int64_t)spl[i] : 0;
       if (i >= m) atomicAdd((unsigned long long*)&st->error, 1ull);
-      items[slot] = it;
+      for (int f = 0; f < c; f += kFillChunk) {
+        Item it;
+        it.start = sm.p[b] + f; it.len = min(kFillChunk, c - f); it.kind = kItemFill | (buf << 4);
+        it.key = i < m ? (int64_t)spl[i] : 0;
+        items[o_small++] = it;
+      }
     } else if (ty == kBinOvf) {
-      unsigned long long slot = atomicAdd((unsigned long long*)&st->n_ovf, 1ull);
-      OvfSeg o; o.start = s_p[b]; o.len = c;
-      ovf[slot] = o;
+      OvfSeg o; o.start = sm.p[b]; o.len = c;
+      ovf[o_ovf++] = o;
     }
   }
   noneq = block_reduce_sum<NT>(noneq, s_red64);
@@ -376,8 +465,11 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
                                                  const SegDesc* __restrict__ segs, const int* __restrict__ chunk_seg,
                                                  int64_t chunk_size, const K* __restrict__ spl_all,
                                                  const uint8_t* __restrict__ eq_all, const int* __restrict__ m_all,
-                                                 const uint32_t* __restrict__ mat) {
+                                                 const uint32_t* __restrict__ mat, const DevStats* __restrict__ gate) {
   using SM = ScatterSmem<K, HAS_V, NT, VTS>;
+  // speculative launch: only on the partition route, and keys-only with every
+  // key in an equality bucket needs no scatter at all
+  if (gate && (gate->route != kRoutePartition || (!HAS_V && gate->noneq_total == 0))) return;
   constexpr int NW = SM::NW;
   constexpr int ST = SM::ST;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -389,8 +481,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
   const int g = c - seg.chunk_base;
   const int nb = seg.nbins;
   const int m = m_all[s];
-  int P2;
-  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq, P2);
+  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
   for (int b = tid; b < nb; b += NT)
     sm.cur[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * seg.nchunks + g] - seg.len_prefix));
   __syncthreads();
@@ -414,7 +505,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
       bool valid = pos < c1;
-      int b = valid ? classify_key<K>(x[i], sm.spl, sm.eq, m, P2) : kMaxBins;
+      int b = valid ? classify_key<K>(x[i], sm.spl, sm.eq, m) : kMaxBins;
       unsigned peers = __match_any_sync(0xffffffffu, b);
       int base = sm.wcnt[w][b];
       rk[i] = base + __popc(peers & lt);
@@ -462,19 +553,130 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
 }
 
 // ---------------------------------------------------------------------------
+// K10 (keys only): 3-way scatter with atomic bucket reservation.  Equal keys
+// are indistinguishable, so the order inside a range bucket is irrelevant (the
+// finishing sort fixes it) and keys of equality buckets are not written at all
+// (the fill writes them; "spared from the recursive calls").  Per
+// sub-tile: classify, rank inside the CTA with shared-memory atomics, reserve
+// each bucket's slice with one global atomic on its cursor, stage in bucket
+// order, write contiguous slices.
+template <typename K, int NT, int VTS>
+struct ScatterKeysSmem {
+  static constexpr int ST = NT * VTS;
+  K spl[kMaxBuckets];
+  K stk[ST];
+  uint32_t cnt[kMaxBins];
+  uint32_t lstart[kMaxBins];
+  uint32_t base[kMaxBins];
+  uint16_t stb[ST];
+  uint8_t eq[kMaxBuckets];
+  uint32_t red[NT / 32 + 1];
+  uint32_t total;
+};
+
+template <typename K, int NT, int VTS>
+__global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, K* __restrict__ dst,
+                                                      const SegDesc* __restrict__ segs,
+                                                      const int* __restrict__ chunk_seg, int64_t chunk_size,
+                                                      const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
+                                                      const int* __restrict__ m_all, uint32_t* __restrict__ cursor,
+                                                      const DevStats* __restrict__ gate) {
+  if (gate && (gate->route != kRoutePartition || gate->noneq_total == 0)) return;
+  using SM = ScatterKeysSmem<K, NT, VTS>;
+  constexpr int ST = SM::ST;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x;
+  const int s = chunk_seg[c];
+  const SegDesc seg = segs[s];
+  const int g = c - seg.chunk_base;
+  const int nb = seg.nbins;
+  const int m = m_all[s];
+  uint32_t* cur = cursor + seg.mat_base;
+  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
+  const int64_t c0 = seg.start + (int64_t)g * chunk_size;
+  const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
+  for (int64_t sub = c0; sub < c1; sub += ST) {
+    for (int b = tid; b < nb; b += NT) sm.cnt[b] = 0;
+    __syncthreads();
+    K x[VTS];
+    int bin[VTS];
+    uint32_t rk[VTS];
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      int64_t pos = sub + i * NT + tid;
+      x[i] = pos < c1 ? src[pos] : K(0);
+    }
+    classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m);
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      int64_t pos = sub + i * NT + tid;
+      // range buckets only; equality buckets are filled later
+      if (pos >= c1 || (bin[i] & 1)) bin[i] = -1;
+      else rk[i] = atomicAdd(&sm.cnt[bin[i]], 1u);
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += NT) {
+      uint32_t cb = sm.cnt[b];
+      sm.lstart[b] = cb;
+      if (cb) sm.base[b] = atomicAdd(&cur[b], cb);
+    }
+    __syncthreads();
+    smem_scan<NT>(sm.lstart, nb, 0u, [](uint32_t a, uint32_t b) { return a + b; }, true, false, sm.red);
+    if (tid == 0) sm.total = sm.lstart[nb - 1] + sm.cnt[nb - 1];
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      if (bin[i] >= 0) {
+        uint32_t lp = sm.lstart[bin[i]] + rk[i];
+        sm.stk[lp] = x[i];
+        sm.stb[lp] = (uint16_t)bin[i];
+      }
+    }
+    __syncthreads();
+    const int tot = (int)sm.total;
+    for (int p = tid; p < tot; p += NT) {
+      int b = sm.stb[p];
+      dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K11: finishing (H11 + H4 segmented).  Persistent CTAs walk the item list:
 // fills write the equality value (and move payloads); sorts load the range
 // into shared memory, skip the sort when it is already ordered (is_sorted at
 // every call) and otherwise run the stable tile sort, then
-// write into the caller's buffers.
+// write into the caller's buffers.  Items of up to 2*NV keys sort both halves
+// in shared memory and merge them straight into global memory.
 template <typename K, bool HAS_V, int NT, int VT>
+struct FinishSmem {
+  static constexpr int NV = NT * VT;
+  // keys only: two bitonic halves, the second one's double buffer above the first;
+  // pairs: two stable merge-sorted halves plus payloads
+  static constexpr int KEYS = HAS_V ? 2 * NV + VT : 3 * NV + VT;
+  static constexpr int VALS = HAS_V ? 2 * NV + VT : 1;
+  static constexpr size_t bytes() { return sizeof(K) * KEYS + 4 * VALS; }
+};
+
+template <typename K, bool HAS_V, int NT, int VT>
+__device__ __forceinline__ void finish_sort_smem(K* ks, uint32_t* vs, int len) {
+  if (HAS_V) BlockSort<K, HAS_V, NT, VT>::sort(ks, vs, len);
+  else BitonicSort<K, NT, VT>::sort(ks, len);
+}
+
+template <typename K, bool HAS_V, int NT, int VT, bool TWO_HALVES>
 __global__ void __launch_bounds__(NT) k_finish(const Item* __restrict__ items, const int64_t* __restrict__ count_ptr,
                                                 int64_t item_begin, K* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                const K* __restrict__ ws_k, const uint32_t* __restrict__ ws_v) {
-  using BS = BlockSort<K, HAS_V, NT, VT>;
+                                                const K* __restrict__ ws_k, const uint32_t* __restrict__ ws_v,
+                                                const DevStats* __restrict__ gate, int64_t gate_route) {
+  if (gate && gate->route != gate_route) return;  // speculative launch on another route
+  using FS = FinishSmem<K, HAS_V, NT, VT>;
+  constexpr int NV = NT * VT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* ks = reinterpret_cast<K*>(smem_raw);
-  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * BS::KEYS_SMEM);
+  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * FS::KEYS);
   const int64_t count = *count_ptr - item_begin;
   for (int64_t it = blockIdx.x; it < count; it += gridDim.x) {
     const Item item = items[item_begin + it];
@@ -490,21 +692,58 @@ __global__ void __launch_bounds__(NT) k_finish(const Item* __restrict__ items, c
       }
       continue;
     }
-    const K* sk = from_ws ? ws_k : keys;
-    const uint32_t* sv = from_ws ? ws_v : vals;
-    for (int i = threadIdx.x; i < len; i += NT) {
-      ks[pad_idx<K>(i)] = sk[s + i];
-      if (HAS_V) vs[pad_idx<uint32_t>(i)] = sv[s + i];
+    const K* sk = (from_ws ? ws_k : keys) + s;
+    const uint32_t* sv = (from_ws ? ws_v : vals) + s;
+    K* dk = keys + s;
+    uint32_t* dv = vals + s;
+    const int first = (!TWO_HALVES || len <= NV) ? len : NV;
+    for (int i = threadIdx.x; i < first; i += NT) {
+      ks[i] = sk[i];
+      if (HAS_V) vs[i] = sv[i];
     }
-    __syncthreads();
+    // is_sorted, read straight from the source range
     int unsorted = 0;
-    for (int i = threadIdx.x; i + 1 < len; i += NT) unsorted |= ks[pad_idx<K>(i + 1)] < ks[pad_idx<K>(i)];
+    for (int i = threadIdx.x; i + 1 < len; i += NT) unsorted |= sk[i + 1] < sk[i];
     unsorted = __syncthreads_or(unsorted);
-    if (unsorted) BS::sort(ks, vs, len);
-    if (unsorted || from_ws) {
+    if (!unsorted) {
+      if (from_ws)
+        for (int i = threadIdx.x; i < len; i += NT) {
+          dk[i] = sk[i];
+          if (HAS_V) dv[i] = sv[i];
+        }
+      __syncthreads();
+      continue;
+    }
+    if (!TWO_HALVES || len <= NV) {  // small-item kernels never see len > NV
+      finish_sort_smem<K, HAS_V, NT, VT>(ks, vs, len);
       for (int i = threadIdx.x; i < len; i += NT) {
-        keys[s + i] = ks[pad_idx<K>(i)];
-        if (HAS_V) vals[s + i] = vs[pad_idx<uint32_t>(i)];
+        dk[i] = ks[i];
+        if (HAS_V) dv[i] = vs[i];
+      }
+    } else {
+      // two halves sorted in shared memory, then one merge level written
+      // straight to global memory
+      finish_sort_smem<K, HAS_V, NT, VT>(ks, vs, NV);
+      const int nb = len - NV;
+      for (int i = threadIdx.x; i < nb; i += NT) {
+        ks[NV + i] = sk[NV + i];
+        if (HAS_V) vs[NV + i] = sv[NV + i];
+      }
+      __syncthreads();
+      finish_sort_smem<K, HAS_V, NT, VT>(ks + NV, vs + NV, nb);
+      for (int d0 = threadIdx.x * VT; d0 < len; d0 += NT * VT) {
+        int mp = merge_path_search<K>([&](int i) { return ks[i]; }, NV, [&](int i) { return ks[NV + i]; }, nb, d0);
+        int ai = mp, bi = d0 - mp;
+#pragma unroll
+        for (int i = 0; i < VT; i++) {
+          if (d0 + i < len) {
+            const bool p = (bi >= nb) || (ai < NV && !(ks[NV + bi] < ks[ai]));
+            dk[d0 + i] = p ? ks[ai] : ks[NV + bi];
+            if (HAS_V) dv[d0 + i] = p ? vs[ai] : vs[NV + bi];
+            ai += p;
+            bi += !p;
+          }
+        }
       }
     }
     __syncthreads();

@@ -18,36 +18,47 @@ namespace sr {
 // (3-way split, switched on per splitter by the gamma test
 // of PAPER.md:168), else 2i.
 template <typename K>
-__device__ __forceinline__ int classify_key(K x, const K* spl, const uint8_t* eqf, int m, int P2) {
+__device__ __forceinline__ int classify_key(K x, const K* spl, const uint8_t* eqf, int m) {
   int i = 0;
-  for (int step = P2 >> 1; step > 0; step >>= 1)
+#pragma unroll
+  for (int step = kMaxBuckets / 2; step > 0; step >>= 1)
     if (spl[i + step - 1] < x) i += step;
   return 2 * i + ((i < m && spl[i] == x && eqf[i]) ? 1 : 0);
 }
 
-__host__ __device__ __forceinline__ int pow2_above(int m) {  // smallest power of 2 >= m+1
-  int p = 1;
-  while (p < m + 1) p <<= 1;
-  return p;
+// Batched classification: the U searches advance in lockstep so their
+// shared-memory loads are independent and overlap (U-way ILP).
+template <typename K, int U>
+__device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], const K* spl, const uint8_t* eqf, int m) {
+  int idx[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) idx[u] = 0;
+#pragma unroll
+  for (int step = kMaxBuckets / 2; step > 0; step >>= 1) {
+#pragma unroll
+    for (int u = 0; u < U; u++) idx[u] += (spl[idx[u] + step - 1] < x[u]) ? step : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int i = idx[u];
+    bin[u] = 2 * i + ((i < m && spl[i] == x[u] && eqf[i]) ? 1 : 0);
+  }
 }
 
+// Splitters into shared memory, padded with +inf to kMaxBuckets-1 entries so
+// the search above always takes log2(kMaxBuckets) unrolled steps.
 template <typename K>
-__device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_spl, uint8_t* s_eq,
-                                                    int& P2) {
-  P2 = pow2_above(m);
-  for (int i = threadIdx.x; i < P2 - 1; i += blockDim.x) {
+__device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_spl,
+                                                    uint8_t* s_eq) {
+  for (int i = threadIdx.x; i < kMaxBuckets; i += blockDim.x) {
     s_spl[i] = i < m ? spl[i] : KeyTraits<K>::max_key();
     s_eq[i] = i < m ? eqf[i] : 0;
   }
 }
 
-// Warp-aggregated shared-memory histogram increment.
+// Shared-memory histogram increment (hardware-serialised on conflicts).
 __device__ __forceinline__ void hist_add(uint32_t* hist, int bin, bool valid) {
-  unsigned mask = __ballot_sync(0xffffffffu, valid);
-  if (valid) {
-    unsigned peers = __match_any_sync(mask, bin);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
-  }
+  if (valid) atomicAdd(&hist[bin], 1u);
 }
 
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
@@ -60,8 +71,9 @@ template <typename K, bool STRICT, bool FUSE, int NT>
 __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys, int64_t n, int tile,
                                                       TileSummary* __restrict__ sums, const K* __restrict__ spl,
                                                       const uint8_t* __restrict__ eqf, const int* __restrict__ mcount,
-                                                      uint32_t* __restrict__ mat, int nbins, int G) {
-  constexpr int U = 4;
+                                                      uint32_t* __restrict__ mat, int nbins, int G,
+                                                      uint32_t* __restrict__ tot) {
+  constexpr int U = 8;
   __shared__ K s_spl[FUSE ? kMaxBuckets : 1];
   __shared__ uint8_t s_eq[FUSE ? kMaxBuckets : 1];
   __shared__ uint32_t s_hist[FUSE ? kMaxBins : 1];
@@ -69,10 +81,10 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t t0 = (int64_t)blockIdx.x * tile;
   const int64_t t1 = t0 + tile < n ? t0 + tile : n;
-  int m = 0, P2 = 1;
+  int m = 0;
   if (FUSE) {
     m = mcount[0];
-    load_splitters_smem(spl, eqf, m, s_spl, s_eq, P2);
+    load_splitters_smem(spl, eqf, m, s_spl, s_eq);
     for (int b = tid; b < nbins; b += NT) s_hist[b] = 0;
     __syncthreads();
   }
@@ -95,11 +107,12 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
         bool brk = STRICT ? !(y < x[u]) : (x[u] < y);
         if (brk) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }
       }
-      if (FUSE) {
-        bool valid = i < t1;
-        int bin = valid ? classify_key<K>(x[u], s_spl, s_eq, m, P2) : 0;
-        hist_add(s_hist, bin, valid);
-      }
+    }
+    if (FUSE) {
+      int bin[U];
+      classify_keys<K, U>(x, bin, s_spl, s_eq, m);
+#pragma unroll
+      for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], base + u * NT + tid < t1);
     }
   }
   cd = block_reduce_sum<NT>(cd, s_red);
@@ -115,7 +128,12 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   }
   if (FUSE) {
     __syncthreads();
-    for (int b = tid; b < nbins; b += NT) mat[(int64_t)b * G + blockIdx.x] = s_hist[b];
+    if (tot) {  // keys only: bucket totals (no count matrix)
+      for (int b = tid; b < nbins; b += NT)
+        if (s_hist[b]) atomicAdd(&tot[b], s_hist[b]);
+    } else {
+      for (int b = tid; b < nbins; b += NT) mat[(int64_t)b * G + blockIdx.x] = s_hist[b];
+    }
   }
 }
 
@@ -125,7 +143,7 @@ template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ keys, int64_t n,
                                                          const TileSummary* __restrict__ sums, int G, int64_t lmin,
                                                          RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
-                                                         DevStats* __restrict__ st) {
+                                                         DevStats* __restrict__ st, int force, int merge_ok) {
   __shared__ int32_t s_incl[2][NT];
   __shared__ int64_t s_red64[NT / 32 + 1];
   __shared__ int32_t s_red[NT / 32 + 1];
@@ -205,6 +223,17 @@ __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ ke
     st->n_desc_runs = ndsc;
     st->asc_cover = covA;
     st->desc_cover = covD;
+    // device-side route (H3 first stage); kRouteUndecided hands the merge-vs-
+    // partition cost comparison to the host planner.
+    int64_t route;
+    if (D == 0) route = kRouteSorted;
+    else if (A == 0 && force == 0) route = kRouteReversed;
+    else if (force == kRouteMerge) route = kRouteMerge;
+    else if (n <= kCap) route = kRouteTile;
+    else if (force == kRoutePartition) route = kRoutePartition;
+    else if (merge_ok && 2 * (covA + covD) >= n) route = kRouteUndecided;
+    else route = kRoutePartition;
+    st->route = route;
   }
 }
 
@@ -215,23 +244,33 @@ __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ ke
 template <typename K, bool HAS_V, int NT>
 __global__ void __launch_bounds__(NT) k_reverse(K* __restrict__ keys, uint32_t* __restrict__ vals,
                                                  const RunDesc* __restrict__ ranges,
-                                                 const int64_t* __restrict__ chunk_prefix, int nranges) {
+                                                 const int64_t* __restrict__ chunk_prefix, int nranges,
+                                                 const DevStats* __restrict__ gate, int64_t whole_len) {
+  if (gate && gate->route != kRouteReversed) return;  // speculative launch
   constexpr int U = 8;
   constexpr int CH = NT * U;
-  __shared__ int s_r;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = nranges - 1;
-    while (lo < hi) {  // last r with chunk_prefix[r] <= blockIdx.x
-      int mid = (lo + hi + 1) >> 1;
-      if (chunk_prefix[mid] <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  int64_t s, len, c0;
+  if (!ranges) {  // the whole array [0, whole_len)
+    s = 0;
+    len = whole_len;
+    c0 = (int64_t)blockIdx.x * CH;
+  } else {
+    __shared__ int s_r;
+    if (threadIdx.x == 0) {
+      int lo = 0, hi = nranges - 1;
+      while (lo < hi) {  // last r with chunk_prefix[r] <= blockIdx.x
+        int mid = (lo + hi + 1) >> 1;
+        if (chunk_prefix[mid] <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+      }
+      s_r = lo;
     }
-    s_r = lo;
+    __syncthreads();
+    const int r = s_r;
+    s = ranges[r].start;
+    len = ranges[r].len;
+    c0 = ((int64_t)blockIdx.x - chunk_prefix[r]) * CH;
   }
-  __syncthreads();
-  const int r = s_r;
-  const int64_t s = ranges[r].start, len = ranges[r].len;
   const int64_t half = len / 2;
-  const int64_t c0 = ((int64_t)blockIdx.x - chunk_prefix[r]) * CH;
   K a[U], b[U];
   uint32_t va[U], vb[U];
 #pragma unroll

@@ -10,6 +10,8 @@
 //   long natural runs     -> MERGE if its simulated bytes beat PARTITION
 //   otherwise             -> PARTITION (levels until every bucket <= kCap)
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -44,9 +46,17 @@ struct ThreadState {
   cudaStream_t prof_stream = nullptr;
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // pinned staging for small host->device uploads (pageable cudaMemcpyAsync
+  // may synchronise the host with the stream and stall the enqueue pipeline)
+  unsigned char* up = nullptr;
+  size_t up_bytes = 0;
+  cudaEvent_t up_done = nullptr;
+  bool up_pending = false;
   ~ThreadState() {
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
+    if (up) cudaFreeHost(up);
+    if (up_done) cudaEventDestroy(up_done);
   }
 };
 thread_local ThreadState t_state;
@@ -103,8 +113,14 @@ struct Ctx {
   sr_plan& plan;
   std::vector<void*> allocs;
   bool profile;
+  size_t up_off = 0;
   explicit Ctx(cudaStream_t s) : st(s), plan(t_state.plan), profile(g_profile != 0) {
     plan = sr_plan{};
+    ThreadState& ts = t_state;
+    if (ts.up_pending) {  // the staging buffer of the previous call may still be in flight
+      cudaEventSynchronize(ts.up_done);
+      ts.up_pending = false;
+    }
     if (profile) {
       for (auto& e : t_state.prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
       t_state.prof.clear();
@@ -112,21 +128,53 @@ struct Ctx {
     }
   }
   ~Ctx() {
+    static const bool timing = getenv("SR_TIMING") != nullptr;
+    if (timing)
+      fprintf(stderr, "[sr_sort] n=%lld route=%d launches=%d enqueue=%.1fus wait=%.1fus tail=%.1fus\n",
+              (long long)plan.n, plan.route, plan.launches, t_enqueue * 1e6, t_wait * 1e6,
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t_mark).count() * 1e6);
     for (void* p : allocs) cudaFreeAsync(p, st);
+    if (up_off) {
+      ThreadState& ts = t_state;
+      if (!ts.up_done) cudaEventCreateWithFlags(&ts.up_done, cudaEventDisableTiming);
+      cudaEventRecord(ts.up_done, st);
+      ts.up_pending = true;
+    }
+  }
+  // One stream-ordered pool allocation up front (reserve) that later allocs
+  // carve from, so a call costs one cudaMallocAsync instead of dozens.
+  unsigned char* arena = nullptr;
+  size_t arena_size = 0, arena_off = 0;
+  void reserve(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    void* p = nullptr;
+    check_cuda(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+    allocs.push_back(p);
+    arena = reinterpret_cast<unsigned char*>(p);
+    arena_size = bytes;
+    arena_off = 0;
+    plan.workspace_bytes += (int64_t)bytes;
   }
   template <typename T>
   T* alloc(int64_t count) {
     if (count <= 0) count = 1;
-    void* p = nullptr;
     size_t bytes = (size_t)count * sizeof(T);
     bytes = (bytes + 255) & ~size_t(255);
+    if (arena && arena_off + bytes <= arena_size) {
+      T* r = reinterpret_cast<T*>(arena + arena_off);
+      arena_off += bytes;
+      return r;
+    }
+    void* p = nullptr;
     check_cuda(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
     allocs.push_back(p);
     plan.workspace_bytes += (int64_t)bytes;
     return reinterpret_cast<T*>(p);
   }
+  // Launch through f(); returns a handle so that a speculative launch that
+  // turned out to be gated off can give its planned bytes back (unplan()).
   template <typename F>
-  void launch(const char* name, int64_t bytes, F&& f) {
+  int launch(const char* name, int64_t bytes, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (profile) {
       cudaEventCreate(&a);
@@ -141,44 +189,88 @@ struct Ctx {
     }
     plan.launches++;
     plan.bytes_planned += bytes;
+    launched.push_back({bytes, profile ? (int)t_state.prof.size() - 1 : -1});
+    return (int)launched.size() - 1;
   }
+  void unplan(int h) {
+    if (h < 0) return;
+    plan.bytes_planned -= launched[h].first;
+    if (launched[h].second >= 0) t_state.prof[launched[h].second].bytes = 0;
+    launched[h].first = 0;
+  }
+  std::vector<std::pair<int64_t, int>> launched;
   void memset0(void* p, size_t bytes) { check_cuda(cudaMemsetAsync(p, 0, bytes, st), "cudaMemsetAsync"); }
   template <typename T>
   void upload(T* dst, const std::vector<T>& src) {
     if (src.empty()) return;
-    check_cuda(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+    const size_t bytes = src.size() * sizeof(T);
+    ThreadState& ts = t_state;
+    const size_t off = (up_off + 15) & ~size_t(15);
+    if (off + bytes > ts.up_bytes) {
+      if (up_off == 0 && bytes <= (size_t(16) << 20)) {  // (re)size the staging area between calls
+        if (ts.up) cudaFreeHost(ts.up);
+        ts.up_bytes = std::max<size_t>(bytes, size_t(1) << 20);
+        check_cuda(cudaHostAlloc((void**)&ts.up, ts.up_bytes, cudaHostAllocDefault), "cudaHostAlloc");
+      } else {  // staging full within this call: fall back to a synchronous pageable copy
+        check_cuda(cudaMemcpyAsync(dst, src.data(), bytes, cudaMemcpyHostToDevice, st), "upload");
+        return;
+      }
+    }
+    const size_t o2 = (up_off + 15) & ~size_t(15);
+    std::memcpy(ts.up + o2, src.data(), bytes);
+    check_cuda(cudaMemcpyAsync(dst, ts.up + o2, bytes, cudaMemcpyHostToDevice, st), "upload");
+    up_off = o2 + bytes;
   }
   // Readback of `bytes` from device into pinned memory + synchronise (the planner's host sync).
+  double t_enqueue = 0, t_wait = 0;  // host seconds (SR_TIMING diagnostics)
+  std::chrono::steady_clock::time_point t_mark = std::chrono::steady_clock::now();
   void* readback(const void* dev, size_t bytes) {
+    auto t0 = std::chrono::steady_clock::now();
+    t_enqueue += std::chrono::duration<double>(t0 - t_mark).count();
     void* h = pinned(bytes);
     check_cuda(cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, st), "readback");
     check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     plan.host_syncs++;
+    t_mark = std::chrono::steady_clock::now();
+    t_wait += std::chrono::duration<double>(t_mark - t0).count();
     return h;
   }
 };
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, size); the
+// attribute call is far more expensive than a launch.
 template <typename Kern>
 void set_smem(Kern k, size_t bytes) {
-  static_assert(sizeof(Kern) > 0, "");
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& d : done)
+    if (d.first == (const void*)k && d.second >= bytes) return;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.push_back({(const void*)k, bytes});
 }
 
 // ------------------------------------------------------------------ tunables
 constexpr int kScanNT = 256, kScanIPT = 16;              // K9
-constexpr int kFinNT = 512, kFinVT = 16;                 // K11 (kCap = 8192)
-constexpr int kSplNT = 512, kSplVT = 16;                 // K7 (S <= 8192)
-constexpr int kScatNT = 256, kScatVT = 16;               // K10
+constexpr int kFinNT = 256, kFinVT = 16;                 // K11 big items (two halves of 4096 = kCap)
+constexpr int kFinSmallNT = 128;                         // K11 small items (<= 2048 = kSmallItem)
+constexpr int kSplNT = 1024, kSplVT = 8;                 // K7 (S <= 8192)
+constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
+constexpr int kScatKNT = 1024, kScatKVT = 8;             // K10 (keys only)
+constexpr int kScanNT1 = 1024;                           // K1
+constexpr int kCountNT = 1024;                           // K8
+constexpr int64_t kFuseMin = 16 * 1024 * 1024;          // fuse the level-1 histogram into K1 above this n
 constexpr int kMergeNT = 256, kMergeVT = 16;             // K6
 constexpr int kMergeNV = kMergeNT * kMergeVT;
-static_assert(kFinNT * kFinVT == kCap, "finishing tile must equal kCap");
+static_assert(2 * kFinNT * kFinVT == kCap, "finishing item must equal kCap");
+static_assert(kFinSmallNT * kFinVT == kSmallItem, "small finishing tile");
 
 int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
   int64_t t = pow2ceil(std::max<int64_t>(1, n / 512));
   return std::min<int64_t>(65536, std::max<int64_t>(8192, t));
 }
 int choose_buckets(int64_t len) {
-  int64_t b = pow2ceil(ceil_div<int64_t>(len, 2048));
+  int64_t b = pow2ceil(ceil_div<int64_t>(len, kTargetBucket));
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
@@ -204,24 +296,38 @@ struct Sorter {
   }
 
   // ---- finishing kernel over a device item list
-  void finish(const Item* items, const int64_t* count_ptr, int64_t begin, int64_t max_items, int64_t bytes) {
-    if (max_items <= 0) return;
-    using BS = BlockSort<K, HAS_V, kFinNT, kFinVT>;
-    size_t smem = sizeof(K) * BS::KEYS_SMEM + (HAS_V ? 4 * BS::VALS_SMEM : 0);
-    auto kern = k_finish<K, HAS_V, kFinNT, kFinVT>;
+  // NT = 128: items <= kSmallItem (2048 keys, one bitonic / merge tile);
+  // NT = 256: items <= kCap (two 4096-key halves merged into global memory).
+  template <int NT = kFinNT>
+  int finish(const Item* items, const int64_t* count_ptr, int64_t begin, int64_t max_items, int64_t bytes,
+             const DevStats* gate = nullptr, int64_t gate_route = 0) {
+    if (max_items <= 0) return -1;
+    size_t smem = FinishSmem<K, HAS_V, NT, kFinVT>::bytes();
+    auto kern = k_finish<K, HAS_V, NT, kFinVT, (NT == kFinNT)>;
     set_smem(kern, smem);
-    int grid = (int)std::min<int64_t>(max_items, 148 * 8);
+    int grid = (int)std::min<int64_t>(max_items, 148 * 16);
     K* kk = keys;
     uint32_t* vv = vals;
     const K* wkk = wk;
     const uint32_t* wvv = wv;
-    c.launch("finish", bytes, [&] { kern<<<grid, kFinNT, smem, c.st>>>(items, count_ptr, begin, kk, vv, wkk, wvv); });
+    return c.launch(NT == kFinNT ? "finish" : "finish_small", bytes, [&] {
+      kern<<<grid, NT, smem, c.st>>>(items, count_ptr, begin, kk, vv, wkk, wvv, gate, gate_route);
+    });
   }
 
-  void reverse_ranges(const std::vector<RunDesc>& ranges) {
-    if (ranges.empty()) return;
+  int reverse_ranges(const std::vector<RunDesc>& ranges, const DevStats* gate = nullptr) {
+    if (ranges.empty()) return -1;
     constexpr int NT = 256;
     constexpr int64_t CH = NT * 8;
+    K* kk = keys;
+    uint32_t* vv = vals;
+    if (ranges.size() == 1 && ranges[0].start == 0 && ranges[0].len == n) {  // whole array: no upload
+      const int64_t blocks = std::max<int64_t>(1, ceil_div<int64_t>(n / 2, CH));
+      const int64_t nn = n;
+      return c.launch("reverse", 2 * n * (kw + vw), [&] {
+        k_reverse<K, HAS_V, NT><<<(unsigned)blocks, NT, 0, c.st>>>(kk, vv, nullptr, nullptr, 0, gate, nn);
+      });
+    }
     std::vector<int64_t> pre(ranges.size());
     int64_t tot = 0, bytes = 0;
     for (size_t i = 0; i < ranges.size(); i++) {
@@ -233,10 +339,9 @@ struct Sorter {
     int64_t* d_p = c.alloc<int64_t>(pre.size());
     c.upload(d_r, ranges);
     c.upload(d_p, pre);
-    K* kk = keys;
-    uint32_t* vv = vals;
     int nr = (int)ranges.size();
-    c.launch("reverse", bytes, [&] { k_reverse<K, HAS_V, NT><<<(unsigned)tot, NT, 0, c.st>>>(kk, vv, d_r, d_p, nr); });
+    return c.launch("reverse", bytes,
+             [&] { k_reverse<K, HAS_V, NT><<<(unsigned)tot, NT, 0, c.st>>>(kk, vv, d_r, d_p, nr, gate, 0); });
   }
 
   // ---- one partition level over `segs` of buffer src (0 primary, 1 ws); writes the other buffer.
@@ -262,14 +367,26 @@ struct Sorter {
     unsigned long long* d_status = nullptr;
     int* d_tile_counter = nullptr;
     int64_t scan_tiles = 0;
-    Item* d_items = nullptr;
+    Item* d_items = nullptr;      // small items (<= kSmallItem) and fills
+    Item* d_items_big = nullptr;  // items in (kSmallItem, kCap]
+    int64_t items_cap = 0;
     OvfSeg* d_ovf = nullptr;
     int src = 0;
+    // keys only: bucket totals + cursors instead of a count matrix (atomic scatter)
+    bool atomic = false;
+    uint32_t* d_tot = nullptr;
+    uint32_t* d_cursor = nullptr;
+    // splitter sample: per-segment ranks (zeroed) and keys
+    uint32_t* d_rank = nullptr;
+    K* d_sample = nullptr;
+    int64_t sample_total = 0;
+    int max_sample = 0;
   };
 
   void level_alloc(Level& L, const std::vector<OvfSeg>& parts, int64_t chunk_size, int src, int forced_b = 0) {
     L.src = src;
     L.chunk_size = chunk_size;
+    L.atomic = !HAS_V;
     int64_t chunk_base = 0, mat = 0, lp = 0, bins = 0;
     std::vector<int> chunk_seg;
     for (size_t s = 0; s < parts.size(); s++) {
@@ -280,8 +397,13 @@ struct Sorter {
       d.nbins = 2 * d.nbuckets + 1;
       d.nchunks = (int32_t)ceil_div<int64_t>(d.len, chunk_size);
       d.chunk_base = (int32_t)chunk_base;
-      d.mat_base = mat;
+      d.mat_base = L.atomic ? bins : mat;  // keys only: bin base into totals / cursors
       d.len_prefix = lp;
+      d.sample_base = L.sample_total;
+      d.pad = 0;
+      const int64_t S_s = std::min<int64_t>({d.len, (int64_t)d.nbuckets * kOversample, (int64_t)kMaxSample});
+      L.sample_total += S_s;
+      L.max_sample = std::max<int>(L.max_sample, (int)S_s);
       for (int g = 0; g < d.nchunks; g++) chunk_seg.push_back((int)s);
       chunk_base += d.nchunks;
       mat += (int64_t)d.nbins * d.nchunks;
@@ -290,7 +412,7 @@ struct Sorter {
       L.segs.push_back(d);
     }
     L.total_chunks = chunk_base;
-    L.mat_entries = mat;
+    L.mat_entries = L.atomic ? 0 : mat;
     L.total_bins = bins;
     const int64_t S = (int64_t)parts.size();
     L.d_segs = c.alloc<SegDesc>(S);
@@ -298,67 +420,89 @@ struct Sorter {
     L.d_spl = c.alloc<K>(S * kMaxBuckets);
     L.d_eq = c.alloc<uint8_t>(S * kMaxBuckets);
     L.d_m = c.alloc<int>(S);
-    L.d_mat = c.alloc<uint32_t>(mat);
-    L.scan_tiles = ceil_div<int64_t>(mat, kScanNT * kScanIPT);
-    // control block: stats | tile counter | scan status
-    size_t ctrl = sizeof(DevStats) + 256 + sizeof(unsigned long long) * (size_t)L.scan_tiles;
+    L.scan_tiles = L.atomic ? 0 : ceil_div<int64_t>(mat, kScanNT * kScanIPT);
+    if (!L.atomic) L.d_mat = c.alloc<uint32_t>(mat);
+    // control block: stats | tile counter | scan status | bucket totals (zeroed together)
+    const size_t tot_off = sizeof(DevStats) + 256 + sizeof(unsigned long long) * (size_t)L.scan_tiles;
+    const size_t rank_off = tot_off + (L.atomic ? 4 * (size_t)bins : 0);
+    size_t ctrl = rank_off + 4 * (size_t)L.sample_total;
     unsigned char* cb = c.alloc<unsigned char>((int64_t)ctrl);
     c.memset0(cb, ctrl);
     L.d_st = reinterpret_cast<DevStats*>(cb);
     L.d_tile_counter = reinterpret_cast<int*>(cb + sizeof(DevStats));
     L.d_status = reinterpret_cast<unsigned long long*>(cb + sizeof(DevStats) + 256);
-    L.d_items = c.alloc<Item>(bins);
+    if (L.atomic) {
+      L.d_tot = reinterpret_cast<uint32_t*>(cb + tot_off);
+      L.d_cursor = c.alloc<uint32_t>(bins);
+    }
+    L.d_rank = reinterpret_cast<uint32_t*>(cb + rank_off);
+    L.d_sample = c.alloc<K>(L.sample_total);
+    L.items_cap = bins + lp / kFillChunk + (int64_t)parts.size() + 1;
+    L.d_items = c.alloc<Item>(L.items_cap);
+    L.d_items_big = c.alloc<Item>(bins);
     L.d_ovf = c.alloc<OvfSeg>(bins);
     c.upload(L.d_segs, L.segs);
-    c.upload(L.d_chunk_seg, chunk_seg);
+    if (parts.size() == 1) c.memset0(L.d_chunk_seg, sizeof(int) * chunk_base);
+    else c.upload(L.d_chunk_seg, chunk_seg);
   }
 
   const K* buf_k(int b) const { return b ? wk : keys; }
   const uint32_t* buf_v(int b) const { return b ? wv : vals; }
 
-  void level_splitters(Level& L) {
-    using BS = BlockSort<K, false, kSplNT, kSplVT>;
-    size_t smem = sizeof(K) * BS::KEYS_SMEM;
-    auto kern = k_splitters<K, kSplNT, kSplVT>;
-    set_smem(kern, smem);
+  // K7a + K7b.  gate: device stats whose route must be PARTITION (level-1
+  // launches that precede the host's route decision), or nullptr.
+  void level_splitters(Level& L, const DevStats* gate = nullptr) {
+    constexpr int NT = 128, J = 8;
     const K* src = buf_k(L.src);
-    int S = (int)L.segs.size();
-    int64_t bytes = 0;
-    for (auto& s : L.segs) bytes += std::min<int64_t>(s.len, (int64_t)s.nbuckets * kOversample) * kw;
-    c.launch("splitters", bytes,
-             [&] { kern<<<S, kSplNT, smem, c.st>>>(src, L.d_segs, kOversample, L.d_spl, L.d_eq, L.d_m); });
+    const int S = (int)L.segs.size();
+    int64_t pairs = 0;
+    for (auto& sd : L.segs) {
+      int64_t s_s = std::min<int64_t>({sd.len, (int64_t)sd.nbuckets * kOversample, (int64_t)kMaxSample});
+      pairs += s_s * s_s;
+    }
+    dim3 grid((unsigned)ceil_div<int64_t>(L.max_sample, NT), J, (unsigned)S);
+    c.launch("sample_rank", L.sample_total * kw * 2, [&] {
+      k_sample_rank<K, NT, J><<<grid, NT, 0, c.st>>>(src, L.d_segs, kOversample, L.d_rank, L.d_sample, gate);
+    });
+    auto kern = k_select_splitters<K, 1024>;
+    size_t smem = sizeof(K) * kMaxSample;
+    set_smem(kern, smem);
+    c.launch("select_splitters", L.sample_total * (kw + 4), [&] {
+      kern<<<S, 1024, smem, c.st>>>(L.d_segs, kOversample, L.d_rank, L.d_sample, L.d_spl, L.d_eq, L.d_m, gate);
+    });
+    (void)pairs;
   }
 
-  void level_count(Level& L) {
+  void level_count(Level& L, const DevStats* gate = nullptr) {
     const K* src = buf_k(L.src);
     int64_t keys_in = 0;
     for (auto& s : L.segs) keys_in += s.len;
     c.launch("count", keys_in * kw + L.mat_entries * 4, [&] {
-      k_count<K, 256><<<(unsigned)L.total_chunks, 256, 0, c.st>>>(src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl,
-                                                                 L.d_eq, L.d_m, L.d_mat);
+      k_count<K, kCountNT><<<(unsigned)L.total_chunks, kCountNT, 0, c.st>>>(
+          src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_tot, gate);
     });
   }
 
-  void level_scan_plan(Level& L) {
+  void level_scan_plan(Level& L, const DevStats* gate = nullptr) {
     int64_t cnt = L.mat_entries;
-    c.launch("scan", cnt * 8, [&] {
-      k_scan_u32<kScanNT, kScanIPT><<<(unsigned)L.scan_tiles, kScanNT, 0, c.st>>>(L.d_mat, cnt, L.d_status,
-                                                                                 L.d_tile_counter);
-    });
+    if (!L.atomic)
+      c.launch("scan", cnt * 8, [&] {
+        k_scan_u32<kScanNT, kScanIPT><<<(unsigned)L.scan_tiles, kScanNT, 0, c.st>>>(L.d_mat, cnt, L.d_status,
+                                                                                   L.d_tile_counter, gate);
+      });
     int S = (int)L.segs.size();
     int dst = 1 - L.src;
+    auto kern = k_plan<K, 1024>;
+    set_smem(kern, sizeof(PlanSmem));
     c.launch("plan", L.total_bins * 8, [&] {
-      k_plan<K, 1024><<<S, 1024, 0, c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_ovf, L.d_st);
+      kern<<<S, 1024, sizeof(PlanSmem), c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_items_big,
+                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate);
     });
   }
 
-  void level_scatter(Level& L, const DevStats& hs) {
-    const bool skip = !HAS_V && hs.noneq_total == 0;  // keys-only, everything in equality buckets
-    if (skip) return;
-    using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
-    size_t smem = sizeof(SM);
-    auto kern = k_scatter<K, HAS_V, kScatNT, kScatVT>;
-    set_smem(kern, smem);
+  // hs == nullptr: speculative launch gated on the device route (level 1)
+  int level_scatter(Level& L, const DevStats* hs) {
+    if (hs && !HAS_V && hs->noneq_total == 0) return -1;  // keys-only, everything in equality buckets
     ensure_ws();
     const K* sk = buf_k(L.src);
     const uint32_t* sv = buf_v(L.src);
@@ -366,18 +510,45 @@ struct Sorter {
     uint32_t* dv = L.src ? vals : wv;
     int64_t keys_in = 0;
     for (auto& s : L.segs) keys_in += s.len;
-    int64_t bytes = keys_in * (kw + vw) + hs.noneq_total * kw + keys_in * vw + L.mat_entries * 4;
-    c.launch("scatter", bytes, [&] {
+    const int64_t noneq = hs ? hs->noneq_total : keys_in;
+    const DevStats* gate = hs ? nullptr : L.d_st;
+    if (L.atomic) {
+      using SM = ScatterKeysSmem<K, kScatKNT, kScatKVT>;
+      size_t smem = sizeof(SM);
+      auto kern = k_scatter_keys<K, kScatKNT, kScatKVT>;
+      set_smem(kern, smem);
+      return c.launch("scatter", keys_in * kw + noneq * kw, [&] {
+        kern<<<(unsigned)L.total_chunks, kScatKNT, smem, c.st>>>(sk, dk, L.d_segs, L.d_chunk_seg, L.chunk_size,
+                                                                 L.d_spl, L.d_eq, L.d_m, L.d_cursor, gate);
+      });
+    }
+    using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
+    size_t smem = sizeof(SM);
+    auto kern = k_scatter<K, HAS_V, kScatNT, kScatVT>;
+    set_smem(kern, smem);
+    int64_t bytes = keys_in * (kw + vw) + noneq * kw + keys_in * vw + L.mat_entries * 4;
+    return c.launch("scatter", bytes, [&] {
       kern<<<(unsigned)L.total_chunks, kScatNT, smem, c.st>>>(sk, sv, dk, dv, L.d_segs, L.d_chunk_seg, L.chunk_size,
-                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat);
+                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat, gate);
     });
   }
 
-  void level_finish(Level& L, const DevStats& hs) {
-    // sort items read+write the range buckets; fills write keys (+ move vals)
-    int64_t bytes = 2 * (hs.noneq_total - hs.ovf_keys) * (kw + vw) + hs.eq_keys * kw + (L.src == 0 ? 2 : 0) * hs.eq_keys * vw;
-    finish(L.d_items, &L.d_st->n_items, 0, hs.n_items, bytes);
-    c.plan.equal_keys += hs.eq_keys;
+  // hs == nullptr: speculative level-1 launch gated on the device route; the
+  // grid is sized by the item capacity and idle CTAs exit.
+  int level_finish(Level& L, const DevStats* hs) {
+    if (hs) {
+      // sort items read+write the range buckets; fills write keys (+ move vals)
+      int64_t bytes = 2 * (hs->noneq_total - hs->ovf_keys) * (kw + vw) + hs->eq_keys * kw +
+                      (L.src == 0 ? 2 : 0) * hs->eq_keys * vw;
+      c.plan.equal_keys += hs->eq_keys;
+      int h = finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, hs->n_items, bytes);
+      finish(L.d_items_big, &L.d_st->n_items_big, 0, hs->n_items_big, 0);
+      return h;
+    }
+    int h = finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, L.items_cap, 2 * n * (kw + vw), L.d_st,
+                                kRoutePartition);
+    c.unplan(finish(L.d_items_big, &L.d_st->n_items_big, 0, L.total_bins, 0, L.d_st, kRoutePartition));
+    return h;
   }
 
   // Partition levels >= 2 (segments from the previous level's oversized buckets).
@@ -403,8 +574,8 @@ struct Sorter {
           for (auto& p : parts)
             if (o.start == p.start && o.len == p.len) fail(SR_ERR_INTERNAL, "partition made no progress");
       }
-      level_scatter(L, hs);
-      level_finish(L, hs);
+      level_scatter(L, &hs);
+      level_finish(L, &hs);
       c.plan.levels = level;
       parts.swap(next);
       src = 1 - src;
@@ -652,16 +823,36 @@ struct Sorter {
   }
 
   // ---- top level
+  // Everything up to the first statistics readback is enqueued without a host
+  // round trip: the presortedness scan (fused with the level-1 histogram), the
+  // device-side route decision, the level-1 plan, and the kernels of the
+  // SORTED / REVERSED / TILE / single-level PARTITION routes as speculative
+  // launches that return at once unless the device route selects them.
   void run() {
     c.plan.n = n;
+    const int force = g_force_route;
     const int64_t T = choose_tile(n);
     const int64_t G = ceil_div<int64_t>(n, T);
     const bool part = n > kCap;
+    {  // one allocation for everything up to the first readback (+ workspace)
+      const int64_t bins = 2 * (int64_t)choose_buckets(n) + 1;
+      auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+      int64_t b = r(n * kw) + r(n * vw) + r(G * 32) + 2 * r((G + 1) * 32) + r(64) + r(G * 4) +
+                  r(kMaxBuckets * kw) + r(kMaxBuckets) + r(4) + (HAS_V ? r(bins * G * 4) : 0) +
+                  r(sizeof(DevStats) + 256 + 8 * ceil_div<int64_t>(bins * G, kScanNT * kScanIPT) + 4 * bins) +
+                  r(4 * bins) + r(24 * (bins + n / kFillChunk + 2)) + r(24 * bins) + r(16 * bins) + 8 * 256;
+      c.reserve((size_t)b);
+    }
+    // Large n: the level-1 histogram rides on the presortedness read (one HBM
+    // pass saved), so the splitters come first.  L2-resident n: the route is
+    // decided first and every partition kernel is gated on it, so sorted and
+    // reversed inputs pay for nothing but the scan.
+    const bool fused = part && n > kFuseMin;
     Level L1;
     if (part) {
       std::vector<OvfSeg> whole{{0, n}};
       level_alloc(L1, whole, T, 0);
-      level_splitters(L1);
+      if (fused) level_splitters(L1);
     }
     TileSummary* d_sums = c.alloc<TileSummary>(G);
     RunDesc* d_asc = c.alloc<RunDesc>(G + 1);
@@ -670,60 +861,83 @@ struct Sorter {
     if (!part) c.memset0(d_pst, sizeof(DevStats));
     const K* kk = keys;
     const int nbins1 = part ? L1.segs[0].nbins : 0;
-    c.launch("presort_scan", n * kw + (part ? (int64_t)nbins1 * G * 4 : 0), [&] {
-      if (part) {
+    c.launch("presort_scan", n * kw + (fused ? (int64_t)nbins1 * G * 4 : 0), [&] {
+      if (fused) {
         if (HAS_V)
-          k_presort_scan<K, true, true, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq,
-                                                                           L1.d_m, L1.d_mat, nbins1, (int)G);
+          k_presort_scan<K, true, true, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot);
         else
-          k_presort_scan<K, false, true, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq,
-                                                                            L1.d_m, L1.d_mat, nbins1, (int)G);
+          k_presort_scan<K, false, true, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot);
       } else {
         if (HAS_V)
-          k_presort_scan<K, true, false, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, nullptr, nullptr,
-                                                                            nullptr, nullptr, 0, (int)G);
+          k_presort_scan<K, true, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr);
         else
-          k_presort_scan<K, false, false, 256><<<(unsigned)G, 256, 0, c.st>>>(kk, n, (int)T, d_sums, nullptr, nullptr,
-                                                                             nullptr, nullptr, 0, (int)G);
+          k_presort_scan<K, false, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr);
       }
     });
+    const int merge_ok = g_merge_route;
     c.launch("presort_resolve", G * (int64_t)sizeof(TileSummary), [&] {
-      k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst);
+      k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst, force, merge_ok);
     });
-    if (part) level_scan_plan(L1);
-    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(d_pst, sizeof(DevStats)));
-    c.plan.descents = hs.descents;
-    c.plan.asc_breaks = hs.asc_breaks;
-    c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
-    if (hs.error) fail(SR_ERR_INTERNAL, "plan kernel inconsistency");
-
-    const int force = g_force_route;
-    if (hs.descents == 0) {  // is_sorted exit
-      c.plan.route = SR_ROUTE_SORTED;
-      return;
-    }
-    if (hs.asc_breaks == 0 && force != SR_ROUTE_PARTITION && force != SR_ROUTE_MERGE) {
-      // one descending run over the whole array (strict for pairs): reverse
-      c.plan.route = SR_ROUTE_REVERSED;
-      c.plan.desc_runs_reversed = 1;
-      reverse_ranges({RunDesc{0, n, 0, 0}});
-      return;
-    }
-    if (!part && force != SR_ROUTE_MERGE) {
-      c.plan.route = SR_ROUTE_TILE;
+    // speculative route kernels
+    int h_rev = -1, h_tile = -1, h_scat = -1, h_fin = -1, h_count = -1;
+    if (force == 0) h_rev = reverse_ranges({RunDesc{0, n, 0, 0}}, d_pst);
+    if (!part) {
       std::vector<Item> one{Item{0, 0, (int32_t)n, kItemSort}};
       Item* d_items = c.alloc<Item>(1);
       int64_t* d_cnt = c.alloc<int64_t>(1);
       std::vector<int64_t> cnt{1};
       c.upload(d_items, one);
       c.upload(d_cnt, cnt);
-      finish(d_items, d_cnt, 0, 1, 2 * n * (kw + vw));
-      return;
+      h_tile = finish(d_items, d_cnt, 0, 1, 2 * n * (kw + vw), d_pst, kRouteTile);
+    } else {
+      if (!fused) {
+        level_splitters(L1, d_pst);
+        h_count = (int)c.launched.size();
+        level_count(L1, d_pst);
+      }
+      level_scan_plan(L1, d_pst);
+      ensure_ws();
+      h_scat = level_scatter(L1, nullptr);
+      h_fin = level_finish(L1, nullptr);
     }
-    // MERGE vs PARTITION by planned bytes
-    bool use_merge = force == SR_ROUTE_MERGE;
+    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(d_pst, sizeof(DevStats)));
+    c.plan.descents = hs.descents;
+    c.plan.asc_breaks = hs.asc_breaks;
+    c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
+    if (hs.error) fail(SR_ERR_INTERNAL, "plan kernel inconsistency");
+    const int64_t route = hs.route;
+    if (route != kRouteReversed) c.unplan(h_rev);
+    if (route != kRoutePartition) c.unplan(h_count);
+    if (route != kRouteTile) c.unplan(h_tile);
+    if (route != kRoutePartition || (!HAS_V && hs.noneq_total == 0)) c.unplan(h_scat);
+    if (route != kRoutePartition) c.unplan(h_fin);
+    if (part && route == kRoutePartition) {  // fix the finish bytes to the real item mix
+      c.unplan(h_fin);
+      c.plan.equal_keys += hs.eq_keys;
+      c.plan.bytes_planned += 2 * (hs.noneq_total - hs.ovf_keys) * (kw + vw) + hs.eq_keys * kw + 2 * hs.eq_keys * vw;
+    }
+    switch (route) {
+      case kRouteSorted:  // is_sorted exit
+        c.plan.route = SR_ROUTE_SORTED;
+        return;
+      case kRouteReversed:  // one descending run (strict for pairs), reversed
+        c.plan.route = SR_ROUTE_REVERSED;
+        c.plan.desc_runs_reversed = 1;
+        return;
+      case kRouteTile:
+        c.plan.route = SR_ROUTE_TILE;
+        return;
+      default:
+        break;
+    }
+    bool use_merge = route == kRouteMerge;
     std::vector<Seg> segs;
-    if (force == SR_ROUTE_MERGE || (force == 0 && g_merge_route && hs.asc_cover + hs.desc_cover >= n / 2)) {
+    if (route == kRouteMerge || route == kRouteUndecided) {
+      // MERGE vs PARTITION by planned bytes over the natural runs
       std::vector<RunDesc> asc, desc;
       if (hs.n_asc_runs) {
         const RunDesc* h = reinterpret_cast<const RunDesc*>(c.readback(d_asc, sizeof(RunDesc) * hs.n_asc_runs));
@@ -743,11 +957,10 @@ struct Sorter {
     }
     if (use_merge) {
       c.plan.route = SR_ROUTE_MERGE;
-      if (segs.empty()) segs = build_segments({}, {});
       run_merge_route(segs);
       return;
     }
-    // PARTITION
+    // PARTITION (level 1 already enqueued unless the route was undecided)
     c.plan.route = SR_ROUTE_PARTITION;
     c.plan.levels = 1;
     if (!part) fail(SR_ERR_INTERNAL, "partition route without level 1");
@@ -756,8 +969,21 @@ struct Sorter {
       const OvfSeg* h = reinterpret_cast<const OvfSeg*>(c.readback(L1.d_ovf, sizeof(OvfSeg) * hs.n_ovf));
       next.assign(h, h + hs.n_ovf);
     }
-    level_scatter(L1, hs);
-    level_finish(L1, hs);
+    if (route == kRouteUndecided) {  // the speculative level-1 kernels were gated off
+      if (!fused) {
+        level_splitters(L1);
+        level_count(L1);
+      }
+      level_scan_plan(L1);
+      hs = *reinterpret_cast<DevStats*>(c.readback(L1.d_st, sizeof(DevStats)));
+      next.clear();
+      if (hs.n_ovf > 0) {
+        const OvfSeg* h = reinterpret_cast<const OvfSeg*>(c.readback(L1.d_ovf, sizeof(OvfSeg) * hs.n_ovf));
+        next.assign(h, h + hs.n_ovf);
+      }
+      level_scatter(L1, &hs);
+      level_finish(L1, &hs);
+    }
     run_levels(next, 1);
   }
 };

@@ -30,12 +30,14 @@ struct DevStats {
   int64_t asc_cover, desc_cover;      // keys covered by long runs
   // partition level (plan kernel)
   int64_t noneq_total;  // keys in range (non-equality) buckets
-  int64_t n_items;      // finish items emitted (cumulative counter)
+  int64_t n_items;      // small finishing items (len <= kSmallItem, and fills)
+  int64_t n_items_big;  // large finishing items (kSmallItem < len <= kCap)
   int64_t n_ovf;        // oversized range buckets for the next level
   int64_t ovf_keys;
   int64_t eq_keys;
   int64_t error;        // device-detected inconsistency (must stay 0)
-  int64_t pad[3];
+  int64_t route;        // device-side route decision (kRoute*)
+  int64_t pad[1];
 };
 
 // One segment of a partition level (H7-H10).
@@ -47,6 +49,8 @@ struct SegDesc {
   int32_t nbins;          // 2*B_s + 1 matrix rows (bucket-major)
   int32_t chunk_base;     // first global chunk index
   int32_t nchunks;        // G_s
+  int64_t sample_base;    // first entry of this segment's sample / rank arrays
+  int64_t pad;
 };
 
 // Work item for the finishing kernel (H11/H4 segmented).
@@ -62,9 +66,18 @@ struct OvfSeg {
   int64_t start, len;
 };
 
-constexpr int kMaxBuckets = 1024;           // B_max per level
+// route codes (equal to the SR_ROUTE_* values of include/sr_sort.h)
+constexpr int64_t kRouteSorted = 1, kRouteReversed = 2, kRouteMerge = 3, kRoutePartition = 4, kRouteTile = 5,
+                  kRouteUndecided = 6;
+
+constexpr int kMaxBuckets = 2048;           // B_max per level
 constexpr int kMaxBins = 2 * kMaxBuckets + 1;
-constexpr int kOversample = 8;              // o: S = B*o <= 8192 samples
-constexpr int kCap = 8192;                  // finishing tile (NT=512, VT=16)
+constexpr int kOversample = 4;              // o: S = B*o <= kMaxSample samples
+constexpr int kMaxSample = kMaxBuckets * kOversample;
+constexpr int kCap = 8192;                  // largest finishing item (two 4096-key halves)
+constexpr int kPack = 1024;                 // buckets <= kPack are packed into items < 2*kPack
+constexpr int kSmallItem = 2 * kPack;       // items <= this go to the small finishing kernel
+constexpr int kFillChunk = 8192;            // equality fills are split into items of this size
+constexpr int kTargetBucket = 1024;         // mean bucket size the planner aims for
 
 }  // namespace sr

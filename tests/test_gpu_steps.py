@@ -127,13 +127,13 @@ def test_h6_trimmed_pair_is_copy():
 # ---------------------------------------------------------------- H7 splitters
 
 @pytest.mark.parametrize("order", ["random", "few_unique", "all_equal", "organ_pipe", "nearly", "few100", "extremes"])
-@pytest.mark.parametrize("nb", [2, 64, 1024])
+@pytest.mark.parametrize("nb", [2, 64, 1024, 2048])
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
 def test_h7_splitters(order, nb, dtype):
     n = 300_007
     k = gen.make(order, n, dtype, config=23)
     gs, ge = sr.splitters(cuda(k), nb)
-    es, ee = oracle.splitters(k, 0, n, nb, 8)
+    es, ee = oracle.splitters(k, 0, n, nb, 4)  # kOversample = 4
     assert gs.tolist() == es.astype(np.int64).tolist()
     assert ge.tolist() == ee.tolist()
 
@@ -141,7 +141,7 @@ def test_h7_splitters(order, nb, dtype):
 # ---------------------------------------------------------------- H8-H10 partition level
 
 @pytest.mark.parametrize("order", ["random", "few_unique", "few100", "nearly", "all_equal", "organ_pipe", "extremes"])
-@pytest.mark.parametrize("nb", [2, 256, 1024])
+@pytest.mark.parametrize("nb", [2, 256, 2048])
 @pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
 def test_h8_h10_partition_level(order, nb, pairs, dtype):
@@ -149,10 +149,19 @@ def test_h8_h10_partition_level(order, nb, pairs, dtype):
     k = gen.make(order, n, dtype, config=24)
     v = gen.index_payload(n)
     ok, ov, counts = sr.partition_level(cuda(k), nb, vals=cuda(v.view(np.int32)) if pairs else None)
-    spl, eq = oracle.splitters(k, 0, n, nb, 8)
+    spl, eq = oracle.splitters(k, 0, n, nb, 4)
     bins = oracle.classify(k, spl, eq)
     ek, ev, ec = oracle.stable_partition(bins, 2 * nb + 1, k, v)
     assert counts.tolist() == ec.tolist()
-    assert np.array_equal(ok.cpu().numpy(), ek)
-    if pairs:
+    gk = ok.cpu().numpy()
+    if pairs:  # stable scatter: the whole output is unique
+        assert np.array_equal(gk, ek)
         assert np.array_equal(ov.cpu().numpy().view(np.uint32), ev)
+    else:
+        # keys only: bucket boundaries and bucket contents are unique; the order
+        # inside a range bucket is not (equal keys are indistinguishable and
+        # the finishing sort orders it) -- compare each bucket as a multiset
+        bounds = np.concatenate([[0], np.cumsum(ec)])
+        for b in range(ec.size):
+            s0, s1 = bounds[b], bounds[b + 1]
+            assert np.array_equal(np.sort(gk[s0:s1]), np.sort(ek[s0:s1])), b
