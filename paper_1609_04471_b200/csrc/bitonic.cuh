@@ -37,11 +37,23 @@ struct BitonicSort {
     }
   }
 
+  // Register-frugal: partners are fetched pairwise (flip) or one at a time.
   __device__ __forceinline__ static void shfl_stage(K (&k)[VT], int mask, bool lower, bool flip) {
-    K b[VT];
+    if (flip) {
 #pragma unroll
-    for (int r = 0; r < VT; r++) b[r] = __shfl_xor_sync(0xffffffffu, k[r], mask);
-    combine(k, b, lower, flip);
+      for (int r = 0; r < VT / 2; r++) {
+        const K b1 = __shfl_xor_sync(0xffffffffu, k[VT - 1 - r], mask);  // partner of k[r]
+        const K b2 = __shfl_xor_sync(0xffffffffu, k[r], mask);           // partner of k[VT-1-r]
+        k[r] = lower ? kmin(k[r], b1) : kmax(k[r], b1);
+        k[VT - 1 - r] = lower ? kmin(k[VT - 1 - r], b2) : kmax(k[VT - 1 - r], b2);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < VT; r++) {
+        const K b = __shfl_xor_sync(0xffffffffu, k[r], mask);
+        k[r] = lower ? kmin(k[r], b) : kmax(k[r], b);
+      }
+    }
   }
 
   __device__ __forceinline__ static void reg_half_cleaners(K (&k)[VT]) {
@@ -123,6 +135,49 @@ struct BitonicSort {
     __syncthreads();
     if (act) BlockSort<K, false, NT, VT>::store_vec(ks + t * VT, k);
     __syncthreads();
+  }
+};
+
+}  // namespace sr
+
+namespace sr {
+
+// One warp sorts up to 32*VT keys held "blocked" in registers (lane l owns
+// elements [l*VT, (l+1)*VT)): Batcher network inside the lane, then bitonic
+// merge levels whose cross-lane stages are __shfl_xor_sync and whose in-lane
+// stages are register compare-exchanges.  No shared memory, no barriers:
+// used for the (bucket-sized) finishing items of the keys-only partition.
+template <typename K, int VT>
+struct WarpBitonic {
+  static constexpr int CAP = 32 * VT;
+  using BT = BitonicSort<K, 32, VT>;
+
+  // ks: this warp's staging area (CAP elements), holding count keys.
+  __device__ static void sort(K* ks, int count) {
+    const int lane = threadIdx.x & 31;
+    const int need = (count + VT - 1) / VT;
+    int nl = 1;  // lanes taking part (power of two)
+    while (nl < need) nl <<= 1;
+    K k[VT];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < VT; i++) {
+      int p = lane * VT + i;
+      k[i] = p < count ? ks[p] : KeyTraits<K>::max_key();
+    }
+    batcher_network<VT>([&](int a, int b) {
+      K x = k[a], y = k[b];
+      k[a] = BT::kmin(x, y);
+      k[b] = BT::kmax(x, y);
+    });
+    for (int tk = 2; tk <= nl; tk <<= 1) {  // lanes per merged run
+      BT::shfl_stage(k, tk - 1, (lane & (tk >> 1)) == 0, true);
+      for (int jt = tk >> 2; jt >= 1; jt >>= 1) BT::shfl_stage(k, jt, (lane & jt) == 0, false);
+      BT::reg_half_cleaners(k);
+    }
+    __syncwarp();
+    if (lane < nl) BlockSort<K, false, 32, VT>::store_vec(ks + lane * VT, k);
+    __syncwarp();
   }
 };
 

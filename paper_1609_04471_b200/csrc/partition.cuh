@@ -115,8 +115,20 @@ __global__ void __launch_bounds__(NT) k_sample_rank(const K* __restrict__ src, c
   const int j1 = j0 + cj < S ? j0 + cj : S;
   if (j0 >= j1) return;
   const int len = j1 - j0;
-  for (int jj = threadIdx.x; jj < len; jj += NT)
-    s_chunk[jj] = src[sample_position(seg.start, seg.len, S, j0 + jj, log2S)];
+  {
+    constexpr int PER = (kMaxSample / J + NT - 1) / NT;
+    K y[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int jj = u * NT + threadIdx.x;
+      y[u] = jj < len ? src[sample_position(seg.start, seg.len, S, j0 + jj, log2S)] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int jj = u * NT + threadIdx.x;
+      if (jj < len) s_chunk[jj] = y[u];
+    }
+  }
   const int i = i0 + threadIdx.x;
   K x = i < S ? src[sample_position(seg.start, seg.len, S, i, log2S)] : K(0);
   if (blockIdx.y == 0 && i < S) sample[seg.sample_base + i] = x;
@@ -180,12 +192,15 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
                                                const int* __restrict__ chunk_seg, int64_t chunk_size,
                                                const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
                                                const int* __restrict__ m_all, uint32_t* __restrict__ mat,
-                                               uint32_t* __restrict__ tot, const DevStats* __restrict__ gate) {
+                                               uint32_t* __restrict__ tot, uint16_t* __restrict__ bins_out,
+                                               const DevStats* __restrict__ gate) {
   if (gate && gate->route != kRoutePartition) return;  // speculative launch
   constexpr int U = 8;
-  __shared__ K s_spl[kMaxBuckets];
-  __shared__ uint8_t s_eq[kMaxBuckets];
-  __shared__ uint32_t s_hist[kMaxBins];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ClassifySmem<K>& csm = *reinterpret_cast<ClassifySmem<K>*>(smem_raw);
+  K* s_spl = csm.tree;
+  uint8_t* s_eq = csm.eq;
+  uint32_t* s_hist = csm.hist;
   const int c = blockIdx.x;
   const int s = chunk_seg[c];
   const SegDesc seg = segs[s];
@@ -206,7 +221,11 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
     int bin[U];
     classify_keys<K, U>(x, bin, s_spl, s_eq, m);
 #pragma unroll
-    for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], base + u * NT + threadIdx.x < c1);
+    for (int u = 0; u < U; u++) {
+      const int64_t i = base + u * NT + threadIdx.x;
+      hist_add(s_hist, bin[u], i < c1);
+      if (bins_out && i < c1) bins_out[i] = (uint16_t)bin[u];  // reused by the scatter
+    }
   }
   __syncthreads();
   if (tot) {  // keys only: per-segment bucket totals at bin base seg.mat_base
@@ -318,7 +337,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
                                               int buf, Item* __restrict__ items, Item* __restrict__ items_big,
                                               OvfSeg* __restrict__ ovf, DevStats* __restrict__ st,
                                               const uint32_t* __restrict__ tot, uint32_t* __restrict__ cursor,
-                                              const DevStats* __restrict__ gate) {
+                                              const DevStats* __restrict__ gate, int small_max) {
   if (gate && gate->route != kRoutePartition) return;  // speculative launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlanSmem& sm = *reinterpret_cast<PlanSmem*>(smem_raw);
@@ -329,7 +348,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
   const int nb = seg.nbins;
   const int G = seg.nchunks;
   const int64_t send = seg.start + seg.len;
-  constexpr int H = kPack;
+  const int H = small_max / 2;  // packing window: chunks of packed buckets stay < small_max
   if (tot) {
     // keys only: bucket starts = seg.start + exclusive scan of the totals
     for (int b = threadIdx.x; b < nb; b += NT) sm.p[b] = (int32_t)tot[seg.mat_base + b];
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
     if (b & 1) ty = c > 0 ? kBinFill : kBinEmpty;
     else if (c == 0) ty = kBinEmpty;
     else if (c > kCap) ty = kBinOvf;
-    else if (c > kPack) ty = kBinBig;
+    else if (c > H) ty = kBinBig;
     else ty = kBinSmall;
     sm.type[b] = ty;
     sm.epoch[b] = (ty == kBinFill || ty == kBinOvf || ty == kBinBig) ? 1 : 0;
@@ -391,7 +410,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
     int c = sm.p[b + 1] - sm.p[b];
     int len = ty == (kBinSmall | 0x80) ? ((b + 1 < nb ? sm.next[b + 1] : (int32_t)send) - sm.p[b])
                                        : (ty == kBinBig ? c : 0);
-    if (len) (len <= kSmallItem ? n_small : n_big)++;
+    if (len) (len <= small_max ? n_small : n_big)++;
     if (ty == kBinFill) n_small += (c + kFillChunk - 1) / kFillChunk;
     if (ty == kBinOvf) n_ovf++;
   }
@@ -410,7 +429,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
     if (len) {
       Item it;
       it.start = sm.p[b]; it.len = len; it.kind = kItemSort | (buf << 4); it.key = 0;
-      if (len <= kSmallItem) items[o_small++] = it; else items_big[o_big++] = it;
+      if (len <= small_max) items[o_small++] = it; else items_big[o_big++] = it;
     } else if (ty == kBinFill) {
       int i = (b - 1) / 2;
       if (i >= m) atomicAdd((unsigned long long*)&st->error, 1ull);
@@ -447,7 +466,7 @@ template <typename K, bool HAS_V, int NT, int VTS>
 struct ScatterSmem {
   static constexpr int NW = NT / 32;
   static constexpr int ST = NT * VTS;
-  K spl[kMaxBuckets];
+  K spl[2 * kMaxBuckets];
   K stk[ST];
   uint32_t stv[HAS_V ? ST : 1];
   uint32_t cur[kMaxBins];
@@ -465,7 +484,8 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
                                                  const SegDesc* __restrict__ segs, const int* __restrict__ chunk_seg,
                                                  int64_t chunk_size, const K* __restrict__ spl_all,
                                                  const uint8_t* __restrict__ eq_all, const int* __restrict__ m_all,
-                                                 const uint32_t* __restrict__ mat, const DevStats* __restrict__ gate) {
+                                                 const uint32_t* __restrict__ mat, const uint16_t* __restrict__ bins_in,
+                                                 const DevStats* __restrict__ gate) {
   using SM = ScatterSmem<K, HAS_V, NT, VTS>;
   // speculative launch: only on the partition route, and keys-only with every
   // key in an equality bucket needs no scatter at all
@@ -505,7 +525,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
       bool valid = pos < c1;
-      int b = valid ? classify_key<K>(x[i], sm.spl, sm.eq, m) : kMaxBins;
+      int b = !valid ? kMaxBins : (bins_in ? (int)bins_in[pos] : classify_key<K>(x[i], sm.spl, sm.eq, m));
       unsigned peers = __match_any_sync(0xffffffffu, b);
       int base = sm.wcnt[w][b];
       rk[i] = base + __popc(peers & lt);
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
 template <typename K, int NT, int VTS>
 struct ScatterKeysSmem {
   static constexpr int ST = NT * VTS;
-  K spl[kMaxBuckets];
+  K spl[2 * kMaxBuckets];
   K stk[ST];
   uint32_t cnt[kMaxBins];
   uint32_t lstart[kMaxBins];
@@ -580,6 +600,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
                                                       const int* __restrict__ chunk_seg, int64_t chunk_size,
                                                       const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
                                                       const int* __restrict__ m_all, uint32_t* __restrict__ cursor,
+                                                      const uint16_t* __restrict__ bins_in,
                                                       const DevStats* __restrict__ gate) {
   if (gate && (gate->route != kRoutePartition || gate->noneq_total == 0)) return;
   using SM = ScatterKeysSmem<K, NT, VTS>;
@@ -594,7 +615,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
   const int nb = seg.nbins;
   const int m = m_all[s];
   uint32_t* cur = cursor + seg.mat_base;
-  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
+  if (!bins_in) load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
   for (int64_t sub = c0; sub < c1; sub += ST) {
@@ -607,8 +628,9 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + i * NT + tid;
       x[i] = pos < c1 ? src[pos] : K(0);
+      if (bins_in) bin[i] = pos < c1 ? (int)bins_in[pos] : 0;
     }
-    classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m);
+    if (!bins_in) classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m);
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + i * NT + tid;
@@ -640,6 +662,58 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
       dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K11w (keys only): every warp finishes whole items of up to 32*VT keys with
+// the warp-register bitonic sort: coalesced load into the warp's staging
+// area, is_sorted check, sort, coalesced store into the
+// caller's keys.  Fills (equality buckets) are written here too.
+template <typename K, int VT, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_finish_warp(const Item* __restrict__ items,
+                                                             const int64_t* __restrict__ count_ptr, K* __restrict__ keys,
+                                                             const K* __restrict__ ws_k,
+                                                             const DevStats* __restrict__ gate, int64_t gate_route) {
+  if (gate && gate->route != gate_route) return;  // speculative launch on another route
+  using WB = WarpBitonic<K, VT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  K* ks = reinterpret_cast<K*>(smem_raw) + w * WB::CAP;
+  const int64_t count = *count_ptr;
+  for (int64_t it = (int64_t)blockIdx.x * WARPS + w; it < count; it += (int64_t)gridDim.x * WARPS) {
+    const Item item = items[it];
+    const bool from_ws = (item.kind >> 4) & 1;
+    const int64_t s = item.start;
+    const int len = item.len;
+    K* dk = keys + s;
+    if ((item.kind & 0xf) == kItemFill) {
+      const K key = (K)item.key;
+      for (int i = lane; i < len; i += 32) dk[i] = key;
+      continue;
+    }
+    const K* sk = (from_ws ? ws_k : keys) + s;
+    // all loads in flight at once (striped, coalesced), then stage in smem
+    {
+      K x[VT];
+#pragma unroll
+      for (int r = 0; r < VT; r++) {
+        const int i = r * 32 + lane;
+        x[r] = i < len ? sk[i] : KeyTraits<K>::max_key();
+      }
+#pragma unroll
+      for (int r = 0; r < VT; r++) ks[r * 32 + lane] = x[r];
+    }
+    __syncwarp();
+    int unsorted = 0;
+    for (int i = lane; i + 1 < len; i += 32) unsorted |= ks[i + 1] < ks[i];
+    unsorted = __any_sync(0xffffffffu, unsorted);
+    if (unsorted) WB::sort(ks, len);
+    if (unsorted || from_ws) {
+      __syncwarp();
+      for (int i = lane; i < len; i += 32) dk[i] = ks[i];
+    }
+    __syncwarp();
   }
 }
 
@@ -697,13 +771,29 @@ __global__ void __launch_bounds__(NT) k_finish(const Item* __restrict__ items, c
     K* dk = keys + s;
     uint32_t* dv = vals + s;
     const int first = (!TWO_HALVES || len <= NV) ? len : NV;
-    for (int i = threadIdx.x; i < first; i += NT) {
-      ks[i] = sk[i];
-      if (HAS_V) vs[i] = sv[i];
+    {  // VT loads per thread in flight at once (striped, coalesced)
+      K x[VT];
+      uint32_t y[VT];
+#pragma unroll
+      for (int r = 0; r < VT; r++) {
+        const int i = r * NT + threadIdx.x;
+        x[r] = i < first ? sk[i] : K(0);
+        if (HAS_V) y[r] = i < first ? sv[i] : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < VT; r++) {
+        const int i = r * NT + threadIdx.x;
+        if (i < first) {
+          ks[i] = x[r];
+          if (HAS_V) vs[i] = y[r];
+        }
+      }
     }
-    // is_sorted, read straight from the source range
+    // is_sorted
     int unsorted = 0;
-    for (int i = threadIdx.x; i + 1 < len; i += NT) unsorted |= sk[i + 1] < sk[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i + 1 < first; i += NT) unsorted |= ks[i + 1] < ks[i];
+    for (int i = first - 1 + threadIdx.x; i + 1 < len; i += NT) unsorted |= sk[i + 1] < sk[i];
     unsorted = __syncthreads_or(unsorted);
     if (!unsorted) {
       if (from_ws)

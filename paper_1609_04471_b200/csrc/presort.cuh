@@ -13,48 +13,71 @@
 
 namespace sr {
 
-// Branchless lower_bound over the padded splitter array (P2-1 entries, pads =
-// +inf): i = #{t_j < x}.  Bucket id 2i+1 when x equals an equality splitter
-// (3-way split, switched on per splitter by the gamma test
-// of PAPER.md:168), else 2i.
+// Splitter search structure in shared memory (H8).  tree[1..kMaxBuckets-1]
+// holds the splitters padded with +inf to 2^L - 1 = kMaxBuckets - 1 entries in
+// level (Eytzinger) order; tree[kMaxBuckets + i] holds the i-th splitter in
+// sorted order for the equality test, eqf[i] its equality flag.  A binary
+// search over a plain sorted array sends every lane of a warp to the same
+// bank at the deep levels (addresses = step-1 mod 2*step); in level order each
+// level is contiguous, so the lanes spread over the banks.
+constexpr int kTreeLevels = 11;  // log2(kMaxBuckets)
+static_assert((1 << kTreeLevels) == kMaxBuckets, "");
+
+// Bucket id of x: i = #{t_j < x} (lower_bound); 2i+1 when x equals an
+// equality splitter (3-way split, switched on per splitter
+// by the gamma test of PAPER.md:168), else 2i.
 template <typename K>
-__device__ __forceinline__ int classify_key(K x, const K* spl, const uint8_t* eqf, int m) {
-  int i = 0;
+__device__ __forceinline__ int classify_key(K x, const K* tree, const uint8_t* eqf, int m) {
+  int j = 1;
 #pragma unroll
-  for (int step = kMaxBuckets / 2; step > 0; step >>= 1)
-    if (spl[i + step - 1] < x) i += step;
-  return 2 * i + ((i < m && spl[i] == x && eqf[i]) ? 1 : 0);
+  for (int l = 0; l < kTreeLevels; l++) j = 2 * j + (tree[j] < x ? 1 : 0);
+  const int i = j - kMaxBuckets;
+  return 2 * i + ((i < m && tree[kMaxBuckets + i] == x && eqf[i]) ? 1 : 0);
 }
 
 // Batched classification: the U searches advance in lockstep so their
 // shared-memory loads are independent and overlap (U-way ILP).
 template <typename K, int U>
-__device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], const K* spl, const uint8_t* eqf, int m) {
-  int idx[U];
+__device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], const K* tree, const uint8_t* eqf, int m) {
+  int j[U];
 #pragma unroll
-  for (int u = 0; u < U; u++) idx[u] = 0;
+  for (int u = 0; u < U; u++) j[u] = 1;
 #pragma unroll
-  for (int step = kMaxBuckets / 2; step > 0; step >>= 1) {
+  for (int l = 0; l < kTreeLevels; l++) {
 #pragma unroll
-    for (int u = 0; u < U; u++) idx[u] += (spl[idx[u] + step - 1] < x[u]) ? step : 0;
+    for (int u = 0; u < U; u++) j[u] = 2 * j[u] + (tree[j[u]] < x[u] ? 1 : 0);
   }
 #pragma unroll
   for (int u = 0; u < U; u++) {
-    const int i = idx[u];
-    bin[u] = 2 * i + ((i < m && spl[i] == x[u] && eqf[i]) ? 1 : 0);
+    const int i = j[u] - kMaxBuckets;
+    bin[u] = 2 * i + ((i < m && tree[kMaxBuckets + i] == x[u] && eqf[i]) ? 1 : 0);
   }
 }
 
-// Splitters into shared memory, padded with +inf to kMaxBuckets-1 entries so
-// the search above always takes log2(kMaxBuckets) unrolled steps.
+// Build the search structure (2*kMaxBuckets entries of s_tree, kMaxBuckets
+// flags) from the m sorted splitters.
 template <typename K>
-__device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_spl,
+__device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_tree,
                                                     uint8_t* s_eq) {
   for (int i = threadIdx.x; i < kMaxBuckets; i += blockDim.x) {
-    s_spl[i] = i < m ? spl[i] : KeyTraits<K>::max_key();
+    const K v = i < m ? spl[i] : KeyTraits<K>::max_key();
+    s_tree[kMaxBuckets + i] = v;
     s_eq[i] = i < m ? eqf[i] : 0;
+    if (i >= 1) {  // node i of the level-order tree <- sorted position pos(i)
+      const int d = 31 - __clz(i);
+      const int pos = ((2 * (i - (1 << d)) + 1) << (kTreeLevels - 1 - d)) - 1;
+      s_tree[i] = pos < m ? spl[pos] : KeyTraits<K>::max_key();
+    }
   }
 }
+
+// Shared memory of the histogram passes (K1 fused, K8): dynamic, > 48 KB for int64.
+template <typename K>
+struct ClassifySmem {
+  K tree[2 * kMaxBuckets];
+  uint32_t hist[kMaxBins];
+  uint8_t eq[kMaxBuckets];
+};
 
 // Shared-memory histogram increment (hardware-serialised on conflicts).
 __device__ __forceinline__ void hist_add(uint32_t* hist, int bin, bool valid) {
@@ -72,11 +95,13 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
                                                       TileSummary* __restrict__ sums, const K* __restrict__ spl,
                                                       const uint8_t* __restrict__ eqf, const int* __restrict__ mcount,
                                                       uint32_t* __restrict__ mat, int nbins, int G,
-                                                      uint32_t* __restrict__ tot) {
+                                                      uint32_t* __restrict__ tot, uint16_t* __restrict__ bins_out) {
   constexpr int U = 8;
-  __shared__ K s_spl[FUSE ? kMaxBuckets : 1];
-  __shared__ uint8_t s_eq[FUSE ? kMaxBuckets : 1];
-  __shared__ uint32_t s_hist[FUSE ? kMaxBins : 1];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ClassifySmem<K>& csm = *reinterpret_cast<ClassifySmem<K>*>(smem_raw);  // FUSE only (dynamic)
+  K* s_spl = csm.tree;
+  uint8_t* s_eq = csm.eq;
+  uint32_t* s_hist = csm.hist;
   __shared__ int32_t s_red[NT / 32 + 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t t0 = (int64_t)blockIdx.x * tile;
@@ -112,7 +137,11 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
       int bin[U];
       classify_keys<K, U>(x, bin, s_spl, s_eq, m);
 #pragma unroll
-      for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], base + u * NT + tid < t1);
+      for (int u = 0; u < U; u++) {
+        const int64_t i = base + u * NT + tid;
+        hist_add(s_hist, bin[u], i < t1);
+        if (bins_out && i < t1) bins_out[i] = (uint16_t)bin[u];  // reused by the scatter
+      }
     }
   }
   cd = block_reduce_sum<NT>(cd, s_red);

@@ -32,6 +32,10 @@ namespace {
 int g_force_route = 0;
 int g_profile = 0;
 int g_merge_route = 1;
+#ifndef SR_WARP_VT64
+#define SR_WARP_VT64 1
+#endif
+constexpr bool g_warp_vt64 = SR_WARP_VT64;
 
 struct ProfEntry {
   const char* name;
@@ -133,13 +137,16 @@ struct Ctx {
       fprintf(stderr, "[sr_sort] n=%lld route=%d launches=%d enqueue=%.1fus wait=%.1fus tail=%.1fus\n",
               (long long)plan.n, plan.route, plan.launches, t_enqueue * 1e6, t_wait * 1e6,
               std::chrono::duration<double>(std::chrono::steady_clock::now() - t_mark).count() * 1e6);
-    for (void* p : allocs) cudaFreeAsync(p, st);
-    if (up_off) {
-      ThreadState& ts = t_state;
-      if (!ts.up_done) cudaEventCreateWithFlags(&ts.up_done, cudaEventDisableTiming);
-      cudaEventRecord(ts.up_done, st);
-      ts.up_pending = true;
+    if (profile && getenv("SR_TIMELINE") && !t_state.prof.empty()) {
+      cudaStreamSynchronize(st);
+      for (auto& e : t_state.prof) {
+        float t0 = 0, d = 0;
+        cudaEventElapsedTime(&t0, t_state.prof[0].a, e.a);
+        cudaEventElapsedTime(&d, e.a, e.b);
+        fprintf(stderr, "[sr_timeline] %-18s start %9.1f us  dur %9.1f us\n", e.name, t0 * 1e3, d * 1e3);
+      }
     }
+    for (void* p : allocs) cudaFreeAsync(p, st);
   }
   // One stream-ordered pool allocation up front (reserve) that later allocs
   // carve from, so a call costs one cudaMallocAsync instead of dozens.
@@ -220,6 +227,9 @@ struct Ctx {
     std::memcpy(ts.up + o2, src.data(), bytes);
     check_cuda(cudaMemcpyAsync(dst, ts.up + o2, bytes, cudaMemcpyHostToDevice, st), "upload");
     up_off = o2 + bytes;
+    if (!ts.up_done) cudaEventCreateWithFlags(&ts.up_done, cudaEventDisableTiming);
+    cudaEventRecord(ts.up_done, st);  // the next call reuses the staging area once this copy is done
+    ts.up_pending = true;
   }
   // Readback of `bytes` from device into pinned memory + synchronise (the planner's host sync).
   double t_enqueue = 0, t_wait = 0;  // host seconds (SR_TIMING diagnostics)
@@ -253,13 +263,13 @@ void set_smem(Kern k, size_t bytes) {
 // ------------------------------------------------------------------ tunables
 constexpr int kScanNT = 256, kScanIPT = 16;              // K9
 constexpr int kFinNT = 256, kFinVT = 16;                 // K11 big items (two halves of 4096 = kCap)
-constexpr int kFinSmallNT = 128;                         // K11 small items (<= 2048 = kSmallItem)
-constexpr int kSplNT = 1024, kSplVT = 8;                 // K7 (S <= 8192)
+constexpr int kFinSmallNT = 128;                         // K11 small items (pairs, <= 2048 = kSmallItem)
+constexpr int kWarpItemsPerCta = 4;                      // K11w (keys only): warps per CTA
 constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
 constexpr int kScatKNT = 1024, kScatKVT = 8;             // K10 (keys only)
 constexpr int kScanNT1 = 1024;                           // K1
 constexpr int kCountNT = 1024;                           // K8
-constexpr int64_t kFuseMin = 16 * 1024 * 1024;          // fuse the level-1 histogram into K1 above this n
+constexpr int64_t kFuseMin = INT64_MAX;  // fusing the level-1 histogram into K1 costs presorted inputs more than it saves
 constexpr int kMergeNT = 256, kMergeVT = 16;             // K6
 constexpr int kMergeNV = kMergeNT * kMergeVT;
 static_assert(2 * kFinNT * kFinVT == kCap, "finishing item must equal kCap");
@@ -283,8 +293,12 @@ struct Sorter {
   int64_t n;
   K* wk = nullptr;
   uint32_t* wv = nullptr;
+  uint16_t* d_bins_all = nullptr;
   static constexpr int64_t kw = sizeof(K);
   static constexpr int64_t vw = HAS_V ? 4 : 0;
+  // keys only: warp-register finishing (32 lanes x VT keys); pairs: CTA merge sort
+  static constexpr int kWarpVT = (sizeof(K) == 4 && g_warp_vt64) ? 64 : 32;
+  static constexpr int kSmallMax = HAS_V ? kSmallItem : 32 * kWarpVT;
 
   Sorter(Ctx& ctx, K* k, uint32_t* v, int64_t nn) : c(ctx), keys(k), vals(v), n(nn) {}
 
@@ -305,7 +319,7 @@ struct Sorter {
     size_t smem = FinishSmem<K, HAS_V, NT, kFinVT>::bytes();
     auto kern = k_finish<K, HAS_V, NT, kFinVT, (NT == kFinNT)>;
     set_smem(kern, smem);
-    int grid = (int)std::min<int64_t>(max_items, 148 * 16);
+    int grid = (int)std::min<int64_t>(max_items, gate ? 148 * 6 : 148 * 16);  // gated launches: few CTAs if off
     K* kk = keys;
     uint32_t* vv = vals;
     const K* wkk = wk;
@@ -379,6 +393,7 @@ struct Sorter {
     // splitter sample: per-segment ranks (zeroed) and keys
     uint32_t* d_rank = nullptr;
     K* d_sample = nullptr;
+    uint16_t* d_bins = nullptr;  // per-key bucket ids from the count pass (indexed by position)
     int64_t sample_total = 0;
     int max_sample = 0;
   };
@@ -437,6 +452,8 @@ struct Sorter {
     }
     L.d_rank = reinterpret_cast<uint32_t*>(cb + rank_off);
     L.d_sample = c.alloc<K>(L.sample_total);
+    if (!d_bins_all) d_bins_all = c.alloc<uint16_t>(n);
+    L.d_bins = d_bins_all;
     L.items_cap = bins + lp / kFillChunk + (int64_t)parts.size() + 1;
     L.d_items = c.alloc<Item>(L.items_cap);
     L.d_items_big = c.alloc<Item>(bins);
@@ -477,9 +494,12 @@ struct Sorter {
     const K* src = buf_k(L.src);
     int64_t keys_in = 0;
     for (auto& s : L.segs) keys_in += s.len;
+    auto kern = k_count<K, kCountNT>;
+    const size_t smem = sizeof(ClassifySmem<K>);
+    set_smem(kern, smem);
     c.launch("count", keys_in * kw + L.mat_entries * 4, [&] {
-      k_count<K, kCountNT><<<(unsigned)L.total_chunks, kCountNT, 0, c.st>>>(
-          src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_tot, gate);
+      kern<<<(unsigned)L.total_chunks, kCountNT, smem, c.st>>>(
+          src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_tot, L.d_bins, gate);
     });
   }
 
@@ -496,7 +516,7 @@ struct Sorter {
     set_smem(kern, sizeof(PlanSmem));
     c.launch("plan", L.total_bins * 8, [&] {
       kern<<<S, 1024, sizeof(PlanSmem), c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_items_big,
-                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate);
+                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate, kSmallMax);
     });
   }
 
@@ -519,7 +539,7 @@ struct Sorter {
       set_smem(kern, smem);
       return c.launch("scatter", keys_in * kw + noneq * kw, [&] {
         kern<<<(unsigned)L.total_chunks, kScatKNT, smem, c.st>>>(sk, dk, L.d_segs, L.d_chunk_seg, L.chunk_size,
-                                                                 L.d_spl, L.d_eq, L.d_m, L.d_cursor, gate);
+                                                                 L.d_spl, L.d_eq, L.d_m, L.d_cursor, L.d_bins, gate);
       });
     }
     using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
@@ -529,24 +549,41 @@ struct Sorter {
     int64_t bytes = keys_in * (kw + vw) + noneq * kw + keys_in * vw + L.mat_entries * 4;
     return c.launch("scatter", bytes, [&] {
       kern<<<(unsigned)L.total_chunks, kScatNT, smem, c.st>>>(sk, sv, dk, dv, L.d_segs, L.d_chunk_seg, L.chunk_size,
-                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat, gate);
+                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_bins, gate);
     });
   }
 
   // hs == nullptr: speculative level-1 launch gated on the device route; the
   // grid is sized by the item capacity and idle CTAs exit.
+  // keys only: the small list (items <= 32*kWarpVT keys, and fills) goes to the
+  // warp-register kernel
+  int finish_small(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
+    if (HAS_V) return finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, max_items, bytes, gate, kRoutePartition);
+    if (max_items <= 0) return -1;
+    constexpr int VT = kWarpVT, W = kWarpItemsPerCta;
+    auto kern = k_finish_warp<K, VT, W>;
+    const size_t smem = sizeof(K) * 32 * VT * W;
+    set_smem(kern, smem);
+    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(max_items, W), gate ? 148 * 6 : 148 * 32);
+    K* kk = keys;
+    const K* wkk = wk;
+    const int64_t* cnt = &L.d_st->n_items;
+    return c.launch("finish_small", bytes, [&] {
+      kern<<<grid, 32 * W, smem, c.st>>>(L.d_items, cnt, kk, wkk, gate, kRoutePartition);
+    });
+  }
+
   int level_finish(Level& L, const DevStats* hs) {
     if (hs) {
       // sort items read+write the range buckets; fills write keys (+ move vals)
       int64_t bytes = 2 * (hs->noneq_total - hs->ovf_keys) * (kw + vw) + hs->eq_keys * kw +
                       (L.src == 0 ? 2 : 0) * hs->eq_keys * vw;
       c.plan.equal_keys += hs->eq_keys;
-      int h = finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, hs->n_items, bytes);
+      int h = finish_small(L, hs->n_items, bytes, nullptr);
       finish(L.d_items_big, &L.d_st->n_items_big, 0, hs->n_items_big, 0);
       return h;
     }
-    int h = finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, L.items_cap, 2 * n * (kw + vw), L.d_st,
-                                kRoutePartition);
+    int h = finish_small(L, L.items_cap, 2 * n * (kw + vw), L.d_st);
     c.unplan(finish(L.d_items_big, &L.d_st->n_items_big, 0, L.total_bins, 0, L.d_st, kRoutePartition));
     return h;
   }
@@ -840,7 +877,8 @@ struct Sorter {
       int64_t b = r(n * kw) + r(n * vw) + r(G * 32) + 2 * r((G + 1) * 32) + r(64) + r(G * 4) +
                   r(kMaxBuckets * kw) + r(kMaxBuckets) + r(4) + (HAS_V ? r(bins * G * 4) : 0) +
                   r(sizeof(DevStats) + 256 + 8 * ceil_div<int64_t>(bins * G, kScanNT * kScanIPT) + 4 * bins) +
-                  r(4 * bins) + r(24 * (bins + n / kFillChunk + 2)) + r(24 * bins) + r(16 * bins) + 8 * 256;
+                  r(4 * bins) + r(24 * (bins + n / kFillChunk + 2)) + r(24 * bins) + r(16 * bins) + r(2 * n) +
+                  r(kMaxSample * (kw + 4)) + 8 * 256;
       c.reserve((size_t)b);
     }
     // Large n: the level-1 histogram rides on the presortedness read (one HBM
@@ -861,21 +899,26 @@ struct Sorter {
     if (!part) c.memset0(d_pst, sizeof(DevStats));
     const K* kk = keys;
     const int nbins1 = part ? L1.segs[0].nbins : 0;
+    const size_t csmem = sizeof(ClassifySmem<K>);
+    if (fused) {
+      set_smem(k_presort_scan<K, true, true, kScanNT1>, csmem);
+      set_smem(k_presort_scan<K, false, true, kScanNT1>, csmem);
+    }
     c.launch("presort_scan", n * kw + (fused ? (int64_t)nbins1 * G * 4 : 0), [&] {
       if (fused) {
         if (HAS_V)
-          k_presort_scan<K, true, true, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot);
+          k_presort_scan<K, true, true, kScanNT1><<<(unsigned)G, kScanNT1, csmem, c.st>>>(
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins);
         else
-          k_presort_scan<K, false, true, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot);
+          k_presort_scan<K, false, true, kScanNT1><<<(unsigned)G, kScanNT1, csmem, c.st>>>(
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins);
       } else {
         if (HAS_V)
           k_presort_scan<K, true, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr);
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr);
         else
           k_presort_scan<K, false, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr);
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr);
       }
     });
     const int merge_ok = g_merge_route;
