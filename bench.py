@@ -124,11 +124,53 @@ class ClockSampler:
                 "samples": len(self.sm), "sm_mhz_min": min(self.sm)}
 
 
+# bench kernel names (sr_last_profile) -> ncu kernel-name prefixes
+NCU_NAMES = {"presort_scan": "k_presort_scan", "presort_resolve": "k_presort_resolve", "reverse": "k_reverse",
+             "sample_rank": "k_sample_rank", "select_splitters": "k_select_splitters", "count": "k_count",
+             "plan": "k_plan", "scatter": "k_scatter", "finish_small": "k_finish_warp", "finish": "k_finish<",
+             "merge": "k_merge<", "scan": "k_scan_u32"}
+
+
+def ncu_traffic(kernel: str, dtype_name: str):
+    """DRAM read+write bytes per launch of `kernel` from the newest committed
+    ncu --set full summary (profiles/*_ncu_summary.json), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
+    pref = NCU_NAMES.get(kernel)
+    for f in reversed(files):
+        try:
+            full = json.load(open(f)).get("full", {})
+        except Exception:
+            continue
+        for name, d in full.items():
+            if pref and name.startswith(pref) and f"<{dtype_name}" in name.replace(" ", ""):
+                r, w = d.get("dram_bytes_read") or 0, d.get("dram_bytes_write") or 0
+                return {"bytes": int(r + w), "source": os.path.relpath(f, ROOT), "ncu_kernel": name}
+    return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def instance_ids(rank: int, per_rank: int) -> list:
+    """Weak scaling over independent problems: rank r sorts its own instances
+    r*per_rank .. r*per_rank+per_rank-1 (no data-path collective)."""
+    return [rank * per_rank + i for i in range(per_rank)]
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank time over all ranks (1 rank: identity)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_reference(args, wl):
@@ -224,9 +266,10 @@ def main():
     ninst = 1 if big else total
     pristine = {}
     host_inputs = {}
+    ids = instance_ids(rank, total)
     for o in orders:
         for i in range(ninst):
-            a = make_input(o, n, dtype, cfg, rank * total + i)
+            a = make_input(o, n, dtype, cfg, ids[i])
             pristine[(o, i)] = torch.from_numpy(a).to(dev)
             if i == 0:
                 host_inputs[o] = a
@@ -266,11 +309,7 @@ def main():
         torch.distributed.barrier()
     per_order_ms = {o: [evs[s][j][0].elapsed_time(evs[s][j][1]) for s in range(args.steps)] for j, o in enumerate(orders)}
     step_ms = [sum(evs[s][j][0].elapsed_time(evs[s][j][1]) for j in range(len(orders))) for s in range(args.steps)]
-    total_ms = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), dev)
     keys_all = n * len(orders) * args.steps * ws
     value = keys_all / (total_ms / 1e3) / 1e6
     launches = sum(p["launches"] for _, p in plans)
@@ -294,10 +333,7 @@ def main():
                 b.synchronize()
                 if s >= args.warmup:
                     e2e_ms += a.elapsed_time(b)
-        if ws > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms, dev)
         e2e = {"value": round(keys_all / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mkeys/s",
                "h2d_bytes_per_step": n * kw * len(orders), "d2h_bytes_per_step": n * kw * len(orders),
                "ms_per_step": round(e2e_ms / args.steps, 4)}
@@ -321,8 +357,11 @@ def main():
     bytes_per_launch = d["bytes"] / d["launches"]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     kern_total = sum(v["ms"] for v in kern.values())
+    tr = ncu_traffic(dname, "int" if dtype == np.int32 else "long")
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                "frac": round(achieved / hbm, 4), "traffic": tr["bytes"] if tr else None,
+                "traffic_source": tr, "algorithmic_bytes_per_launch": int(bytes_per_launch),
+                "avg_launch_ms": round(avg_ms, 5), "peak_source": hbm_src,
                 "share_of_kernel_time": round(d["ms"] / kern_total, 3),
                 "kernels": {k: {"ms_per_launch": round(v["ms"] / v["launches"], 4),
                                 "GBps": round(v["bytes"] / v["launches"] / (v["ms"] / v["launches"] / 1e3) / 1e9, 1),

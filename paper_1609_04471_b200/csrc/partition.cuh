@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
   // item lengths per bin (0 = no item); fills split into kFillChunk pieces
   constexpr int IPT = (kMaxBins + NT - 1) / NT;
   int n_small = 0, n_big = 0, n_ovf = 0;
+  long long bigk = 0;
   for (int k = 0; k < IPT; k++) {
     int b = threadIdx.x + k * NT;
     if (b >= nb) break;
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
     int len = ty == (kBinSmall | 0x80) ? ((b + 1 < nb ? sm.next[b + 1] : (int32_t)send) - sm.p[b])
                                        : (ty == kBinBig ? c : 0);
     if (len) (len <= small_max ? n_small : n_big)++;
+    if (len > small_max) bigk += len;
     if (ty == kBinFill) n_small += (c + kFillChunk - 1) / kFillChunk;
     if (ty == kBinOvf) n_ovf++;
   }
@@ -447,7 +449,9 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
   noneq = block_reduce_sum<NT>(noneq, s_red64);
   eqk = block_reduce_sum<NT>(eqk, s_red64);
   ovk = block_reduce_sum<NT>(ovk, s_red64);
+  bigk = block_reduce_sum<NT>(bigk, s_red64);
   if (threadIdx.x == 0) {
+    if (bigk) atomicAdd((unsigned long long*)&st->big_keys, (unsigned long long)bigk);
     atomicAdd((unsigned long long*)&st->noneq_total, (unsigned long long)noneq);
     atomicAdd((unsigned long long*)&st->eq_keys, (unsigned long long)eqk);
     atomicAdd((unsigned long long*)&st->ovf_keys, (unsigned long long)ovk);

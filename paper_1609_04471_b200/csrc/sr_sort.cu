@@ -199,11 +199,13 @@ struct Ctx {
     launched.push_back({bytes, profile ? (int)t_state.prof.size() - 1 : -1});
     return (int)launched.size() - 1;
   }
-  void unplan(int h) {
+  void unplan(int h) { replan(h, 0); }
+  // Correct the algorithmic bytes of launch h once the statistics are known.
+  void replan(int h, int64_t bytes) {
     if (h < 0) return;
-    plan.bytes_planned -= launched[h].first;
-    if (launched[h].second >= 0) t_state.prof[launched[h].second].bytes = 0;
-    launched[h].first = 0;
+    plan.bytes_planned += bytes - launched[h].first;
+    if (launched[h].second >= 0) t_state.prof[launched[h].second].bytes = bytes;
+    launched[h].first = bytes;
   }
   std::vector<std::pair<int64_t, int>> launched;
   void memset0(void* p, size_t bytes) { check_cuda(cudaMemsetAsync(p, 0, bytes, st), "cudaMemsetAsync"); }
@@ -575,18 +577,20 @@ struct Sorter {
 
   int level_finish(Level& L, const DevStats* hs) {
     if (hs) {
-      // sort items read+write the range buckets; fills write keys (+ move vals)
-      int64_t bytes = 2 * (hs->noneq_total - hs->ovf_keys) * (kw + vw) + hs->eq_keys * kw +
+      // sort items read+write their range keys; fills write keys (+ move vals)
+      const int64_t big = hs->big_keys;
+      int64_t bytes = 2 * (hs->noneq_total - hs->ovf_keys - big) * (kw + vw) + hs->eq_keys * kw +
                       (L.src == 0 ? 2 : 0) * hs->eq_keys * vw;
       c.plan.equal_keys += hs->eq_keys;
       int h = finish_small(L, hs->n_items, bytes, nullptr);
-      finish(L.d_items_big, &L.d_st->n_items_big, 0, hs->n_items_big, 0);
+      finish(L.d_items_big, &L.d_st->n_items_big, 0, hs->n_items_big, 2 * big * (kw + vw));
       return h;
     }
     int h = finish_small(L, L.items_cap, 2 * n * (kw + vw), L.d_st);
-    c.unplan(finish(L.d_items_big, &L.d_st->n_items_big, 0, L.total_bins, 0, L.d_st, kRoutePartition));
+    h_fin_big = finish(L.d_items_big, &L.d_st->n_items_big, 0, L.total_bins, 0, L.d_st, kRoutePartition);
     return h;
   }
+  int h_fin_big = -1;
 
   // Partition levels >= 2 (segments from the previous level's oversized buckets).
   void run_levels(std::vector<OvfSeg> parts, int src) {
@@ -957,11 +961,14 @@ struct Sorter {
     if (route != kRoutePartition) c.unplan(h_count);
     if (route != kRouteTile) c.unplan(h_tile);
     if (route != kRoutePartition || (!HAS_V && hs.noneq_total == 0)) c.unplan(h_scat);
-    if (route != kRoutePartition) c.unplan(h_fin);
+    if (route != kRoutePartition) { c.unplan(h_fin); c.unplan(h_fin_big); }
     if (part && route == kRoutePartition) {  // fix the finish bytes to the real item mix
-      c.unplan(h_fin);
+      c.replan(h_fin, 2 * (hs.noneq_total - hs.ovf_keys - hs.big_keys) * (kw + vw) + hs.eq_keys * kw +
+                          2 * hs.eq_keys * vw);
+      c.replan(h_fin_big, 2 * hs.big_keys * (kw + vw));
+      c.replan(h_scat, (!HAS_V && hs.noneq_total == 0) ? 0
+                                                        : n * (kw + vw) + 2 * n + hs.noneq_total * kw + (HAS_V ? n * vw : 0));
       c.plan.equal_keys += hs.eq_keys;
-      c.plan.bytes_planned += 2 * (hs.noneq_total - hs.ovf_keys) * (kw + vw) + hs.eq_keys * kw + 2 * hs.eq_keys * vw;
     }
     switch (route) {
       case kRouteSorted:  // is_sorted exit

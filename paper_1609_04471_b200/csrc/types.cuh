@@ -37,7 +37,7 @@ struct DevStats {
   int64_t eq_keys;
   int64_t error;        // device-detected inconsistency (must stay 0)
   int64_t route;        // device-side route decision (kRoute*)
-  int64_t pad[1];
+  int64_t big_keys;     // keys in large finishing items
 };
 
 // One segment of a partition level (H7-H10).
