@@ -96,12 +96,14 @@ __device__ void smem_scan(T* a, int L, T identity, Op op, bool exclusive, bool r
 // keys ordered before it (<= for j < i, < for j > i), then adds the partial
 // count to rank[i].  O(S^2) compare+add pairs spread over the whole GPU, no
 // serial merge levels.
-template <typename K, int NT, int J>
+template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_sample_rank(const K* __restrict__ src, const SegDesc* __restrict__ segs,
                                                      int oversample, uint32_t* __restrict__ rank,
                                                      K* __restrict__ sample, const DevStats* __restrict__ gate) {
   if (gate && gate->route != kRoutePartition) return;  // speculative launch
-  __shared__ K s_chunk[kMaxSample / J + 4];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* s_chunk = reinterpret_cast<K*>(smem_raw);  // ceil(S_max / J) keys
+  const int J = gridDim.y;
   const SegDesc seg = segs[blockIdx.z];
   int64_t S64 = (int64_t)seg.nbuckets * oversample;
   if (S64 > seg.len) S64 = seg.len;
@@ -115,17 +117,16 @@ __global__ void __launch_bounds__(NT) k_sample_rank(const K* __restrict__ src, c
   const int j1 = j0 + cj < S ? j0 + cj : S;
   if (j0 >= j1) return;
   const int len = j1 - j0;
-  {
-    constexpr int PER = (kMaxSample / J + NT - 1) / NT;
-    K y[PER];
+  for (int base = 0; base < len; base += 8 * NT) {  // 8 gathers per thread in flight
+    K y[8];
 #pragma unroll
-    for (int u = 0; u < PER; u++) {
-      const int jj = u * NT + threadIdx.x;
+    for (int u = 0; u < 8; u++) {
+      const int jj = base + u * NT + threadIdx.x;
       y[u] = jj < len ? src[sample_position(seg.start, seg.len, S, j0 + jj, log2S)] : K(0);
     }
 #pragma unroll
-    for (int u = 0; u < PER; u++) {
-      const int jj = u * NT + threadIdx.x;
+    for (int u = 0; u < 8; u++) {
+      const int jj = base + u * NT + threadIdx.x;
       if (jj < len) s_chunk[jj] = y[u];
     }
   }
@@ -185,6 +186,53 @@ __global__ void __launch_bounds__(NT) k_select_splitters(const SegDesc* __restri
   if (threadIdx.x == 0) m_out[blockIdx.x] = B - 1;
 }
 
+// K7 (small samples, e.g. every level >= 2 segment): one CTA per segment
+// gathers its S <= NT*VT samples, sorts them with the register/shuffle bitonic
+// network and selects the splitters + gamma flags like K7b.
+template <typename K, int NT, int VT>
+__global__ void __launch_bounds__(NT) k_sample_sort(const K* __restrict__ src, const SegDesc* __restrict__ segs,
+                                                     int oversample, K* __restrict__ spl_out,
+                                                     uint8_t* __restrict__ eq_out, int* __restrict__ m_out,
+                                                     const DevStats* __restrict__ gate) {
+  if (gate && gate->route != kRoutePartition) return;  // speculative launch
+  using BT = BitonicSort<K, NT, VT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sorted = reinterpret_cast<K*>(smem_raw);  // BT::SMEM keys
+  const SegDesc seg = segs[blockIdx.x];
+  const int B = seg.nbuckets;
+  int64_t S64 = (int64_t)B * oversample;
+  if (S64 > seg.len) S64 = seg.len;
+  if (S64 > BT::NV) S64 = BT::NV;
+  const int S = (int)S64;
+  const int log2S = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
+  {
+    K y[VT];
+#pragma unroll
+    for (int u = 0; u < VT; u++) {
+      const int k = u * NT + threadIdx.x;
+      y[u] = k < S ? src[sample_position(seg.start, seg.len, S, k, log2S)] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < VT; u++) {
+      const int k = u * NT + threadIdx.x;
+      if (k < S) sorted[k] = y[u];
+    }
+  }
+  __syncthreads();
+  BT::sort(sorted, S);
+  K* out = spl_out + (int64_t)blockIdx.x * kMaxBuckets;
+  uint8_t* eo = eq_out + (int64_t)blockIdx.x * kMaxBuckets;
+  for (int j = threadIdx.x; j < B - 1; j += NT) {
+    const int r = (int)(((int64_t)(j + 1) * S) / B);
+    const K t = sorted[r];
+    const bool m1 = r >= 1 && sorted[r - 1] == t, m2 = r >= 2 && sorted[r - 2] == t;
+    const bool p1 = r + 1 < S && sorted[r + 1] == t, p2 = r + 2 < S && sorted[r + 2] == t;
+    out[j] = t;
+    eo[j] = ((m1 && m2) || (m1 && p1) || (p1 && p2)) ? 1 : 0;  // count > gamma = 2
+  }
+  if (threadIdx.x == 0) m_out[blockIdx.x] = B - 1;
+}
+
 // ---------------------------------------------------------------------------
 // K8: bucket histogram of one chunk (levels >= 2; level 1 fuses it into K1).
 template <typename K, int NT>
@@ -206,6 +254,7 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
   const SegDesc seg = segs[s];
   const int g = c - seg.chunk_base;
   const int m = m_all[s];
+  const int depth = tree_depth(m);
   load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, s_spl, s_eq);
   for (int b = threadIdx.x; b < seg.nbins; b += NT) s_hist[b] = 0;
   __syncthreads();
@@ -219,7 +268,7 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
       x[u] = i < c1 ? src[i] : K(0);
     }
     int bin[U];
-    classify_keys<K, U>(x, bin, s_spl, s_eq, m);
+    classify_keys<K, U>(x, bin, s_spl, s_eq, m, depth);
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t i = base + u * NT + threadIdx.x;
@@ -505,6 +554,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
   const int g = c - seg.chunk_base;
   const int nb = seg.nbins;
   const int m = m_all[s];
+  const int depth = tree_depth(m);
   load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
   for (int b = tid; b < nb; b += NT)
     sm.cur[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * seg.nchunks + g] - seg.len_prefix));
@@ -529,7 +579,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
       bool valid = pos < c1;
-      int b = !valid ? kMaxBins : (bins_in ? (int)bins_in[pos] : classify_key<K>(x[i], sm.spl, sm.eq, m));
+      int b = !valid ? kMaxBins : (bins_in ? (int)bins_in[pos] : classify_key<K>(x[i], sm.spl, sm.eq, m, depth));
       unsigned peers = __match_any_sync(0xffffffffu, b);
       int base = sm.wcnt[w][b];
       rk[i] = base + __popc(peers & lt);
@@ -592,6 +642,7 @@ struct ScatterKeysSmem {
   uint32_t cnt[kMaxBins];
   uint32_t lstart[kMaxBins];
   uint32_t base[kMaxBins];
+  uint32_t run[kMaxBins];  // matrix mode: running destination of each bucket in this chunk
   uint16_t stb[ST];
   uint8_t eq[kMaxBuckets];
   uint32_t red[NT / 32 + 1];
@@ -605,6 +656,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
                                                       const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
                                                       const int* __restrict__ m_all, uint32_t* __restrict__ cursor,
                                                       const uint16_t* __restrict__ bins_in,
+                                                      const uint32_t* __restrict__ mat,
                                                       const DevStats* __restrict__ gate) {
   if (gate && (gate->route != kRoutePartition || gate->noneq_total == 0)) return;
   using SM = ScatterKeysSmem<K, NT, VTS>;
@@ -618,7 +670,11 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
   const int g = c - seg.chunk_base;
   const int nb = seg.nbins;
   const int m = m_all[s];
-  uint32_t* cur = cursor + seg.mat_base;
+  const int depth = tree_depth(m);
+  uint32_t* cur = mat ? nullptr : cursor + seg.mat_base;
+  if (mat)  // matrix mode (large levels): this chunk's slice of every bucket, no global atomics
+    for (int b = tid; b < nb; b += NT)
+      sm.run[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * seg.nchunks + g] - seg.len_prefix));
   if (!bins_in) load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
@@ -634,7 +690,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
       x[i] = pos < c1 ? src[pos] : K(0);
       if (bins_in) bin[i] = pos < c1 ? (int)bins_in[pos] : 0;
     }
-    if (!bins_in) classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m);
+    if (!bins_in) classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m, depth);
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
       int64_t pos = sub + i * NT + tid;
@@ -646,7 +702,12 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
     for (int b = tid; b < nb; b += NT) {
       uint32_t cb = sm.cnt[b];
       sm.lstart[b] = cb;
-      if (cb) sm.base[b] = atomicAdd(&cur[b], cb);
+      if (mat) {
+        sm.base[b] = sm.run[b];
+        sm.run[b] += cb;
+      } else if (cb) {
+        sm.base[b] = atomicAdd(&cur[b], cb);
+      }
     }
     __syncthreads();
     smem_scan<NT>(sm.lstart, nb, 0u, [](uint32_t a, uint32_t b) { return a + b; }, true, false, sm.red);

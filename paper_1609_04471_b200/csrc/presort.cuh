@@ -27,46 +27,57 @@ static_assert((1 << kTreeLevels) == kMaxBuckets, "");
 // equality splitter (3-way split, switched on per splitter
 // by the gamma test of PAPER.md:168), else 2i.
 template <typename K>
-__device__ __forceinline__ int classify_key(K x, const K* tree, const uint8_t* eqf, int m) {
+__device__ __forceinline__ int classify_key(K x, const K* tree, const uint8_t* eqf, int m, int depth) {
   int j = 1;
-#pragma unroll
-  for (int l = 0; l < kTreeLevels; l++) j = 2 * j + (tree[j] < x ? 1 : 0);
-  const int i = j - kMaxBuckets;
+  for (int l = 0; l < depth; l++) j = 2 * j + (tree[j] < x ? 1 : 0);
+  const int i = j - (1 << depth);
   return 2 * i + ((i < m && tree[kMaxBuckets + i] == x && eqf[i]) ? 1 : 0);
 }
 
 // Batched classification: the U searches advance in lockstep so their
-// shared-memory loads are independent and overlap (U-way ILP).
+// shared-memory loads are independent and overlap (U-way ILP).  depth =
+// log2(padded bucket count) of this segment (<= kTreeLevels).
 template <typename K, int U>
-__device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], const K* tree, const uint8_t* eqf, int m) {
+__device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], const K* tree, const uint8_t* eqf, int m,
+                                              int depth) {
   int j[U];
 #pragma unroll
   for (int u = 0; u < U; u++) j[u] = 1;
-#pragma unroll
-  for (int l = 0; l < kTreeLevels; l++) {
+#pragma unroll 1
+  for (int l = 0; l < depth; l++) {
 #pragma unroll
     for (int u = 0; u < U; u++) j[u] = 2 * j[u] + (tree[j[u]] < x[u] ? 1 : 0);
   }
 #pragma unroll
   for (int u = 0; u < U; u++) {
-    const int i = j[u] - kMaxBuckets;
+    const int i = j[u] - (1 << depth);
     bin[u] = 2 * i + ((i < m && tree[kMaxBuckets + i] == x[u] && eqf[i]) ? 1 : 0);
   }
 }
 
-// Build the search structure (2*kMaxBuckets entries of s_tree, kMaxBuckets
-// flags) from the m sorted splitters.
+// Build the search structure from the m sorted splitters: tree[1..2^depth)
+// in level order (splitters padded with +inf to 2^depth - 1), the sorted
+// splitters at tree[kMaxBuckets..), flags eqf[0..m).  depth = tree_depth(m).
+__host__ __device__ __forceinline__ int tree_depth(int m) {
+  int d = 1;
+  while ((1 << d) - 1 < m) d++;
+  return d;
+}
 template <typename K>
 __device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_tree,
                                                     uint8_t* s_eq) {
+  const int depth = tree_depth(m);
+  const int nodes = 1 << depth;
   for (int i = threadIdx.x; i < kMaxBuckets; i += blockDim.x) {
-    const K v = i < m ? spl[i] : KeyTraits<K>::max_key();
-    s_tree[kMaxBuckets + i] = v;
-    s_eq[i] = i < m ? eqf[i] : 0;
-    if (i >= 1) {  // node i of the level-order tree <- sorted position pos(i)
-      const int d = 31 - __clz(i);
-      const int pos = ((2 * (i - (1 << d)) + 1) << (kTreeLevels - 1 - d)) - 1;
-      s_tree[i] = pos < m ? spl[pos] : KeyTraits<K>::max_key();
+    if (i < nodes) {
+      const K v = i < m ? spl[i] : KeyTraits<K>::max_key();
+      s_tree[kMaxBuckets + i] = v;
+      s_eq[i] = i < m ? eqf[i] : 0;
+      if (i >= 1) {  // node i of the level-order tree <- sorted position pos(i)
+        const int d = 31 - __clz(i);
+        const int pos = ((2 * (i - (1 << d)) + 1) << (depth - 1 - d)) - 1;
+        s_tree[i] = pos < m ? spl[pos] : KeyTraits<K>::max_key();
+      }
     }
   }
 }
@@ -106,9 +117,10 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t t0 = (int64_t)blockIdx.x * tile;
   const int64_t t1 = t0 + tile < n ? t0 + tile : n;
-  int m = 0;
+  int m = 0, depth = 1;
   if (FUSE) {
     m = mcount[0];
+    depth = tree_depth(m);
     load_splitters_smem(spl, eqf, m, s_spl, s_eq);
     for (int b = tid; b < nbins; b += NT) s_hist[b] = 0;
     __syncthreads();
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
     }
     if (FUSE) {
       int bin[U];
-      classify_keys<K, U>(x, bin, s_spl, s_eq, m);
+      classify_keys<K, U>(x, bin, s_spl, s_eq, m, depth);
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int64_t i = base + u * NT + tid;

@@ -271,6 +271,7 @@ constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
 constexpr int kScatKNT = 1024, kScatKVT = 8;             // K10 (keys only)
 constexpr int kScanNT1 = 1024;                           // K1
 constexpr int kCountNT = 1024;                           // K8
+constexpr int64_t kAtomicMaxEntries = 2 << 20;  // keys-only count-matrix threshold (entries)
 constexpr int64_t kFuseMin = INT64_MAX;  // fusing the level-1 histogram into K1 costs presorted inputs more than it saves
 constexpr int kMergeNT = 256, kMergeVT = 16;             // K6
 constexpr int kMergeNV = kMergeNT * kMergeVT;
@@ -281,8 +282,10 @@ int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
   int64_t t = pow2ceil(std::max<int64_t>(1, n / 512));
   return std::min<int64_t>(65536, std::max<int64_t>(8192, t));
 }
-int choose_buckets(int64_t len) {
-  int64_t b = pow2ceil(ceil_div<int64_t>(len, kTargetBucket));
+// Buckets per segment: mean bucket ~kTargetBucket at level 1, ~kTargetBucket/2
+// below (those buckets are finished by one warp with 32 keys per lane).
+int choose_buckets(int64_t len, int level = 1) {
+  int64_t b = pow2ceil(ceil_div<int64_t>(len, level > 1 ? kTargetBucket / 2 : kTargetBucket));
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
@@ -298,9 +301,6 @@ struct Sorter {
   uint16_t* d_bins_all = nullptr;
   static constexpr int64_t kw = sizeof(K);
   static constexpr int64_t vw = HAS_V ? 4 : 0;
-  // keys only: warp-register finishing (32 lanes x VT keys); pairs: CTA merge sort
-  static constexpr int kWarpVT = (sizeof(K) == 4 && g_warp_vt64) ? 64 : 32;
-  static constexpr int kSmallMax = HAS_V ? kSmallItem : 32 * kWarpVT;
 
   Sorter(Ctx& ctx, K* k, uint32_t* v, int64_t nn) : c(ctx), keys(k), vals(v), n(nn) {}
 
@@ -388,6 +388,9 @@ struct Sorter {
     int64_t items_cap = 0;
     OvfSeg* d_ovf = nullptr;
     int src = 0;
+    int level = 1;
+    int warp_vt = 64;   // keys-only finishing: keys per lane (items <= 32 * warp_vt)
+    int small_max = kSmallItem;
     // keys only: bucket totals + cursors instead of a count matrix (atomic scatter)
     bool atomic = false;
     uint32_t* d_tot = nullptr;
@@ -400,17 +403,27 @@ struct Sorter {
     int max_sample = 0;
   };
 
-  void level_alloc(Level& L, const std::vector<OvfSeg>& parts, int64_t chunk_size, int src, int forced_b = 0) {
+  void level_alloc(Level& L, const std::vector<OvfSeg>& parts, int64_t chunk_size, int src, int forced_b = 0,
+                   int level = 1) {
     L.src = src;
     L.chunk_size = chunk_size;
-    L.atomic = !HAS_V;
+    L.level = level;
+    L.warp_vt = (sizeof(K) == 4 && level == 1) ? 64 : 32;
+    L.small_max = HAS_V ? kSmallItem : 32 * L.warp_vt;
+    {  // keys only: atomic bucket reservation while the count matrix would be small,
+       // else the matrix (one scan) -- thousands of CTAs hammering 4k cursors is slower
+      int64_t ent = 0;
+      for (auto& p : parts)
+        ent += (2 * (int64_t)(forced_b ? forced_b : choose_buckets(p.len, level)) + 1) * ceil_div<int64_t>(p.len, chunk_size);
+      L.atomic = !HAS_V && ent <= kAtomicMaxEntries;
+    }
     int64_t chunk_base = 0, mat = 0, lp = 0, bins = 0;
     std::vector<int> chunk_seg;
     for (size_t s = 0; s < parts.size(); s++) {
       SegDesc d;
       d.start = parts[s].start;
       d.len = parts[s].len;
-      d.nbuckets = forced_b ? forced_b : choose_buckets(d.len);
+      d.nbuckets = forced_b ? forced_b : choose_buckets(d.len, level);
       d.nbins = 2 * d.nbuckets + 1;
       d.nchunks = (int32_t)ceil_div<int64_t>(d.len, chunk_size);
       d.chunk_base = (int32_t)chunk_base;
@@ -471,8 +484,24 @@ struct Sorter {
   // K7a + K7b.  gate: device stats whose route must be PARTITION (level-1
   // launches that precede the host's route decision), or nullptr.
   void level_splitters(Level& L, const DevStats* gate = nullptr) {
-    constexpr int NT = 128, J = 8;
+    constexpr int NT = 128;
     const K* src = buf_k(L.src);
+    if (L.segs.size() > 1 || L.max_sample <= 2048) {  // many segments (levels >= 2): one CTA sorts each sample
+      using BT = BitonicSort<K, 1024, 8>;
+      auto kern = k_sample_sort<K, 1024, 8>;
+      const size_t smem = sizeof(K) * BT::SMEM;
+      set_smem(kern, smem);
+      const int S = (int)L.segs.size();
+      c.launch("sample_sort", L.sample_total * kw, [&] {
+        kern<<<S, 1024, smem, c.st>>>(src, L.d_segs, kOversample, L.d_spl, L.d_eq, L.d_m, gate);
+      });
+      return;
+    }
+    // split each sample's comparisons over J chunks only when the sample is
+    // large enough to keep a CTA busy (level 1); small level-2 samples: J = 1
+    const int J = (int)std::max<int64_t>(1, std::min<int64_t>(8, L.max_sample / 1024));
+    const size_t rsmem = sizeof(K) * (size_t)ceil_div<int64_t>(L.max_sample, J);
+    set_smem(k_sample_rank<K, NT>, rsmem);
     const int S = (int)L.segs.size();
     int64_t pairs = 0;
     for (auto& sd : L.segs) {
@@ -481,7 +510,7 @@ struct Sorter {
     }
     dim3 grid((unsigned)ceil_div<int64_t>(L.max_sample, NT), J, (unsigned)S);
     c.launch("sample_rank", L.sample_total * kw * 2, [&] {
-      k_sample_rank<K, NT, J><<<grid, NT, 0, c.st>>>(src, L.d_segs, kOversample, L.d_rank, L.d_sample, gate);
+      k_sample_rank<K, NT><<<grid, NT, rsmem, c.st>>>(src, L.d_segs, kOversample, L.d_rank, L.d_sample, gate);
     });
     auto kern = k_select_splitters<K, 1024>;
     size_t smem = sizeof(K) * kMaxSample;
@@ -518,7 +547,7 @@ struct Sorter {
     set_smem(kern, sizeof(PlanSmem));
     c.launch("plan", L.total_bins * 8, [&] {
       kern<<<S, 1024, sizeof(PlanSmem), c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_items_big,
-                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate, kSmallMax);
+                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate, L.small_max);
     });
   }
 
@@ -534,14 +563,15 @@ struct Sorter {
     for (auto& s : L.segs) keys_in += s.len;
     const int64_t noneq = hs ? hs->noneq_total : keys_in;
     const DevStats* gate = hs ? nullptr : L.d_st;
-    if (L.atomic) {
+    if (!HAS_V) {
       using SM = ScatterKeysSmem<K, kScatKNT, kScatKVT>;
       size_t smem = sizeof(SM);
       auto kern = k_scatter_keys<K, kScatKNT, kScatKVT>;
       set_smem(kern, smem);
       return c.launch("scatter", keys_in * kw + noneq * kw, [&] {
         kern<<<(unsigned)L.total_chunks, kScatKNT, smem, c.st>>>(sk, dk, L.d_segs, L.d_chunk_seg, L.chunk_size,
-                                                                 L.d_spl, L.d_eq, L.d_m, L.d_cursor, L.d_bins, gate);
+                                                                 L.d_spl, L.d_eq, L.d_m, L.d_cursor, L.d_bins,
+                                                                 L.atomic ? nullptr : L.d_mat, gate);
       });
     }
     using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
@@ -559,10 +589,9 @@ struct Sorter {
   // grid is sized by the item capacity and idle CTAs exit.
   // keys only: the small list (items <= 32*kWarpVT keys, and fills) goes to the
   // warp-register kernel
-  int finish_small(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
-    if (HAS_V) return finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, max_items, bytes, gate, kRoutePartition);
-    if (max_items <= 0) return -1;
-    constexpr int VT = kWarpVT, W = kWarpItemsPerCta;
+  template <int VT>
+  int finish_warp(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
+    constexpr int W = kWarpItemsPerCta;
     auto kern = k_finish_warp<K, VT, W>;
     const size_t smem = sizeof(K) * 32 * VT * W;
     set_smem(kern, smem);
@@ -573,6 +602,12 @@ struct Sorter {
     return c.launch("finish_small", bytes, [&] {
       kern<<<grid, 32 * W, smem, c.st>>>(L.d_items, cnt, kk, wkk, gate, kRoutePartition);
     });
+  }
+  int finish_small(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
+    if (HAS_V) return finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, max_items, bytes, gate, kRoutePartition);
+    if (max_items <= 0) return -1;
+    if (L.warp_vt == 64 && sizeof(K) == 4) return finish_warp<64>(L, max_items, bytes, gate);
+    return finish_warp<32>(L, max_items, bytes, gate);
   }
 
   int level_finish(Level& L, const DevStats* hs) {
@@ -601,7 +636,7 @@ struct Sorter {
       for (auto& p : parts) tot += p.len;
       int64_t cs = std::min<int64_t>(65536, std::max<int64_t>(4096, pow2ceil(std::max<int64_t>(1, tot / 512))));
       Level L;
-      level_alloc(L, parts, cs, src);
+      level_alloc(L, parts, cs, src, 0, level);
       level_splitters(L);
       level_count(L);
       level_scan_plan(L);
