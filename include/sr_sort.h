@@ -103,7 +103,10 @@ const char *sr_last_error(void); /* thread-local; "" when none */
 enum {
   SR_OPT_FORCE_ROUTE = 0, /* 0 auto, SR_ROUTE_MERGE or SR_ROUTE_PARTITION (tests, ablations) */
   SR_OPT_PROFILE = 1,     /* 1: time every kernel with CUDA events (see sr_last_profile) */
-  SR_OPT_MERGE_ROUTE = 2  /* 0: never choose the merge route automatically */
+  SR_OPT_MERGE_ROUTE = 2, /* 0: never choose the merge route automatically */
+  SR_OPT_RESIDENT = 3,    /* 0: never use the single-launch resident path (keys only, 8192 < n <= 2^22) */
+  SR_OPT_RESIDENT_CAP = 4 /* resident path: largest bucket finished in-kernel, 1..4096 (default 4096);
+                             larger buckets go to the next partition level (tests lower it) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

@@ -116,6 +116,7 @@ struct BlockSort {
   __device__ __forceinline__ static uint32_t lo32(uint32_t x) { return x; }
   template <typename T>
   __device__ __forceinline__ static void store_vec(T* base, const T (&x)[VT]) {
+    static_assert((VT * sizeof(T)) % 16 == 0, "blocked vector I/O needs VT * sizeof(T) to be a multiple of 16");
     uint4* p = reinterpret_cast<uint4*>(base);
     if constexpr (sizeof(T) == 4) {
 #pragma unroll
@@ -131,6 +132,7 @@ struct BlockSort {
   }
   template <typename T>
   __device__ __forceinline__ static void load_vec(const T* base, T (&x)[VT]) {
+    static_assert((VT * sizeof(T)) % 16 == 0, "blocked vector I/O needs VT * sizeof(T) to be a multiple of 16");
     const uint4* p = reinterpret_cast<const uint4*>(base);
     if constexpr (sizeof(T) == 4) {
 #pragma unroll

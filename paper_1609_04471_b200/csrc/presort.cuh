@@ -180,11 +180,14 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
 
 // K2: resolve tile summaries into D, the long runs of both directions and
 // their covers (single CTA; loops over the tiles with a carried prefix).
+// Block-level body of K2 (all NT threads of one CTA call it); also run by CTA 0
+// of the resident kernel (resident.cuh).  Cross-CTA inputs are read with
+// __ldcg so a caller that produced them in an earlier grid-sync phase sees them.
 template <typename K, int NT>
-__global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ keys, int64_t n,
-                                                         const TileSummary* __restrict__ sums, int G, int64_t lmin,
-                                                         RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
-                                                         DevStats* __restrict__ st, int force, int merge_ok) {
+__device__ __forceinline__ void presort_resolve_block(const K* __restrict__ keys, int64_t n,
+                                                      const TileSummary* __restrict__ sums, int G, int64_t lmin,
+                                                      RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
+                                                      DevStats* __restrict__ st, int force, int merge_ok) {
   __shared__ int32_t s_incl[2][NT];
   __shared__ int64_t s_red64[NT / 32 + 1];
   __shared__ int32_t s_red[NT / 32 + 1];
@@ -194,8 +197,11 @@ __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ ke
   for (int c0 = 0; c0 < G; c0 += NT) {
     const int t = c0 + tid;
     TileSummary s;
-    if (t < G) s = sums[t];
-    else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; }
+    if (t < G) {
+      const int4* p = reinterpret_cast<const int4*>(sums + t);
+      int4 a = __ldcg(p), b = __ldcg(p + 1);
+      s.ndesc = a.x; s.nab = a.y; s.fdesc = a.z; s.ldesc = a.w; s.fab = b.x; s.lab = b.y; s.pad0 = 0; s.pad1 = 0;
+    } else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; }
     D += s.ndesc;
     A += s.nab;
     int32_t iD = block_inclusive_max<NT>(s.ldesc, s_red, -1);
@@ -276,6 +282,14 @@ __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ ke
     else route = kRoutePartition;
     st->route = route;
   }
+}
+
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ keys, int64_t n,
+                                                         const TileSummary* __restrict__ sums, int G, int64_t lmin,
+                                                         RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
+                                                         DevStats* __restrict__ st, int force, int merge_ok) {
+  presort_resolve_block<K, NT>(keys, n, sums, G, lmin, asc, desc, st, force, merge_ok);
 }
 
 // K3: in-place reversal of ranges [start, start+len) (H2; PAPER.md:93 and

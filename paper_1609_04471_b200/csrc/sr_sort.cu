@@ -23,6 +23,7 @@
 #include "merge.cuh"
 #include "partition.cuh"
 #include "presort.cuh"
+#include "resident.cuh"
 
 using namespace sr;
 
@@ -32,6 +33,8 @@ namespace {
 int g_force_route = 0;
 int g_profile = 0;
 int g_merge_route = 1;
+int g_resident = 1;
+int g_res_cap = kResCtaCap;
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -898,6 +901,194 @@ struct Sorter {
     c.launch("merge", bytes, [&] { kern<<<(unsigned)ctas, kMergeNT, smem, c.st>>>(pk, pv, wkk, wvv, d, nj, splits); });
   }
 
+  // ---- resident path: the whole keys-only sort as one cooperative launch (resident.cuh)
+  static int resident_grid() {  // CTAs of the cooperative launch (one per SM), 0 if it cannot run
+    static int grid[2] = {-1, -1};
+    int& g = grid[sizeof(K) == 8];
+    if (g < 0) {
+      g = 0;
+      int dev = 0, sms = 0, coop = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+      const size_t smem = sizeof(ResSmem<K>);
+      if (coop && cudaFuncSetAttribute(k_resident<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                      cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resident<K>, kResNT, smem) == cudaSuccess && per > 0)
+        g = sms;  // one CTA per SM: the phases are sized for it
+      cudaGetLastError();
+    }
+    return g;
+  }
+  bool resident_ok() const {
+    if (HAS_V || !g_resident || n <= kCap || n > kResMaxN) return false;
+    const int P = resident_grid();
+    return P >= 16;
+  }
+
+  void run_resident() {
+    c.plan.n = n;
+    const int64_t T = choose_tile(n);
+    const int64_t G = ceil_div<int64_t>(n, T);
+    const int P = resident_grid();
+    const int B = (int)std::min<int64_t>(ResCfg<K>::BMAX,
+                                         std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(n, kResTarget))));
+    const int S = B * kOversample;
+    if (S / std::min(S, kResSlice) > 16 || S / std::min(S, kResSlice) > P)
+      fail(SR_ERR_INTERNAL, "resident sample does not fit the slice layout");
+    {
+      auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+      c.reserve((size_t)(r(n * kw) + r(2 * n) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats)) + r(S * kw) +
+                         r(B * kw) + r(B) + r(4 * (2 * B + 1)) + r(16 * B) + 8 * 256));
+    }
+    ensure_ws();
+    ResArgs<K> a;
+    a.keys = keys;
+    a.ws = wk;
+    a.n = n;
+    a.tile = (int)T;
+    a.G = (int)G;
+    a.bins = c.alloc<uint16_t>(n);
+    a.sums = c.alloc<TileSummary>(G);
+    a.asc = c.alloc<RunDesc>(G + 1);
+    a.desc = c.alloc<RunDesc>(G + 1);
+    a.st = c.alloc<DevStats>(1);
+    a.sample = c.alloc<K>(S);
+    a.S = S;
+    a.B = B;
+    a.spl = c.alloc<K>(B);
+    a.eqf = c.alloc<uint8_t>(B);
+    a.tot = c.alloc<uint32_t>(2 * B + 1);
+    a.ovf = c.alloc<OvfSeg>(B);
+    a.lmin = T;
+    a.force = g_force_route;
+    a.merge_ok = g_merge_route;
+    static const bool stamps = getenv("SR_TIMING") != nullptr;
+    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P) : nullptr;
+    if (stamps) c.memset0(a.tstamp, 64 * (P + 1));
+    a.cta_cap = g_res_cap;
+    a.warp_cap = std::min(kResWarpCap, g_res_cap);
+    const size_t smem = sizeof(ResSmem<K>);
+    const int h = c.launch("resident", n * kw, [&] {
+      void* args[] = {&a};
+      check_cuda(cudaLaunchCooperativeKernel((void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
+    });
+    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(a.st, sizeof(DevStats)));
+    if (stamps) {
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 1)));
+      static const char* what[8] = {"A.scan", "A.end", "B.loaded", "B.end", "C.tree", "C.end", "D.end", "E.end"};
+      for (int k = 0; k < 8; k++) {
+        std::vector<double> v;
+        for (int q = 0; q < P; q++)
+          if (t[8 + 8 * q + k]) v.push_back((double)(t[8 + 8 * q + k] - t[0]) * 1e-3);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "[sr_resident]   %-9s since start: min %6.1f  med %6.1f  max %6.1f us  (%zu CTAs)\n", what[k], v[0],
+                v[v.size() / 2], v.back(), v.size());
+      }
+      fprintf(stderr, "[sr_resident] n=%lld route=%lld phase us: A %.1f B %.1f C %.1f D %.1f E %.1f (end %s)\n",
+              (long long)n, (long long)hs.route, (t[1] - t[0]) * 1e-3, t[2] ? (t[2] - t[1]) * 1e-3 : 0.0,
+              t[3] ? (t[3] - t[2]) * 1e-3 : 0.0, t[4] ? (t[4] - t[3]) * 1e-3 : 0.0,
+              t[5] ? (t[5] - t[4]) * 1e-3 : 0.0, t[5] ? "E" : "early");
+    }
+    if (getenv("SR_RES_DEBUG") && hs.route == kRoutePartition) {
+      std::vector<K> sp(B - 1), smp(S);
+      std::vector<uint8_t> eq(B - 1);
+      std::vector<uint32_t> tt(2 * B + 1);
+      cudaMemcpyAsync(sp.data(), a.spl, sizeof(K) * (B - 1), cudaMemcpyDeviceToHost, c.st);
+      cudaMemcpyAsync(eq.data(), a.eqf, B - 1, cudaMemcpyDeviceToHost, c.st);
+      cudaMemcpyAsync(smp.data(), a.sample, sizeof(K) * S, cudaMemcpyDeviceToHost, c.st);
+      cudaMemcpyAsync(tt.data(), a.tot, 4 * (2 * B + 1), cudaMemcpyDeviceToHost, c.st);
+      cudaStreamSynchronize(c.st);
+      int bad = 0, neq = 0, slices_bad = 0;
+      for (int j = 1; j < B - 1; j++) bad += sp[j] < sp[j - 1];
+      for (int j = 0; j < B - 1; j++) neq += eq[j];
+      const int SL = std::min(S, kResSlice);
+      for (int j = 0; j < S / SL; j++) {
+        int s0 = j * SL, s1 = s0 + SL;
+        for (int q = s0 + 1; q < s1; q++) if (smp[q] < smp[q - 1]) { slices_bad++; break; }
+      }
+      std::vector<K> all(smp);
+      std::sort(all.begin(), all.end());
+      int wrong = 0;
+      for (int j = 0; j < B - 1; j++) wrong += sp[j] != all[((int64_t)(j + 1) * S) / B];
+      uint32_t mx = 0;
+      for (auto v : tt) mx = std::max(mx, v);
+      fprintf(stderr, "[sr_res_debug] B=%d S=%d P=%d unsorted_spl=%d eq_flags=%d slices_unsorted=%d wrong_spl=%d max_bin=%u\n",
+              B, S, P, bad, neq, slices_bad, wrong, mx);
+    }
+    c.plan.descents = hs.descents;
+    c.plan.asc_breaks = hs.asc_breaks;
+    c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
+    if (hs.error) fail(SR_ERR_INTERNAL, "resident kernel inconsistency");
+    switch (hs.route) {
+      case kRouteSorted:
+        c.plan.route = SR_ROUTE_SORTED;
+        return;
+      case kRouteReversed:
+        c.plan.route = SR_ROUTE_REVERSED;
+        c.plan.desc_runs_reversed = 1;
+        c.replan(h, 3 * n * kw);
+        return;
+      case kRoutePartition: {
+        c.plan.route = SR_ROUTE_PARTITION;
+        c.plan.levels = 1;
+        c.plan.equal_keys += hs.eq_keys;
+        // scan + classify (read, bucket ids written) + scatter (keys + ids read,
+        // range keys written) + finishing (range keys read + written, fills written)
+        c.replan(h, n * kw + (n * kw + 2 * n) + (n * kw + 2 * n + hs.noneq_total * kw) +
+                        2 * (hs.noneq_total - hs.ovf_keys) * kw + hs.eq_keys * kw);
+        if (hs.n_ovf > 0) {
+          const OvfSeg* o = reinterpret_cast<const OvfSeg*>(c.readback(a.ovf, sizeof(OvfSeg) * hs.n_ovf));
+          std::vector<OvfSeg> next(o, o + hs.n_ovf);
+          run_levels(next, 1);
+        }
+        return;
+      }
+      default:
+        break;
+    }
+    // MERGE (forced) or undecided: the host planner compares the routes' bytes
+    c.replan(h, n * kw);
+    std::vector<RunDesc> asc, desc;
+    if (hs.n_asc_runs) {
+      const RunDesc* p = reinterpret_cast<const RunDesc*>(c.readback(a.asc, sizeof(RunDesc) * hs.n_asc_runs));
+      asc.assign(p, p + hs.n_asc_runs);
+    }
+    if (hs.n_desc_runs) {
+      const RunDesc* p = reinterpret_cast<const RunDesc*>(c.readback(a.desc, sizeof(RunDesc) * hs.n_desc_runs));
+      desc.assign(p, p + hs.n_desc_runs);
+    }
+    std::vector<Seg> segs = build_segments(asc, desc);
+    bool use_merge = hs.route == kRouteMerge;
+    if (!use_merge) {
+      const int64_t N = n * (kw + vw);
+      use_merge = merge_route_bytes(segs) < 4 * N + (n > 4 * 1024 * 1024 ? 3 * N : 0);
+    }
+    if (use_merge) {
+      c.plan.route = SR_ROUTE_MERGE;
+      run_merge_route(segs);
+      return;
+    }
+    c.plan.route = SR_ROUTE_PARTITION;
+    c.plan.levels = 1;
+    Level L1;
+    std::vector<OvfSeg> whole{{0, n}};
+    level_alloc(L1, whole, T, 0);
+    level_splitters(L1);
+    level_count(L1);
+    level_scan_plan(L1);
+    DevStats ls = *reinterpret_cast<DevStats*>(c.readback(L1.d_st, sizeof(DevStats)));
+    std::vector<OvfSeg> next;
+    if (ls.n_ovf > 0) {
+      const OvfSeg* o = reinterpret_cast<const OvfSeg*>(c.readback(L1.d_ovf, sizeof(OvfSeg) * ls.n_ovf));
+      next.assign(o, o + ls.n_ovf);
+    }
+    level_scatter(L1, &ls);
+    level_finish(L1, &ls);
+    run_levels(next, 1);
+  }
+
   // ---- top level
   // Everything up to the first statistics readback is enqueued without a host
   // round trip: the presortedness scan (fused with the level-1 histogram), the
@@ -906,6 +1097,10 @@ struct Sorter {
   // launches that return at once unless the device route selects them.
   void run() {
     c.plan.n = n;
+    if (resident_ok()) {
+      run_resident();
+      return;
+    }
     const int force = g_force_route;
     const int64_t T = choose_tile(n);
     const int64_t G = ceil_div<int64_t>(n, T);
@@ -1214,6 +1409,13 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       return SR_OK;
     case SR_OPT_MERGE_ROUTE:
       g_merge_route = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_RESIDENT:
+      g_resident = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_RESIDENT_CAP:
+      if (value < 1 || value > kResCtaCap) return SR_ERR_INVALID_ARGUMENT;
+      g_res_cap = (int)value;
       return SR_OK;
     default:
       return SR_ERR_INVALID_ARGUMENT;

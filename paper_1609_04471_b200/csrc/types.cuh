@@ -81,3 +81,4 @@ constexpr int kFillChunk = 8192;            // equality fills are split into ite
 constexpr int kTargetBucket = 1024;         // mean bucket size the planner aims for
 
 }  // namespace sr
+static_assert(sizeof(sr::TileSummary) == 32, "TileSummary is read as two int4");

@@ -1,0 +1,117 @@
+"""Parity of the resident path (-m gpu): keys-only sorts of 8192 < n <= 2^22
+run as ONE cooperative launch (resident.cuh), checked bit-exact against the
+CPU oracle, with the multi-kernel path as a second witness.
+
+The in-kernel finishing caps are lowered through SR_OPT_RESIDENT_CAP so that
+the CTA-finished buckets and the hand-off of oversized buckets to the host's
+next partition level (Appendix B recursion) are exercised
+on ordinary inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1609_04471_b200 as sr
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+ORDERS = ["random", "reversed", "nearly", "few_unique", "sorted", "all_equal", "organ_pipe", "extremes",
+          "runs1024", "last1pct", "sharp_teeth", "even_teeth", "equal_teeth", "distance256", "few100", "swaps_1e1"]
+SIZES = [8193, 12345, 65537, 300_007]
+RES_MAX = 1 << 22
+
+
+@pytest.fixture(autouse=True)
+def _reset():
+    yield
+    sr.set_option(sr.OPT_RESIDENT, 1)
+    sr.set_option(sr.OPT_RESIDENT_CAP, 4096)
+    sr.set_option(sr.OPT_FORCE_ROUTE, 0)
+
+
+def check(k, expect=None):
+    d = torch.from_numpy(k.copy()).cuda()
+    sr.sort_keys(d)
+    torch.cuda.synchronize()
+    e = oracle.sort_keys(k) if expect is None else expect
+    got = d.cpu().numpy()
+    assert np.array_equal(got, e), f"n={k.size}: first mismatch at {int(np.argmax(got != e))}"
+    return sr.last_plan()
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("order", ORDERS)
+def test_resident_parity(order, dtype):
+    for n in SIZES:
+        k = gen.make(order, n, dtype, config=8)
+        p = check(k)
+        one = p["route_name"] in ("sorted", "reversed") or (
+            p["route_name"] == "partition" and p["levels"] == 1 and p["long_runs"] == 0)
+        if one:
+            assert p["launches"] == 1, p  # the whole sort was the one cooperative launch
+
+
+@pytest.mark.parametrize("order", ["random", "nearly", "few_unique", "few100", "organ_pipe", "reversed"])
+def test_resident_c2_and_limits(order):
+    for n in [1_000_000, 2_000_000, RES_MAX, RES_MAX + 1]:
+        k = gen.make(order, n, np.int32, config=1)
+        p = check(k)
+        if n > RES_MAX:
+            assert p["launches"] > 1  # beyond the resident limit: multi-kernel path
+
+
+@pytest.mark.parametrize("cap", [1, 37, 300, 1024, 2000])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_resident_lowered_caps(cap, dtype):
+    """Buckets above the cap leave the kernel in the workspace and finish in the
+    host-driven next level; buckets in (min(cap, 1024), cap] are CTA-finished."""
+    sr.set_option(sr.OPT_RESIDENT_CAP, cap)
+    for order in ["random", "few100", "nearly", "organ_pipe"]:
+        for n in [9000, 200_003]:
+            k = gen.make(order, n, dtype, config=9)
+            p = check(k)
+            if order == "random" and cap <= 300:
+                assert p["levels"] >= 2, p
+
+
+def test_resident_matches_multikernel():
+    for order in ORDERS:
+        k = gen.make(order, 1 << 20, np.int32, config=10)
+        sr.set_option(sr.OPT_RESIDENT, 0)
+        a = torch.from_numpy(k.copy()).cuda()
+        sr.sort_keys(a)
+        pa = sr.last_plan()
+        sr.set_option(sr.OPT_RESIDENT, 1)
+        b = torch.from_numpy(k.copy()).cuda()
+        sr.sort_keys(b)
+        pb = sr.last_plan()
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), order
+        assert pa["route_name"] == pb["route_name"], (order, pa, pb)
+        assert pa["descents"] == pb["descents"] and pa["long_runs"] == pb["long_runs"], order
+
+
+def test_resident_forced_routes():
+    for route in [sr.ROUTE_MERGE, sr.ROUTE_PARTITION]:
+        sr.set_option(sr.OPT_FORCE_ROUTE, route)
+        for order in ["random", "reversed", "runs1024", "few_unique"]:
+            k = gen.make(order, 500_000, np.int32, config=11)
+            p = check(k)
+            if order != "reversed" or route == sr.ROUTE_MERGE:
+                assert p["route"] == route or p["route_name"] == "sorted", (order, p)
+
+
+def test_resident_stream_and_repeat():
+    """Back-to-back calls on a side stream (the workspace is stream-ordered)."""
+    s = torch.cuda.Stream()
+    ks = [gen.make("random", 1 << 20, np.int32, config=12, instance=i) for i in range(4)]
+    ds = [torch.from_numpy(k.copy()).cuda() for k in ks]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for d in ds:
+            sr.sort_keys(d)
+    s.synchronize()
+    for k, d in zip(ks, ds):
+        assert np.array_equal(d.cpu().numpy(), oracle.sort_keys(k))
