@@ -105,8 +105,9 @@ enum {
   SR_OPT_PROFILE = 1,     /* 1: time every kernel with CUDA events (see sr_last_profile) */
   SR_OPT_MERGE_ROUTE = 2, /* 0: never choose the merge route automatically */
   SR_OPT_RESIDENT = 3,    /* 0: never use the single-launch resident path (keys only, 8192 < n <= 2^22) */
-  SR_OPT_RESIDENT_CAP = 4 /* resident path: largest bucket finished in-kernel, 1..4096 (default 4096);
-                             larger buckets go to the next partition level (tests lower it) */
+  SR_OPT_RESIDENT_CAP = 4 /* resident path: largest level-1 bucket sorted in-kernel, 1..16384 (default and
+                             maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
+                             host-driven partition levels (tests lower it) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

@@ -58,10 +58,14 @@ __device__ __forceinline__ void classify_keys(const K (&x)[U], int (&bin)[U], co
 // Build the search structure from the m sorted splitters: tree[1..2^depth)
 // in level order (splitters padded with +inf to 2^depth - 1), the sorted
 // splitters at tree[kMaxBuckets..), flags eqf[0..m).  depth = tree_depth(m).
-__host__ __device__ __forceinline__ int tree_depth(int m) {
+__host__ __device__ __forceinline__ int tree_depth(int m) {  // smallest d >= 1 with 2^d - 1 >= m
+#ifdef __CUDA_ARCH__
+  return m <= 1 ? 1 : 32 - __clz(m);
+#else
   int d = 1;
   while ((1 << d) - 1 < m) d++;
   return d;
+#endif
 }
 template <typename K>
 __device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t* eqf, int m, K* s_tree,
@@ -183,14 +187,18 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
 // Block-level body of K2 (all NT threads of one CTA call it); also run by CTA 0
 // of the resident kernel (resident.cuh).  Cross-CTA inputs are read with
 // __ldcg so a caller that produced them in an earlier grid-sync phase sees them.
-template <typename K, int NT>
-__device__ __forceinline__ void presort_resolve_block(const K* __restrict__ keys, int64_t n,
+// Returns the device route to every thread; WRITE = false computes the route
+// only (the resident kernel's CTAs other than 0 resolve redundantly instead of
+// waiting for a grid barrier).
+template <typename K, int NT, bool WRITE = true>
+__device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ keys, int64_t n,
                                                       const TileSummary* __restrict__ sums, int G, int64_t lmin,
                                                       RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
                                                       DevStats* __restrict__ st, int force, int merge_ok) {
   __shared__ int32_t s_incl[2][NT];
   __shared__ int64_t s_red64[NT / 32 + 1];
   __shared__ int32_t s_red[NT / 32 + 1];
+  __shared__ int64_t s_route;
   const int tid = threadIdx.x;
   int32_t carryD = -1, carryA = -1;
   int64_t D = 0, A = 0, nasc = 0, ndsc = 0, covA = 0, covD = 0;
@@ -221,13 +229,13 @@ __device__ __forceinline__ void presort_resolve_block(const K* __restrict__ keys
     int32_t totA, totD;
     int32_t exA = block_exclusive_sum<NT>(fA, s_red, &totA);
     int32_t exD = block_exclusive_sum<NT>(fDd, s_red, &totD);
-    if (fA) {
+    if (WRITE && fA) {
       RunDesc r;
       r.start = prevD + 1; r.len = lenA;
       r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
       asc[nasc + exA] = r;
     }
-    if (fDd) {
+    if (WRITE && fDd) {
       RunDesc r;
       r.start = prevA + 1; r.len = lenDd;
       r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
@@ -249,27 +257,26 @@ __device__ __forceinline__ void presort_resolve_block(const K* __restrict__ keys
     // final runs after the last break
     int64_t lastLen = n - 1 - (int64_t)carryD;
     if (n > 0 && lastLen >= lmin) {
-      RunDesc r;
-      r.start = carryD + 1; r.len = lastLen;
-      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
-      asc[nasc++] = r;
+      if (WRITE) {
+        RunDesc r;
+        r.start = carryD + 1; r.len = lastLen;
+        r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+        asc[nasc] = r;
+      }
+      nasc++;
       covA += lastLen;
     }
     int64_t lastLenD = n - 1 - (int64_t)carryA;
     if (n > 0 && lastLenD >= lmin) {
-      RunDesc r;
-      r.start = carryA + 1; r.len = lastLenD;
-      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
-      desc[ndsc++] = r;
+      if (WRITE) {
+        RunDesc r;
+        r.start = carryA + 1; r.len = lastLenD;
+        r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+        desc[ndsc] = r;
+      }
+      ndsc++;
       covD += lastLenD;
     }
-    st->n = n;
-    st->descents = D;
-    st->asc_breaks = A;
-    st->n_asc_runs = nasc;
-    st->n_desc_runs = ndsc;
-    st->asc_cover = covA;
-    st->desc_cover = covD;
     // device-side route (H3 first stage); kRouteUndecided hands the merge-vs-
     // partition cost comparison to the host planner.
     int64_t route;
@@ -280,8 +287,22 @@ __device__ __forceinline__ void presort_resolve_block(const K* __restrict__ keys
     else if (force == kRoutePartition) route = kRoutePartition;
     else if (merge_ok && 2 * (covA + covD) >= n) route = kRouteUndecided;
     else route = kRoutePartition;
-    st->route = route;
+    if (WRITE) {
+      st->n = n;
+      st->descents = D;
+      st->asc_breaks = A;
+      st->n_asc_runs = nasc;
+      st->n_desc_runs = ndsc;
+      st->asc_cover = covA;
+      st->desc_cover = covD;
+      st->route = route;
+    }
+    s_route = route;
   }
+  __syncthreads();
+  const int64_t route = s_route;
+  __syncthreads();
+  return route;
 }
 
 template <typename K, int NT>

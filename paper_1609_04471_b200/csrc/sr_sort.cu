@@ -34,7 +34,7 @@ int g_force_route = 0;
 int g_profile = 0;
 int g_merge_route = 1;
 int g_resident = 1;
-int g_res_cap = kResCtaCap;
+int g_res_cap = 16384;
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -67,6 +67,14 @@ struct ThreadState {
   }
 };
 thread_local ThreadState t_state;
+thread_local std::chrono::steady_clock::time_point t_call0;
+void hostprof(const char* what) {  // SR_HOSTPROF: host time since the call began, per step
+  static const bool on = getenv("SR_HOSTPROF") != nullptr;
+  if (on)
+    fprintf(stderr, "[sr_host] %-12s %7.1f us\n", what,
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call0).count() * 1e6);
+}
+
 
 struct SrError {
   int32_t code;
@@ -914,14 +922,15 @@ struct Sorter {
       const size_t smem = sizeof(ResSmem<K>);
       if (coop && cudaFuncSetAttribute(k_resident<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
                       cudaSuccess &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resident<K>, kResNT, smem) == cudaSuccess && per > 0)
-        g = sms;  // one CTA per SM: the phases are sized for it
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resident<K>, kResNT, smem) == cudaSuccess &&
+          per >= kResCtasPerSM)
+        g = sms * kResCtasPerSM;  // the phases are sized for this many co-resident CTAs
       cudaGetLastError();
     }
     return g;
   }
   bool resident_ok() const {
-    if (HAS_V || !g_resident || n <= kCap || n > kResMaxN) return false;
+    if (HAS_V || !g_resident || n <= kCap || n > ResCfg<K>::MAXN) return false;
     const int P = resident_grid();
     return P >= 16;
   }
@@ -931,16 +940,20 @@ struct Sorter {
     const int64_t T = choose_tile(n);
     const int64_t G = ceil_div<int64_t>(n, T);
     const int P = resident_grid();
-    const int B = (int)std::min<int64_t>(ResCfg<K>::BMAX,
-                                         std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(n, kResTarget))));
-    const int S = B * kOversample;
-    if (S / std::min(S, kResSlice) > 16 || S / std::min(S, kResSlice) > P)
-      fail(SR_ERR_INTERNAL, "resident sample does not fit the slice layout");
+    if (T != kResTile) fail(SR_ERR_INTERNAL, "resident tile mismatch");
+    constexpr int CAPB = ResCfg<K>::CAPB;
+    const int B1 = (int)std::min<int64_t>(ResCfg<K>::B1MAX, std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(n, CAPB / 4))));
+    const int NG = (int)ceil_div<int64_t>(n, kResGrp);
+    const int S1 = B1 * kResO1;
+    const int nbins = 2 * B1 + 1;
+    const int64_t n_ovf = B1 + 1;
+    if (NG > kResMaxNG) fail(SR_ERR_INTERNAL, "resident group count");
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-      c.reserve((size_t)(r(n * kw) + r(2 * n) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats)) + r(S * kw) +
-                         r(B * kw) + r(B) + r(4 * (2 * B + 1)) + r(16 * B) + 8 * 256));
+      c.reserve((size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
+                         r(S1 * kw) + 2 * r(4 * (int64_t)NG * nbins) + r(16 * n_ovf) + 8 * 256));
     }
+    hostprof("reserved");
     ensure_ws();
     ResArgs<K> a;
     a.keys = keys;
@@ -948,74 +961,60 @@ struct Sorter {
     a.n = n;
     a.tile = (int)T;
     a.G = (int)G;
-    a.bins = c.alloc<uint16_t>(n);
     a.sums = c.alloc<TileSummary>(G);
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
-    a.st = c.alloc<DevStats>(1);
-    a.sample = c.alloc<K>(S);
-    a.S = S;
-    a.B = B;
-    a.spl = c.alloc<K>(B);
-    a.eqf = c.alloc<uint8_t>(B);
-    a.tot = c.alloc<uint32_t>(2 * B + 1);
-    a.ovf = c.alloc<OvfSeg>(B);
+    {  // control block: statistics + unit counter + bucket totals, zeroed together
+      const size_t bytes = sizeof(DevStats) + 16 + 4 * (size_t)nbins;
+      unsigned char* cb = c.alloc<unsigned char>((int64_t)bytes);
+      c.memset0(cb, bytes);
+      a.st = reinterpret_cast<DevStats*>(cb);
+      a.unit_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
+      a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 16);
+    }
+    a.S1 = S1;
+    a.B1 = B1;
+    a.samp = c.alloc<K>(S1);
+    a.NG = NG;
+    a.mcnt = c.alloc<uint32_t>((int64_t)NG * nbins);
+    a.mlst = c.alloc<uint32_t>((int64_t)NG * nbins);
+    a.ovf = c.alloc<OvfSeg>(n_ovf);
     a.lmin = T;
     a.force = g_force_route;
     a.merge_ok = g_merge_route;
+    a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
-    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P) : nullptr;
-    if (stamps) c.memset0(a.tstamp, 64 * (P + 1));
-    a.cta_cap = g_res_cap;
-    a.warp_cap = std::min(kResWarpCap, g_res_cap);
+    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P + 8) : nullptr;
+    if (stamps) c.memset0(a.tstamp, 64 * (P + 2));
     const size_t smem = sizeof(ResSmem<K>);
+    hostprof("prepared");
     const int h = c.launch("resident", n * kw, [&] {
       void* args[] = {&a};
       check_cuda(cudaLaunchCooperativeKernel((void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
+    hostprof("launched");
     DevStats hs = *reinterpret_cast<DevStats*>(c.readback(a.st, sizeof(DevStats)));
+    hostprof("read back");
     if (stamps) {
-      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 1)));
-      static const char* what[8] = {"A.scan", "A.end", "B.loaded", "B.end", "C.tree", "C.end", "D.end", "E.end"};
-      for (int k = 0; k < 8; k++) {
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 2)));
+      {
+        const unsigned long long* e = t + 8 + 8 * P;
+        fprintf(stderr, "[sr_resident] CTA0 %llu buckets, us: gather %.1f is_sorted+pad %.1f runs %.1f merges %.1f\n",
+                e[7], e[5] * 1e-3, e[0] * 1e-3, e[1] * 1e-3, e[2] * 1e-3);
+      }
+      static const char* what[8] = {"A.scan", "A.end", "C.route", "C.tree", "C.end", "E.start", "E.end", "-"};
+      for (int k = 0; k < 7; k++) {
         std::vector<double> v;
         for (int q = 0; q < P; q++)
           if (t[8 + 8 * q + k]) v.push_back((double)(t[8 + 8 * q + k] - t[0]) * 1e-3);
         if (v.empty()) continue;
         std::sort(v.begin(), v.end());
-        fprintf(stderr, "[sr_resident]   %-9s since start: min %6.1f  med %6.1f  max %6.1f us  (%zu CTAs)\n", what[k], v[0],
+        fprintf(stderr, "[sr_resident]   %-8s since start: min %6.1f  med %6.1f  max %6.1f us  (%zu CTAs)\n", what[k], v[0],
                 v[v.size() / 2], v.back(), v.size());
       }
-      fprintf(stderr, "[sr_resident] n=%lld route=%lld phase us: A %.1f B %.1f C %.1f D %.1f E %.1f (end %s)\n",
-              (long long)n, (long long)hs.route, (t[1] - t[0]) * 1e-3, t[2] ? (t[2] - t[1]) * 1e-3 : 0.0,
-              t[3] ? (t[3] - t[2]) * 1e-3 : 0.0, t[4] ? (t[4] - t[3]) * 1e-3 : 0.0,
-              t[5] ? (t[5] - t[4]) * 1e-3 : 0.0, t[5] ? "E" : "early");
-    }
-    if (getenv("SR_RES_DEBUG") && hs.route == kRoutePartition) {
-      std::vector<K> sp(B - 1), smp(S);
-      std::vector<uint8_t> eq(B - 1);
-      std::vector<uint32_t> tt(2 * B + 1);
-      cudaMemcpyAsync(sp.data(), a.spl, sizeof(K) * (B - 1), cudaMemcpyDeviceToHost, c.st);
-      cudaMemcpyAsync(eq.data(), a.eqf, B - 1, cudaMemcpyDeviceToHost, c.st);
-      cudaMemcpyAsync(smp.data(), a.sample, sizeof(K) * S, cudaMemcpyDeviceToHost, c.st);
-      cudaMemcpyAsync(tt.data(), a.tot, 4 * (2 * B + 1), cudaMemcpyDeviceToHost, c.st);
-      cudaStreamSynchronize(c.st);
-      int bad = 0, neq = 0, slices_bad = 0;
-      for (int j = 1; j < B - 1; j++) bad += sp[j] < sp[j - 1];
-      for (int j = 0; j < B - 1; j++) neq += eq[j];
-      const int SL = std::min(S, kResSlice);
-      for (int j = 0; j < S / SL; j++) {
-        int s0 = j * SL, s1 = s0 + SL;
-        for (int q = s0 + 1; q < s1; q++) if (smp[q] < smp[q - 1]) { slices_bad++; break; }
-      }
-      std::vector<K> all(smp);
-      std::sort(all.begin(), all.end());
-      int wrong = 0;
-      for (int j = 0; j < B - 1; j++) wrong += sp[j] != all[((int64_t)(j + 1) * S) / B];
-      uint32_t mx = 0;
-      for (auto v : tt) mx = std::max(mx, v);
-      fprintf(stderr, "[sr_res_debug] B=%d S=%d P=%d unsorted_spl=%d eq_flags=%d slices_unsorted=%d wrong_spl=%d max_bin=%u\n",
-              B, S, P, bad, neq, slices_bad, wrong, mx);
+      fprintf(stderr, "[sr_resident] n=%lld B1=%d route=%lld phases us: A %.1f C %.1f E %.1f\n", (long long)n, B1,
+              (long long)hs.route, (t[1] - t[0]) * 1e-3, t[2] ? (t[2] - t[1]) * 1e-3 : 0.0,
+              t[3] ? (t[3] - t[2]) * 1e-3 : 0.0);
     }
     c.plan.descents = hs.descents;
     c.plan.asc_breaks = hs.asc_breaks;
@@ -1032,16 +1031,16 @@ struct Sorter {
         return;
       case kRoutePartition: {
         c.plan.route = SR_ROUTE_PARTITION;
-        c.plan.levels = 1;
+        c.plan.levels = 2;  // the global level and the in-CTA level
         c.plan.equal_keys += hs.eq_keys;
         // scan + classify (read, bucket ids written) + scatter (keys + ids read,
-        // range keys written) + finishing (range keys read + written, fills written)
+        // range keys written) + bucket sorts (range keys read + written, fills written)
         c.replan(h, n * kw + (n * kw + 2 * n) + (n * kw + 2 * n + hs.noneq_total * kw) +
                         2 * (hs.noneq_total - hs.ovf_keys) * kw + hs.eq_keys * kw);
-        if (hs.n_ovf > 0) {
+        if (hs.n_ovf > 0) {  // ranges left unsorted in keys (beyond the in-kernel caps): further levels
           const OvfSeg* o = reinterpret_cast<const OvfSeg*>(c.readback(a.ovf, sizeof(OvfSeg) * hs.n_ovf));
           std::vector<OvfSeg> next(o, o + hs.n_ovf);
-          run_levels(next, 1);
+          run_levels(next, 0);
         }
         return;
       }
@@ -1311,7 +1310,9 @@ int32_t guarded(F&& f) {
 }
 
 int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream, bool pairs) {
+  t_call0 = std::chrono::steady_clock::now();
   int32_t v = validate(keys, vals, n, dtype, pairs);
+  hostprof("validated");
   if (v != SR_OK) {
     t_state.err = sr_status_string(v);
     return v;
@@ -1414,7 +1415,7 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       g_resident = value ? 1 : 0;
       return SR_OK;
     case SR_OPT_RESIDENT_CAP:
-      if (value < 1 || value > kResCtaCap) return SR_ERR_INVALID_ARGUMENT;
+      if (value < 1 || value > 16384) return SR_ERR_INVALID_ARGUMENT;
       g_res_cap = (int)value;
       return SR_OK;
     default:
