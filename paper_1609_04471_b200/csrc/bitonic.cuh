@@ -160,11 +160,12 @@ struct WarpBitonic {
     while (nl < need) nl <<= 1;
     K k[VT];
     __syncwarp();
+    // blocked 16-byte vector loads: a scalar load of ks[lane * VT + i] would
+    // put all 32 lanes on one shared-memory bank for VT a multiple of 32 words
+    BlockSort<K, false, 32, VT>::load_vec(ks + lane * VT, k);
 #pragma unroll
-    for (int i = 0; i < VT; i++) {
-      int p = lane * VT + i;
-      k[i] = p < count ? ks[p] : KeyTraits<K>::max_key();
-    }
+    for (int i = 0; i < VT; i++)
+      if (lane * VT + i >= count) k[i] = KeyTraits<K>::max_key();
     batcher_network<VT>([&](int a, int b) {
       K x = k[a], y = k[b];
       k[a] = BT::kmin(x, y);

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
                                               int buf, Item* __restrict__ items, Item* __restrict__ items_big,
                                               OvfSeg* __restrict__ ovf, DevStats* __restrict__ st,
                                               const uint32_t* __restrict__ tot, uint32_t* __restrict__ cursor,
-                                              const DevStats* __restrict__ gate, int small_max) {
+                                              const DevStats* __restrict__ gate, int small_max, int pack_h) {
   if (gate && gate->route != kRoutePartition) return;  // speculative launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlanSmem& sm = *reinterpret_cast<PlanSmem*>(smem_raw);
@@ -397,7 +397,9 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
   const int nb = seg.nbins;
   const int G = seg.nchunks;
   const int64_t send = seg.start + seg.len;
-  const int H = small_max / 2;  // packing window: chunks of packed buckets stay < small_max
+  // packing window: buckets <= H are packed with their neighbours into items < 2H
+  // (adjacent buckets are ordered); larger buckets are items of their own
+  const int H = pack_h;
   if (tot) {
     // keys only: bucket starts = seg.start + exclusive scan of the totals
     for (int b = threadIdx.x; b < nb; b += NT) sm.p[b] = (int32_t)tot[seg.mat_base + b];
@@ -773,7 +775,13 @@ __global__ void __launch_bounds__(32 * WARPS) k_finish_warp(const Item* __restri
     int unsorted = 0;
     for (int i = lane; i + 1 < len; i += 32) unsorted |= ks[i + 1] < ks[i];
     unsorted = __any_sync(0xffffffffu, unsorted);
-    if (unsorted) WB::sort(ks, len);
+    if (unsorted) {  // the narrowest register network that holds the item
+      if (VT >= 4 && len <= 128) WarpBitonic<K, 4>::sort(ks, len);
+      else if (VT >= 8 && len <= 256) WarpBitonic<K, (VT >= 8 ? 8 : VT)>::sort(ks, len);
+      else if (VT >= 16 && len <= 512) WarpBitonic<K, (VT >= 16 ? 16 : VT)>::sort(ks, len);
+      else if (VT >= 32 && len <= 1024) WarpBitonic<K, (VT >= 32 ? 32 : VT)>::sort(ks, len);
+      else WB::sort(ks, len);
+    }
     if (unsorted || from_ws) {
       __syncwarp();
       for (int i = lane; i < len; i += 32) dk[i] = ks[i];

@@ -278,6 +278,7 @@ constexpr int kScanNT = 256, kScanIPT = 16;              // K9
 constexpr int kFinNT = 256, kFinVT = 16;                 // K11 big items (two halves of 4096 = kCap)
 constexpr int kFinSmallNT = 128;                         // K11 small items (pairs, <= 2048 = kSmallItem)
 constexpr int kWarpItemsPerCta = 4;                      // K11w (keys only): warps per CTA
+constexpr int kPackKeys = 128;                           // keys only: buckets <= this are packed into items
 constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
 constexpr int kScatKNT = 1024, kScatKVT = 8;             // K10 (keys only)
 constexpr int kScanNT1 = 1024;                           // K1
@@ -296,7 +297,7 @@ int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
 // Buckets per segment: mean bucket ~kTargetBucket at level 1, ~kTargetBucket/2
 // below (those buckets are finished by one warp with 32 keys per lane).
 int choose_buckets(int64_t len, int level = 1) {
-  int64_t b = pow2ceil(ceil_div<int64_t>(len, level > 1 ? kTargetBucket / 2 : kTargetBucket));
+  int64_t b = pow2ceil(ceil_div<int64_t>(len, level > 1 ? kTargetBucket / 4 : kTargetBucket));
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
@@ -558,7 +559,8 @@ struct Sorter {
     set_smem(kern, sizeof(PlanSmem));
     c.launch("plan", L.total_bins * 8, [&] {
       kern<<<S, 1024, sizeof(PlanSmem), c.st>>>(L.d_segs, L.d_mat, L.d_spl, L.d_m, dst, L.d_items, L.d_items_big,
-                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate, L.small_max);
+                                                L.d_ovf, L.d_st, L.d_tot, L.d_cursor, gate, L.small_max,
+                                                HAS_V ? L.small_max / 2 : kPackKeys);
     });
   }
 
