@@ -128,7 +128,7 @@ class ClockSampler:
 NCU_NAMES = {"presort_scan": "k_presort_scan", "presort_resolve": "k_presort_resolve", "reverse": "k_reverse",
              "sample_rank": "k_sample_rank", "select_splitters": "k_select_splitters", "count": "k_count",
              "plan": "k_plan", "scatter": "k_scatter", "finish_small": "k_finish_warp", "finish": "k_finish<",
-             "merge": "k_merge<", "scan": "k_scan_u32"}
+             "merge": "k_merge<", "scan": "k_scan_u32", "resident": "k_resident"}
 
 
 def ncu_traffic(kernel: str, dtype_name: str):

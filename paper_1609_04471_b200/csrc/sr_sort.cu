@@ -1035,10 +1035,11 @@ struct Sorter {
         c.plan.route = SR_ROUTE_PARTITION;
         c.plan.levels = 2;  // the global level and the in-CTA level
         c.plan.equal_keys += hs.eq_keys;
-        // scan + classify (read, bucket ids written) + scatter (keys + ids read,
-        // range keys written) + bucket sorts (range keys read + written, fills written)
-        c.replan(h, n * kw + (n * kw + 2 * n) + (n * kw + 2 * n + hs.noneq_total * kw) +
-                        2 * (hs.noneq_total - hs.ovf_keys) * kw + hs.eq_keys * kw);
+        // scan (read) + grouping (read, written to the workspace by tile, bucket
+        // tables written) + bucket sorts (range keys gathered and written, tables
+        // read) + equality fills (written)
+        c.replan(h, n * kw + 2 * n * kw + 2 * hs.noneq_total * kw + hs.eq_keys * kw +
+                        2 * 2 * 4 * (int64_t)NG * nbins);
         if (hs.n_ovf > 0) {  // ranges left unsorted in keys (beyond the in-kernel caps): further levels
           const OvfSeg* o = reinterpret_cast<const OvfSeg*>(c.readback(a.ovf, sizeof(OvfSeg) * hs.n_ovf));
           std::vector<OvfSeg> next(o, o + hs.n_ovf);
