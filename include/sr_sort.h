@@ -50,7 +50,9 @@ enum {
   SR_ROUTE_REVERSED = 2,  /* one descending run: reversal only */
   SR_ROUTE_MERGE = 3,     /* natural runs + merge levels (§3, Appendix A) */
   SR_ROUTE_PARTITION = 4, /* splitter partition with equality buckets (§4, Appendix B) */
-  SR_ROUTE_TILE = 5       /* n <= one CTA tile: tile sort only (PAPER.md:155 alpha cutoff) */
+  SR_ROUTE_TILE = 5,      /* n <= one CTA tile: tile sort only (PAPER.md:155 alpha cutoff) */
+  SR_ROUTE_OUTLIER = 6    /* keys only, few descents (k-exchange): descent endpoints extracted,
+                             sorted, merged with the sorted remainder */
 };
 
 /* ------------------------------------------------------------------ sort */
@@ -101,13 +103,15 @@ const char *sr_status_string(int32_t status);
 const char *sr_last_error(void); /* thread-local; "" when none */
 
 enum {
-  SR_OPT_FORCE_ROUTE = 0, /* 0 auto, SR_ROUTE_MERGE or SR_ROUTE_PARTITION (tests, ablations) */
+  SR_OPT_FORCE_ROUTE = 0, /* 0 auto, SR_ROUTE_MERGE, SR_ROUTE_PARTITION or SR_ROUTE_OUTLIER (keys only)
+                             (tests, ablations) */
   SR_OPT_PROFILE = 1,     /* 1: time every kernel with CUDA events (see sr_last_profile) */
   SR_OPT_MERGE_ROUTE = 2, /* 0: never choose the merge route automatically */
   SR_OPT_RESIDENT = 3,    /* 0: never use the single-launch resident path (keys only, 8192 < n <= 2^22) */
-  SR_OPT_RESIDENT_CAP = 4 /* resident path: largest level-1 bucket sorted in-kernel, 1..16384 (default and
-                             maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
-                             host-driven partition levels (tests lower it) */
+  SR_OPT_RESIDENT_CAP = 4, /* resident path: largest level-1 bucket sorted in-kernel, 1..16384 (default and
+                              maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
+                              host-driven partition levels (tests lower it) */
+  SR_OPT_OUTLIER_ROUTE = 5 /* 0: never choose the outlier route automatically */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

@@ -99,6 +99,19 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, int bin, bool valid) {
   if (valid) atomicAdd(&hist[bin], 1u);
 }
 
+// Descent at i (a[i] > a[i+1]) whose outer neighbours are out of order,
+// a[i-1] > a[i+2]: removing the descent's two endpoints would not leave the
+// neighbourhood sorted.  Counted for the outlier route's choice (isolated
+// exchanges, have none; shuffled runs or a random tail have many).
+// pv / n2 are the warp's a[i-1] / a[i+2] (lane 0 and lanes 30-31 reload).
+template <typename K>
+__device__ __forceinline__ int straddle_violation(const K* __restrict__ keys, int64_t n, int64_t i, int lane, K pv, K n2) {
+  if (i < 1 || i + 2 >= n) return 0;
+  const K a0 = lane == 0 ? keys[i - 1] : pv;
+  const K a3 = lane >= 30 ? keys[i + 2] : n2;
+  return a0 > a3 ? 1 : 0;
+}
+
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
 // break rule: a_i <= a_{i+1} (pairs: only strictly descending runs may be
 // reversed, "the reversely sorted subsequence cannot contain equal
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
     for (int b = tid; b < nbins; b += NT) s_hist[b] = 0;
     __syncthreads();
   }
-  int cd = 0, ca = 0;
+  int cd = 0, ca = 0, cv = 0;
   int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
   for (int64_t base = t0; base < t1; base += NT * U) {
     K x[U];
@@ -142,9 +155,13 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
     for (int u = 0; u < U; u++) {
       int64_t i = base + u * NT + tid;
       K y = __shfl_down_sync(0xffffffffu, x[u], 1);
+      const K pv = __shfl_up_sync(0xffffffffu, x[u], 1), n2 = __shfl_down_sync(0xffffffffu, x[u], 2);
       if (lane == 31 && i + 1 < n) y = keys[i + 1];
       if (i < t1 && i + 1 < n) {
-        if (y < x[u]) { cd++; fd = min(fd, (int)i); ld = max(ld, (int)i); }
+        if (y < x[u]) {
+          cd++; fd = min(fd, (int)i); ld = max(ld, (int)i);
+          cv += straddle_violation<K>(keys, n, i, lane, pv, n2);
+        }
         bool brk = STRICT ? !(y < x[u]) : (x[u] < y);
         if (brk) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }
       }
@@ -166,9 +183,10 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   ld = block_reduce_max<NT>(ld, s_red);
   fa = block_reduce_min<NT>(fa, s_red);
   la = block_reduce_max<NT>(la, s_red);
+  cv = block_reduce_sum<NT>(cv, s_red);
   if (tid == 0) {
     TileSummary s;
-    s.ndesc = cd; s.nab = ca; s.fdesc = fd; s.ldesc = ld; s.fab = fa; s.lab = la; s.pad0 = 0; s.pad1 = 0;
+    s.ndesc = cd; s.nab = ca; s.fdesc = fd; s.ldesc = ld; s.fab = fa; s.lab = la; s.nviol = cv; s.pad1 = 0;
     sums[blockIdx.x] = s;
   }
   if (FUSE) {
@@ -201,17 +219,18 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
   __shared__ int64_t s_route;
   const int tid = threadIdx.x;
   int32_t carryD = -1, carryA = -1;
-  int64_t D = 0, A = 0, nasc = 0, ndsc = 0, covA = 0, covD = 0;
+  int64_t D = 0, A = 0, V = 0, nasc = 0, ndsc = 0, covA = 0, covD = 0;
   for (int c0 = 0; c0 < G; c0 += NT) {
     const int t = c0 + tid;
     TileSummary s;
     if (t < G) {
       const int4* p = reinterpret_cast<const int4*>(sums + t);
       int4 a = __ldcg(p), b = __ldcg(p + 1);
-      s.ndesc = a.x; s.nab = a.y; s.fdesc = a.z; s.ldesc = a.w; s.fab = b.x; s.lab = b.y; s.pad0 = 0; s.pad1 = 0;
-    } else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; }
+      s.ndesc = a.x; s.nab = a.y; s.fdesc = a.z; s.ldesc = a.w; s.fab = b.x; s.lab = b.y; s.nviol = b.z; s.pad1 = 0;
+    } else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; s.nviol = 0; }
     D += s.ndesc;
     A += s.nab;
+    V += s.nviol;
     int32_t iD = block_inclusive_max<NT>(s.ldesc, s_red, -1);
     int32_t iA = block_inclusive_max<NT>(s.lab, s_red, -1);
     s_incl[0][tid] = iD;
@@ -251,6 +270,7 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
   }
   D = block_reduce_sum<NT>(D, s_red64);
   A = block_reduce_sum<NT>(A, s_red64);
+  V = block_reduce_sum<NT>(V, s_red64);
   covA = block_reduce_sum<NT>(covA, s_red64);
   covD = block_reduce_sum<NT>(covD, s_red64);
   if (tid == 0) {
@@ -285,7 +305,12 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
     else if (force == kRouteMerge) route = kRouteMerge;
     else if (n <= kCap) route = kRouteTile;
     else if (force == kRoutePartition) route = kRoutePartition;
-    else if (merge_ok && 2 * (covA + covD) >= n) route = kRouteUndecided;
+    else if (force == kRouteOutlier) route = kRouteOutlier;
+    // few, isolated descents (k-exchange-like): extract the outliers
+    else if ((merge_ok & kAllowOutlier) && A > 0 && kViolRatio * V <= D &&
+             ((merge_ok & kOutlierStrict) ? kOutlierRatioStrict : kOutlierRatio) * D <= n)
+      route = kRouteOutlier;
+    else if ((merge_ok & kAllowMerge) && 2 * (covA + covD) >= n) route = kRouteUndecided;
     else route = kRoutePartition;
     if (WRITE) {
       st->n = n;

@@ -135,7 +135,7 @@ struct ResSmem {
   } u;
   int32_t red[kResNT / 32 + 1];
   int64_t red64[kResNT / 32 + 1];
-  int32_t agg[kResWarps][6];
+  int32_t agg[kResWarps][7];
 };
 
 // Level-order (Eytzinger) part of a splitter tree whose sorted copy is at tree[BMAX + i].
@@ -281,17 +281,30 @@ __device__ void res_bucket_sort(K* __restrict__ dst, int L, typename ResSmem<K>:
       const K* A = src + p0;
       const K* B = A + alen;
       const int diag = o - p0;
-      int i = merge_path_search<K>([&](int q) { return A[q]; }, alen, [&](int q) { return B[q]; }, blen, diag);
-      int j = diag - i;
-      K av = i < alen ? A[i] : KeyTraits<K>::max_key();
-      K bv = j < blen ? B[j] : KeyTraits<K>::max_key();
-      K res[VT];
+      const int i = merge_path_search<K>([&](int q) { return A[q]; }, alen, [&](int q) { return B[q]; }, blen, diag);
+      const int j = diag - i;
+      // the VT outputs are the VT smallest of A[i, i+VT) and B[j, j+VT): all
+      // loads issued together, then a half-cleaner against the reversed B
+      // window (a bitonic sequence of the VT smallest) and a bitonic merge in
+      // registers -- no dependent load chain (equal keys are interchangeable)
+      K res[VT], bw[VT];
 #pragma unroll
       for (int k = 0; k < VT; k++) {
-        const bool takeA = j >= blen || (i < alen && !(bv < av));
-        res[k] = takeA ? av : bv;
-        if (takeA) { i++; av = i < alen ? A[i] : KeyTraits<K>::max_key(); }
-        else { j++; bv = j < blen ? B[j] : KeyTraits<K>::max_key(); }
+        res[k] = i + k < alen ? A[i + k] : KeyTraits<K>::max_key();
+        bw[k] = j + k < blen ? B[j + k] : KeyTraits<K>::max_key();
+      }
+#pragma unroll
+      for (int k = 0; k < VT; k++) res[k] = min(res[k], bw[VT - 1 - k]);
+#pragma unroll
+      for (int h = VT / 2; h > 0; h >>= 1) {
+#pragma unroll
+        for (int k = 0; k < VT; k++) {
+          if ((k & h) == 0) {
+            const K x = res[k], y = res[k | h];
+            res[k] = min(x, y);
+            res[k | h] = max(x, y);
+          }
+        }
       }
       if (last) {
 #pragma unroll
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   for (int t = c; t < a.G; t += P) {
     const int64_t t0 = (int64_t)t * a.tile;
     const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
-    int cd = 0, ca = 0;
+    int cd = 0, ca = 0, cv = 0;
     int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
     for (int64_t base = t0; base < t1; base += NT * UA) {
       K x[UA], nx[UA];
@@ -363,9 +376,13 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       for (int u = 0; u < UA; u++) {
         const int64_t i = base + u * NT + tid;
         K y = __shfl_down_sync(0xffffffffu, x[u], 1);
+        const K pv = __shfl_up_sync(0xffffffffu, x[u], 1), n2 = __shfl_down_sync(0xffffffffu, x[u], 2);
         if (lane == 31) y = nx[u];
         if (i < t1 && i + 1 < n) {
-          if (y < x[u]) { cd++; fd = min(fd, (int)i); ld = max(ld, (int)i); }
+          if (y < x[u]) {
+            cd++; fd = min(fd, (int)i); ld = max(ld, (int)i);
+            cv += straddle_violation<K>(a.keys, n, i, lane, pv, n2);
+          }
           if (x[u] < y) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }  // keys only: non-increasing runs
         }
       }
@@ -378,18 +395,21 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       ld = max(ld, __shfl_xor_sync(0xffffffffu, ld, o));
       fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
       la = max(la, __shfl_xor_sync(0xffffffffu, la, o));
+      cv += __shfl_xor_sync(0xffffffffu, cv, o);
     }
     if (lane == 0) {
       sm.agg[w][0] = cd; sm.agg[w][1] = ca; sm.agg[w][2] = fd; sm.agg[w][3] = ld; sm.agg[w][4] = fa; sm.agg[w][5] = la;
+      sm.agg[w][6] = cv;
     }
     __syncthreads();
     if (tid == 0) {
       for (int v = 1; v < kResWarps; v++) {
         cd += sm.agg[v][0]; ca += sm.agg[v][1];
         fd = min(fd, sm.agg[v][2]); ld = max(ld, sm.agg[v][3]); fa = min(fa, sm.agg[v][4]); la = max(la, sm.agg[v][5]);
+        cv += sm.agg[v][6];
       }
       TileSummary ts;
-      ts.ndesc = cd; ts.nab = ca; ts.fdesc = fd; ts.ldesc = ld; ts.fab = fa; ts.lab = la; ts.pad0 = 0; ts.pad1 = 0;
+      ts.ndesc = cd; ts.nab = ca; ts.fdesc = fd; ts.ldesc = ld; ts.fab = fa; ts.lab = la; ts.nviol = cv; ts.pad1 = 0;
       a.sums[t] = ts;
     }
     __syncthreads();

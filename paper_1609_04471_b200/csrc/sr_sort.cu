@@ -21,6 +21,7 @@
 
 #include "../../include/sr_sort.h"
 #include "merge.cuh"
+#include "outlier.cuh"
 #include "partition.cuh"
 #include "presort.cuh"
 #include "resident.cuh"
@@ -34,6 +35,7 @@ int g_force_route = 0;
 int g_profile = 0;
 int g_merge_route = 1;
 int g_resident = 1;
+int g_outlier = 1;
 int g_res_cap = 16384;
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
@@ -314,7 +316,17 @@ struct Sorter {
   static constexpr int64_t kw = sizeof(K);
   static constexpr int64_t vw = HAS_V ? 4 : 0;
 
+  bool nested = false;  // sorting the outliers of an outlier route (no second outlier route)
   Sorter(Ctx& ctx, K* k, uint32_t* v, int64_t nn) : c(ctx), keys(k), vals(v), n(nn) {}
+
+  // routes the device resolve may choose, and the forced route (outlier: keys only)
+  int route_ok() const {
+    return (g_merge_route ? kAllowMerge : 0) | ((!HAS_V && g_outlier && !nested) ? kAllowOutlier : 0);
+  }
+  int forced() const {
+    if (g_force_route == SR_ROUTE_OUTLIER && (HAS_V || nested)) return 0;
+    return g_force_route;
+  }
 
   void ensure_ws() {
     if (!wk) {
@@ -933,6 +945,7 @@ struct Sorter {
   }
   bool resident_ok() const {
     if (HAS_V || !g_resident || n <= kCap || n > ResCfg<K>::MAXN) return false;
+    if (g_force_route == SR_ROUTE_MERGE && !nested) return false;  // forced merge: the multi-kernel planner
     const int P = resident_grid();
     return P >= 16;
   }
@@ -982,8 +995,10 @@ struct Sorter {
     a.mlst = c.alloc<uint32_t>((int64_t)NG * nbins);
     a.ovf = c.alloc<OvfSeg>(n_ovf);
     a.lmin = T;
-    a.force = g_force_route;
-    a.merge_ok = g_merge_route;
+    a.force = forced();
+    // the one-launch partition beats the host-driven outlier rounds at this size
+    // unless the outliers are very few
+    a.merge_ok = route_ok() | kOutlierStrict;
     a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
     a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P + 8) : nullptr;
@@ -1050,8 +1065,14 @@ struct Sorter {
       default:
         break;
     }
-    // MERGE (forced) or undecided: the host planner compares the routes' bytes
     c.replan(h, n * kw);
+    if (hs.route == kRouteOutlier) {
+      c.plan.route = SR_ROUTE_OUTLIER;
+      if (run_outlier()) return;
+      partition_host(T);  // not a few-outlier input: keys hold a permutation
+      return;
+    }
+    // MERGE (forced) or undecided: the host planner compares the routes' bytes
     std::vector<RunDesc> asc, desc;
     if (hs.n_asc_runs) {
       const RunDesc* p = reinterpret_cast<const RunDesc*>(c.readback(a.asc, sizeof(RunDesc) * hs.n_asc_runs));
@@ -1072,6 +1093,112 @@ struct Sorter {
       run_merge_route(segs);
       return;
     }
+    partition_host(T);
+  }
+
+  // ---- outlier route (outlier.cuh): few descents, keys only.  One round
+  // compacts src[0, m) into dst: kept keys [0, r), outliers [r, m); returns r
+  // and the number of descents among the kept keys.
+  std::pair<int64_t, int64_t> outlier_round(const K* src, int64_t m, K* dst) {
+    constexpr int T = OutTile<K>::T;
+    const int64_t G = ceil_div<int64_t>(m, T);
+    uint32_t* cnt = c.alloc<uint32_t>(G + 1);
+    K* fl = c.alloc<K>(2 * G);
+    uint8_t* has = c.alloc<uint8_t>(G);
+    const int64_t tiles = ceil_div<int64_t>(G + 1, kScanNT * kScanIPT);
+    unsigned char* ctrl = c.alloc<unsigned char>(64 + 8 * tiles + 256);
+    c.memset0(ctrl, 64 + 8 * tiles + 256);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctrl);
+    int* tile_counter = reinterpret_cast<int*>(ctrl + 8);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ctrl + 64);
+    c.memset0(cnt + G, 4);
+    c.launch("outlier_count", m * kw, [&] {
+      k_outlier_count<K, kOutNT><<<(unsigned)G, kOutNT, 0, c.st>>>(src, m, cnt);
+    });
+    c.launch("scan", (G + 1) * 8, [&] {
+      k_scan_u32<kScanNT, kScanIPT><<<(unsigned)tiles, kScanNT, 0, c.st>>>(cnt, G + 1, status, tile_counter, nullptr);
+    });
+    c.launch("outlier_split", 2 * m * kw, [&] {
+      k_outlier_split<K, kOutNT><<<(unsigned)G, kOutNT, 0, c.st>>>(src, m, cnt, (int)G, dst, fl, has, bad);
+    });
+    c.launch("outlier_check", 0, [&] {
+      k_outlier_check<K><<<(unsigned)ceil_div<int64_t>(G, 256), 256, 0, c.st>>>(fl, has, (int)G, bad);
+    });
+    // r = cnt[G] and the descent count, in one readback (both live in device memory)
+    uint32_t* pair = c.alloc<uint32_t>(4);
+    check_cuda(cudaMemcpyAsync(pair, cnt + G, 4, cudaMemcpyDeviceToDevice, c.st), "outlier r");
+    check_cuda(cudaMemcpyAsync(pair + 2, bad, 8, cudaMemcpyDeviceToDevice, c.st), "outlier bad");
+    const uint32_t* h = reinterpret_cast<const uint32_t*>(c.readback(pair, 16));
+    const int64_t r = h[0];
+    const int64_t nb = (int64_t)h[2] | ((int64_t)h[3] << 32);
+    return {r, nb};
+  }
+
+  // sort dst[0, m) by the ordinary routes (the outliers), keeping this call's plan
+  void sort_nested(K* p, int64_t m) {
+    if (m <= 1) return;
+    sr_plan saved = c.plan;
+    Sorter<K, HAS_V> sub(c, p, nullptr, m);
+    sub.nested = true;
+    sub.run();
+    const int64_t launches = c.plan.launches, bytes = c.plan.bytes_planned, syncs = c.plan.host_syncs;
+    c.plan = saved;
+    c.plan.launches = launches;
+    c.plan.bytes_planned = bytes;
+    c.plan.host_syncs = syncs;
+  }
+
+  void merge_two(int buf, int64_t la, int64_t lb) {  // merge buf[0, la) with buf[la, la+lb) into the other buffer
+    std::vector<MergeJob> jobs{MergeJob{0, la, lb, 0, buf, 0}};
+    run_merges(jobs, ceil_div<int64_t>(la + lb, kMergeNV), 2 * (la + lb) * kw);
+  }
+
+  // true: sorted; false: not a few-outlier input -- keys then hold a
+  // permutation of the input and the caller partitions them.  Round k
+  // compacts the remainder of round k-1 into the other buffer (kept first,
+  // its outliers after them, the older outliers copied behind), until the
+  // remainder is sorted (usually one or two rounds) or kOutlierRounds.
+  static constexpr int kOutlierRounds = 4;
+  bool run_outlier() {
+    if (HAS_V) return false;
+    ensure_ws();
+    static const bool dbg = getenv("SR_OUTLIER_DEBUG") != nullptr;
+    K* buf[2] = {keys, wk};
+    int cur = 0;        // buffer holding the current remainder [0, r) and outliers [r, n)
+    int64_t r = n;
+    for (int round = 1; round <= kOutlierRounds; round++) {
+      const int dst = 1 - cur;
+      auto res = outlier_round(buf[cur], r, buf[dst]);
+      if (r < n) {  // older outliers follow the new ones
+        std::vector<CopyJob> cj{{r, n - r, 0, dst == 0 ? 1 : 0, 0}};
+        run_copies(cj, ceil_div<int64_t>(n - r, 256 * 8), 2 * (n - r) * kw);
+      }
+      if (dbg)
+        fprintf(stderr, "[sr_outlier] n=%lld round %d: kept %lld of %lld, descents among kept %lld\n", (long long)n,
+                round, (long long)res.first, (long long)r, (long long)res.second);
+      r = res.first;
+      cur = dst;
+      c.plan.levels = round;
+      if (res.second == 0) {
+        sort_nested(buf[cur] + r, n - r);
+        merge_two(cur, r, n - r);  // -> the other buffer
+        if (cur == 0) {            // merged into the workspace: copy back
+          std::vector<CopyJob> cj{{0, n, 0, 1, 0}};
+          run_copies(cj, ceil_div<int64_t>(n, 256 * 8), 2 * n * kw);
+        }
+        return true;
+      }
+      if (8 * (n - r) > n) break;  // too many outliers: not a nearly sorted input
+    }
+    if (cur == 1) {  // the permutation is in the workspace
+      std::vector<CopyJob> cj{{0, n, 0, 1, 0}};
+      run_copies(cj, ceil_div<int64_t>(n, 256 * 8), 2 * n * kw);
+    }
+    return false;
+  }
+
+  // partition of keys driven by the host (no speculative level 1)
+  void partition_host(int64_t T) {
     c.plan.route = SR_ROUTE_PARTITION;
     c.plan.levels = 1;
     Level L1;
@@ -1103,7 +1230,7 @@ struct Sorter {
       run_resident();
       return;
     }
-    const int force = g_force_route;
+    const int force = forced();
     const int64_t T = choose_tile(n);
     const int64_t G = ceil_div<int64_t>(n, T);
     const bool part = n > kCap;
@@ -1157,7 +1284,7 @@ struct Sorter {
               kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr);
       }
     });
-    const int merge_ok = g_merge_route;
+    const int merge_ok = route_ok();
     c.launch("presort_resolve", G * (int64_t)sizeof(TileSummary), [&] {
       k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst, force, merge_ok);
     });
@@ -1215,6 +1342,12 @@ struct Sorter {
         return;
       default:
         break;
+    }
+    if (route == kRouteOutlier) {
+      c.plan.route = SR_ROUTE_OUTLIER;
+      if (run_outlier()) return;
+      partition_host(T);  // not a few-outlier input: keys hold a permutation
+      return;
     }
     bool use_merge = route == kRouteMerge;
     std::vector<Seg> segs;
@@ -1405,7 +1538,8 @@ const char* sr_last_error(void) { return t_state.err.c_str(); }
 int32_t sr_set_option(int32_t key, int64_t value) {
   switch (key) {
     case SR_OPT_FORCE_ROUTE:
-      if (value != 0 && value != SR_ROUTE_MERGE && value != SR_ROUTE_PARTITION) return SR_ERR_INVALID_ARGUMENT;
+      if (value != 0 && value != SR_ROUTE_MERGE && value != SR_ROUTE_PARTITION && value != SR_ROUTE_OUTLIER)
+        return SR_ERR_INVALID_ARGUMENT;
       g_force_route = (int)value;
       return SR_OK;
     case SR_OPT_PROFILE:
@@ -1416,6 +1550,9 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       return SR_OK;
     case SR_OPT_RESIDENT:
       g_resident = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_OUTLIER_ROUTE:
+      g_outlier = value ? 1 : 0;
       return SR_OK;
     case SR_OPT_RESIDENT_CAP:
       if (value < 1 || value > 16384) return SR_ERR_INVALID_ARGUMENT;

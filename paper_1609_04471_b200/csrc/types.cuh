@@ -11,7 +11,8 @@ struct TileSummary {
   int32_t nab;     // #{i in tile : descending-run break}
   int32_t fdesc, ldesc;
   int32_t fab, lab;
-  int32_t pad0, pad1;
+  int32_t nviol;   // descents whose outer neighbours are out of order (outlier route choice)
+  int32_t pad1;
 };
 
 // A long natural run [start, start+len) and its end keys as stored in the
@@ -68,7 +69,12 @@ struct OvfSeg {
 
 // route codes (equal to the SR_ROUTE_* values of include/sr_sort.h)
 constexpr int64_t kRouteSorted = 1, kRouteReversed = 2, kRouteMerge = 3, kRoutePartition = 4, kRouteTile = 5,
-                  kRouteUndecided = 6;
+                  kRouteOutlier = 6, kRouteUndecided = 8;
+// route_ok bits of the device resolve: merge route allowed, outlier route allowed
+constexpr int kAllowMerge = 1, kAllowOutlier = 2, kOutlierStrict = 4;
+constexpr int64_t kOutlierRatioStrict = 512;  // with kOutlierStrict (the one-launch resident range)
+constexpr int64_t kOutlierRatio = 32;  // outlier route when descents <= n / kOutlierRatio ...
+constexpr int64_t kViolRatio = 16;     // ... and at most 1/16 of them have out-of-order neighbours
 
 constexpr int kMaxBuckets = 2048;           // B_max per level
 constexpr int kMaxBins = 2 * kMaxBuckets + 1;

@@ -29,6 +29,7 @@ def _reset():
     sr.set_option(sr.OPT_RESIDENT, 1)
     sr.set_option(sr.OPT_RESIDENT_CAP, 16384)
     sr.set_option(sr.OPT_FORCE_ROUTE, 0)
+    sr.set_option(sr.OPT_OUTLIER_ROUTE, 1)
 
 
 def check(k, expect=None):
@@ -77,6 +78,8 @@ def test_resident_lowered_caps(cap, dtype):
 
 
 def test_resident_matches_multikernel():
+    # the outlier route's threshold differs by design between the two paths
+    sr.set_option(sr.OPT_OUTLIER_ROUTE, 0)
     for order in ORDERS:
         k = gen.make(order, 1 << 20, np.int32, config=10)
         sr.set_option(sr.OPT_RESIDENT, 0)
