@@ -103,13 +103,34 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, int bin, bool valid) {
 // a[i-1] > a[i+2]: removing the descent's two endpoints would not leave the
 // neighbourhood sorted.  Counted for the outlier route's choice (isolated
 // exchanges, have none; shuffled runs or a random tail have many).
-// pv / n2 are the warp's a[i-1] / a[i+2] (lane 0 and lanes 30-31 reload).
+// a[i-1] and a[i+2] come from the warp's shuffles and a halo loaded together
+// with the keys (no dependent loads).
 template <typename K>
-__device__ __forceinline__ int straddle_violation(const K* __restrict__ keys, int64_t n, int64_t i, int lane, K pv, K n2) {
-  if (i < 1 || i + 2 >= n) return 0;
-  const K a0 = lane == 0 ? keys[i - 1] : pv;
-  const K a3 = lane >= 30 ? keys[i + 2] : n2;
-  return a0 > a3 ? 1 : 0;
+__device__ __forceinline__ int straddle_regs(int64_t n, int64_t i, K am1, K ap2) {
+  return (i >= 1 && i + 2 < n && am1 > ap2) ? 1 : 0;
+}
+
+// Halo of a warp's 32 consecutive keys starting at i - lane: lane 0 loads
+// a[i-1], lane 31 loads a[i+1] and a[i+2], all issued with the keys.
+template <typename K>
+__device__ __forceinline__ void load_halo(const K* __restrict__ keys, int64_t n, int64_t i, int lane, K& h1, K& h2) {
+  h1 = K(0);
+  h2 = K(0);
+  if (lane == 0 && i >= 1 && i - 1 < n) h1 = keys[i - 1];
+  if (lane == 31 && i + 1 < n) h1 = keys[i + 1];
+  if (lane == 31 && i + 2 < n) h2 = keys[i + 2];
+}
+
+// Neighbours of x = a[i] from the warp: next a[i+1], prev a[i-1], next2 a[i+2].
+template <typename K>
+__device__ __forceinline__ void warp_neighbours(K x, K h1, K h2, int lane, K& next, K& prev, K& next2) {
+  next = __shfl_down_sync(0xffffffffu, x, 1);
+  prev = __shfl_up_sync(0xffffffffu, x, 1);
+  next2 = __shfl_down_sync(0xffffffffu, x, 2);
+  const K h1n = __shfl_down_sync(0xffffffffu, h1, 1);  // lane 30: lane 31's a[i+1] = its own a[i+2]
+  if (lane == 31) { next = h1; next2 = h2; }
+  if (lane == 30) next2 = h1n;
+  if (lane == 0) prev = h1;
 }
 
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
@@ -145,22 +166,22 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   int cd = 0, ca = 0, cv = 0;
   int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
   for (int64_t base = t0; base < t1; base += NT * U) {
-    K x[U];
+    K x[U], h1[U], h2[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int64_t i = base + u * NT + tid;
       x[u] = i < n ? keys[i] : K(0);
+      load_halo<K>(keys, n, i, lane, h1[u], h2[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int64_t i = base + u * NT + tid;
-      K y = __shfl_down_sync(0xffffffffu, x[u], 1);
-      const K pv = __shfl_up_sync(0xffffffffu, x[u], 1), n2 = __shfl_down_sync(0xffffffffu, x[u], 2);
-      if (lane == 31 && i + 1 < n) y = keys[i + 1];
+      K y, pv, n2;
+      warp_neighbours<K>(x[u], h1[u], h2[u], lane, y, pv, n2);
       if (i < t1 && i + 1 < n) {
         if (y < x[u]) {
           cd++; fd = min(fd, (int)i); ld = max(ld, (int)i);
-          cv += straddle_violation<K>(keys, n, i, lane, pv, n2);
+          cv += straddle_regs<K>(n, i, pv, n2);
         }
         bool brk = STRICT ? !(y < x[u]) : (x[u] < y);
         if (brk) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }
@@ -198,6 +219,24 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
       for (int b = tid; b < nbins; b += NT) mat[(int64_t)b * G + blockIdx.x] = s_hist[b];
     }
   }
+}
+
+// Device-side route (H3 first stage) from the resolved statistics;
+// kRouteUndecided hands the merge-vs-partition cost comparison to the host planner.
+__device__ __forceinline__ int64_t resolve_route(int64_t n, int64_t D, int64_t A, int64_t V, int64_t covA, int64_t covD,
+                                                 int force, int merge_ok) {
+  if (D == 0) return kRouteSorted;
+  if (A == 0 && force == 0) return kRouteReversed;
+  if (force == kRouteMerge) return kRouteMerge;
+  if (n <= kCap) return kRouteTile;
+  if (force == kRoutePartition) return kRoutePartition;
+  if (force == kRouteOutlier) return kRouteOutlier;
+  // few, isolated descents (k-exchange-like): extract the outliers
+  if ((merge_ok & kAllowOutlier) && A > 0 && kViolRatio * V <= D &&
+      ((merge_ok & kOutlierStrict) ? kOutlierRatioStrict : kOutlierRatio) * D <= n)
+    return kRouteOutlier;
+  if ((merge_ok & kAllowMerge) && 2 * (covA + covD) >= n) return kRouteUndecided;
+  return kRoutePartition;
 }
 
 // K2: resolve tile summaries into D, the long runs of both directions and
@@ -297,21 +336,7 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
       ndsc++;
       covD += lastLenD;
     }
-    // device-side route (H3 first stage); kRouteUndecided hands the merge-vs-
-    // partition cost comparison to the host planner.
-    int64_t route;
-    if (D == 0) route = kRouteSorted;
-    else if (A == 0 && force == 0) route = kRouteReversed;
-    else if (force == kRouteMerge) route = kRouteMerge;
-    else if (n <= kCap) route = kRouteTile;
-    else if (force == kRoutePartition) route = kRoutePartition;
-    else if (force == kRouteOutlier) route = kRouteOutlier;
-    // few, isolated descents (k-exchange-like): extract the outliers
-    else if ((merge_ok & kAllowOutlier) && A > 0 && kViolRatio * V <= D &&
-             ((merge_ok & kOutlierStrict) ? kOutlierRatioStrict : kOutlierRatio) * D <= n)
-      route = kRouteOutlier;
-    else if ((merge_ok & kAllowMerge) && 2 * (covA + covD) >= n) route = kRouteUndecided;
-    else route = kRoutePartition;
+    const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok);
     if (WRITE) {
       st->n = n;
       st->descents = D;
@@ -327,6 +352,125 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
   __syncthreads();
   const int64_t route = s_route;
   __syncthreads();
+  return route;
+}
+
+// K2 for one warp (the resident kernel, G <= 32 * 32 tiles): the same
+// statistics, run descriptors and route as presort_resolve_block, from tile
+// summaries already in shared memory, without block barriers.  Lane l owns the
+// contiguous tiles [l TPL, (l+1) TPL); the last break before its chunk comes
+// from a warp max-scan, the run descriptors' slots from a warp prefix sum.
+// All 32 lanes of the warp call; every lane returns the route.
+template <typename K, bool WRITE>
+__device__ int64_t presort_resolve_warp(const K* __restrict__ keys, int64_t n, const TileSummary* ts, int G,
+                                        int64_t lmin, RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
+                                        DevStats* __restrict__ st, int force, int merge_ok) {
+  const int lane = threadIdx.x & 31;
+  const int TPL = (G + 31) / 32;
+  const int t0 = lane * TPL < G ? lane * TPL : G, t1 = t0 + TPL < G ? t0 + TPL : G;
+  int64_t D = 0, A = 0, V = 0;
+  int32_t lastD = -1, lastA = -1;
+  for (int t = t0; t < t1; t++) {
+    D += ts[t].ndesc;
+    A += ts[t].nab;
+    V += ts[t].nviol;
+    lastD = max(lastD, ts[t].ldesc);
+    lastA = max(lastA, ts[t].lab);
+  }
+  int32_t carryD = lastD, carryA = lastA;  // inclusive max-scan, then shifted to exclusive
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t u = __shfl_up_sync(0xffffffffu, carryD, o), v = __shfl_up_sync(0xffffffffu, carryA, o);
+    if (lane >= o) { carryD = max(carryD, u); carryA = max(carryA, v); }
+  }
+  const int32_t endD = __shfl_sync(0xffffffffu, carryD, 31), endA = __shfl_sync(0xffffffffu, carryA, 31);
+  carryD = __shfl_up_sync(0xffffffffu, carryD, 1);
+  carryA = __shfl_up_sync(0xffffffffu, carryA, 1);
+  if (lane == 0) { carryD = -1; carryA = -1; }
+  // runs ending inside this lane's tiles
+  int nA = 0, nD = 0;
+  int64_t covA = 0, covD = 0;
+  {
+    int32_t pD = carryD, pA = carryA;
+    for (int t = t0; t < t1; t++) {
+      const TileSummary s = ts[t];
+      if (s.ndesc > 0 && (int64_t)s.fdesc - pD >= lmin) { nA++; covA += (int64_t)s.fdesc - pD; }
+      if (s.nab > 0 && (int64_t)s.fab - pA >= lmin) { nD++; covD += (int64_t)s.fab - pA; }
+      pD = max(pD, s.ldesc);
+      pA = max(pA, s.lab);
+    }
+  }
+  int exA = nA, exD = nD;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, exA, o), v = __shfl_up_sync(0xffffffffu, exD, o);
+    if (lane >= o) { exA += u; exD += v; }
+  }
+  const int totA = __shfl_sync(0xffffffffu, exA, 31), totD = __shfl_sync(0xffffffffu, exD, 31);
+  exA -= nA;
+  exD -= nD;
+  if (WRITE) {
+    int32_t pD = carryD, pA = carryA;
+    for (int t = t0; t < t1; t++) {
+      const TileSummary s = ts[t];
+      if (s.ndesc > 0 && (int64_t)s.fdesc - pD >= lmin) {
+        RunDesc r;
+        r.start = pD + 1; r.len = (int64_t)s.fdesc - pD;
+        r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
+        asc[exA++] = r;
+      }
+      if (s.nab > 0 && (int64_t)s.fab - pA >= lmin) {
+        RunDesc r;
+        r.start = pA + 1; r.len = (int64_t)s.fab - pA;
+        r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[r.start + r.len - 1];
+        desc[exD++] = r;
+      }
+      pD = max(pD, s.ldesc);
+      pA = max(pA, s.lab);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    D += __shfl_xor_sync(0xffffffffu, D, o);
+    A += __shfl_xor_sync(0xffffffffu, A, o);
+    V += __shfl_xor_sync(0xffffffffu, V, o);
+    covA += __shfl_xor_sync(0xffffffffu, covA, o);
+    covD += __shfl_xor_sync(0xffffffffu, covD, o);
+  }
+  int64_t nasc = totA, ndsc = totD;
+  // final runs after the last break
+  const int64_t lastLen = n - 1 - (int64_t)endD, lastLenD = n - 1 - (int64_t)endA;
+  if (n > 0 && lastLen >= lmin) {
+    if (WRITE && lane == 0) {
+      RunDesc r;
+      r.start = endD + 1; r.len = lastLen;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+      asc[nasc] = r;
+    }
+    nasc++;
+    covA += lastLen;
+  }
+  if (n > 0 && lastLenD >= lmin) {
+    if (WRITE && lane == 0) {
+      RunDesc r;
+      r.start = endA + 1; r.len = lastLenD;
+      r.kfirst = (int64_t)keys[r.start]; r.klast = (int64_t)keys[n - 1];
+      desc[ndsc] = r;
+    }
+    ndsc++;
+    covD += lastLenD;
+  }
+  const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok);
+  if (WRITE && lane == 0) {
+    st->n = n;
+    st->descents = D;
+    st->asc_breaks = A;
+    st->n_asc_runs = nasc;
+    st->n_desc_runs = ndsc;
+    st->asc_cover = covA;
+    st->desc_cover = covD;
+    st->route = route;
+  }
   return route;
 }
 

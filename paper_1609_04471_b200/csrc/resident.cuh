@@ -51,25 +51,38 @@ namespace sr {
 constexpr int kResNT = 512;
 constexpr int kResCtasPerSM = 1;
 constexpr int kResWarps = kResNT / 32;
-constexpr int kResTile = 8192;          // presort tile in the resident range (choose_tile)
-constexpr int kResGrp = 8192;           // phase C grouping unit: one tile-local counting sort
-constexpr int kResO1 = 8;               // level-1 oversampling
-constexpr int kResFill = 32768;         // equality fill per unit
-constexpr int kResMaxNG = 512;          // grouping units (n <= kResMaxNG * kResGrp)
+constexpr int kResGrp = 8192;           // largest tile: H1 scan unit and phase C grouping unit (one
+                                        // tile-local counting sort); the host picks the tile so that
+                                        // every CTA gets <= GPC tiles and the samplers one
+constexpr int kResSB = kResNT / 32;     // level-2 (in-CTA) sub-buckets per bucket: one per warp
+constexpr int kResO2 = 8;               // level-2 oversampling
+constexpr int kResS2 = kResO2 * kResSB; // level-2 sample
+constexpr int kResWarpFill = 4096;      // equality fill per warp unit
+constexpr int kResSamplers = 4;         // CTAs that sort one quarter of the level-1 sample each
+constexpr int kResMaxG = 512;           // tiles (G <= GPC * gridDim.x - kResSamplers)
 
 template <typename K> struct ResCfg;
 template <> struct ResCfg<int32_t> {
   static constexpr int CAPB = 16384;    // largest level-1 bucket sorted by one CTA
-  static constexpr int B1MAX = 1024;    // level-1 buckets
+  static constexpr int B1MAX = 2048;    // level-1 buckets
+  static constexpr int O1 = 4;          // level-1 oversampling (S1 = O1 B1 <= 8192: four 2048-key sampler sorts)
+  static constexpr int GPC = 2;         // grouping units held per CTA across the scatter barrier
+  static constexpr int WCAP = 2048;     // level-1 buckets up to this size are sorted by one warp
+  static constexpr int TARGET = 1024;   // mean level-1 bucket the host aims for
   static constexpr int64_t MAXN = int64_t(4) << 20;
 };
 template <> struct ResCfg<int64_t> {
   static constexpr int CAPB = 8192;
   static constexpr int B1MAX = 1024;
+  static constexpr int O1 = 8;
+  static constexpr int GPC = 1;
+  static constexpr int WCAP = 1024;
+  static constexpr int TARGET = 4096;
   static constexpr int64_t MAXN = int64_t(4) << 20;
 };
 constexpr int64_t kResMaxN = ResCfg<int32_t>::MAXN;  // largest resident n over the key types
-static_assert(kResMaxN <= (int64_t)kResMaxNG * kResGrp, "");
+
+struct ResDone;
 
 template <typename K>
 struct ResArgs {
@@ -82,18 +95,36 @@ struct ResArgs {
   RunDesc* desc;
   DevStats* st;             // route, statistics; n_ovf counts the host list
   int S1, B1;               // level-1 sample size, buckets (power of two <= B1MAX)
-  int NG;                   // grouping units of kResGrp keys
-  K* samp;                  // S1 keys: the two sorted halves of the level-1 sample
-  uint32_t* tot;            // 2 B1 + 1 bucket totals (zeroed by the host)
-  uint32_t* mcnt;           // NG x nbins: per-group bucket counts
-  uint32_t* mlst;           // NG x nbins: per-group bucket starts inside the group's span of ws
+  int NG;                   // grouping units = the scan tiles (NG = G)
+  K* samp;                  // S1 keys: the sorted pieces of the level-1 sample
+  uint32_t* tot;            // 2 B1 + 1 bucket totals (zeroed in phase A)
+  uint32_t* goff;           // NG x nbins: offset of group t's piece inside bucket b
   OvfSeg* ovf;              // ranges of keys left unsorted for the host's next level
   int64_t lmin;
   int force, merge_ok;
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
-  uint32_t* unit_counter;   // phase E work counter (zeroed by the host)
+  uint32_t* unit_counter;   // [0] CTA units, [1] CTAs done, [2] warp units (zeroed by CTA 0 in phase A)
+  int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
+  ResDone* done;            // host-mapped completion record (the last CTA to exit writes it)
+  uint32_t seq;             // this call's completion sequence number
 };
+
+// Host-mapped completion record: the statistics the planner needs, written by
+// the last CTA to leave the kernel, then the sequence number.  The host spins on
+// `seq` instead of a device->host copy + stream synchronisation (~10 us less
+// per call, tools/micro/api.cu).
+struct ResDone {
+  DevStats st;
+  volatile uint32_t seq;
+  uint32_t pad[31];
+};
+
+// phase C sub-steps of CTA 0's first group (SR_TIMING diagnostics)
+#define SR_RES_SUB(kk)                                                                              \
+  do {                                                                                              \
+    if (a.tstamp && c == 0 && k == 0 && tid == 0) a.tstamp[8 + 8 * (size_t)gridDim.x + 8 + (kk)] = res_now(); \
+  } while (0)
 
 #define SR_RES_STAMP(k)                                                                \
   do {                                                                                 \
@@ -106,30 +137,67 @@ __device__ __forceinline__ unsigned long long res_now() {
   return t;
 }
 
+// Every CTA calls this once on its way out (the route decisions are uniform
+// per CTA); the last one publishes the statistics to the host-mapped record.
+// Classic fence + counter: every CTA's global writes (statistics atomics
+// included) precede its increment, so the last CTA sees them all.
+template <typename K>
+__device__ __forceinline__ void res_exit(const ResArgs<K>& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(a.unit_counter + 1, 1u);
+    if (prev == gridDim.x - 1 && a.done) {
+      __threadfence();
+      const unsigned long long* s = reinterpret_cast<const unsigned long long*>(a.st);
+      unsigned long long* d = reinterpret_cast<unsigned long long*>(&a.done->st);
+      for (int i = 0; i < (int)(sizeof(DevStats) / 8); i++) d[i] = __ldcg(s + i);
+      __threadfence_system();
+      a.done->seq = a.seq;
+    }
+  }
+}
+
 // Shared memory: the persistent bucket table + phase-local buffers in a union.
 template <typename K>
 struct ResSmem {
   static constexpr int CAPB = ResCfg<K>::CAPB;
   static constexpr int B1MAX = ResCfg<K>::B1MAX;
   static constexpr int NB1 = 2 * B1MAX + 1;
-  static constexpr int S1MAX = kResO1 * B1MAX;
-  struct alignas(16) CT {          // C: one group's counting sort
-    uint32_t cnt[NB1];
-    uint32_t lst[NB1];
-    K stk[kResGrp];
+  static constexpr int S1MAX = ResCfg<K>::O1 * B1MAX;
+  static constexpr int WCAP = ResCfg<K>::WCAP;
+  static constexpr int GPC = ResCfg<K>::GPC;
+  struct alignas(16) CT {          // C: tile-local counting sorts of this CTA's groups
+    uint32_t cnt[NB1];             // current group's bucket counts; in D its piece offsets (goff)
+    uint32_t lst[GPC][NB1 + 1];    // per held group: bucket starts inside stk, lst[nbins] = group length
+    K stk[GPC][kResGrp];           // per held group: its keys grouped by bucket
+    uint16_t stb[GPC][kResGrp];    // per held group: the bucket of stk[i]
+  };
+  struct alignas(16) SP {          // C: tile summaries, the sorted sample pieces, pairwise merged
+    K q[S1MAX];
+    K mrg[S1MAX];
+    TileSummary ts[kResMaxG];
   };
   struct alignas(16) E {
-    K x[CAPB];                     // the gathered bucket (padded to whole runs)
-    K y[CAPB];                     // merge ping-pong buffer
-    uint32_t piece[kResMaxNG + 1]; // gather offsets of the bucket's per-group pieces
-    uint32_t pbase[kResMaxNG];     // ws position of each piece
+    K x[CAPB];                     // the bucket (E); warp-unit staging areas span x and y
+    K y[CAPB];                     // sub-bucket regions / merge ping-pong buffer
+    K samp[kResS2];                // level-2 sample
+    K tree[kResSB];                // level-2 Eytzinger tree [1, SB)
+    uint32_t wcnt[kResWarps][kResSB];  // per-warp sub-bucket counts, then write cursors
+    uint32_t reg[kResSB + 1];      // sub-bucket regions in y (16-byte aligned, sized for the warp network)
+    uint32_t ost[kResSB + 1];      // sub-bucket starts in the output
+    uint8_t bin[CAPB];             // sub-bucket of x[i]
   };
+  static_assert(kResWarps * WCAP <= 2 * CAPB, "warp-unit staging areas live in x and y");
   uint32_t start[NB1 + 1];         // level-1 bucket starts, start[nbins] = n
-  uint32_t upre[NB1 + 1];          // exclusive prefix of E units per bin
+  uint16_t upa[NB1 + 1];           // exclusive prefix of E warp units, class A (WCAP/2 < range bucket <= WCAP)
+  uint16_t upb[NB1 + 1];           // exclusive prefix of E warp units, class B (smaller range buckets, fills)
+  uint16_t cbin[B1MAX + 8];        // E CTA units: range buckets above WCAP
   K tree1[2 * B1MAX];              // level-1 Eytzinger tree [1, B1) + sorted splitters at [B1MAX, ...)
   uint8_t eq1[B1MAX];
   union alignas(16) {
-    K samp1[S1MAX];                // A: half of the level-1 sample + BitonicSort scratch
+    K samp1[S1MAX];                // A: the sampler's piece of the sample + BitonicSort scratch
+    SP sp;
     CT ct;
     E e;
   } u;
@@ -233,7 +301,7 @@ __device__ __forceinline__ void res_group_sort(const K* src, int count, K* __res
 // PAPER.md:99), the last round writing straight into dst.  The tail up to a
 // whole run is padded with +inf, which sorts last and is not written.
 template <typename K, int NT>
-__device__ void res_bucket_sort(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
+__device__ __noinline__ void res_bucket_sort(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
                                 unsigned long long* prof = nullptr) {
   constexpr int VT = 8;  // merge outputs per thread
   constexpr int RVT = 8, RGL = 16;  // runs: 16-lane groups of VT 8 (128 keys), two per warp
@@ -322,6 +390,162 @@ __device__ void res_bucket_sort(K* __restrict__ dst, int L, typename ResSmem<K>:
   mark(2);
 }
 
+// Footprint of WarpBitonic<K, VT>::sort for `len` keys with the VT the warp
+// units and sub-buckets use (it stores nl * VT keys, nl a power of two).
+__device__ __forceinline__ int res_vt(int len) {
+  return len <= 128 ? 4 : len <= 256 ? 8 : len <= 512 ? 16 : len <= 1024 ? 32 : 64;
+}
+__device__ __forceinline__ int res_footprint(int len) {
+  if (len <= 0) return 0;
+  const int vt = res_vt(len);
+  const int need = (len + vt - 1) / vt;
+  int nl = 1;
+  while (nl < need) nl <<= 1;
+  return vt * nl;
+}
+
+// Sort stage[0, len) (16-byte aligned, res_footprint(len) keys writable) by one
+// warp's register network, the narrowest that holds it.
+template <typename K, int WCAP>
+__device__ __noinline__ void res_warp_sort(K* stage, int len) {
+  if (len <= 128) WarpBitonic<K, 4>::sort(stage, len);
+  else if (len <= 256) WarpBitonic<K, 8>::sort(stage, len);
+  else if (len <= 512) WarpBitonic<K, 16>::sort(stage, len);
+  else if (WCAP >= 1024 && len <= 1024) WarpBitonic<K, (WCAP >= 1024 ? 32 : 16)>::sort(stage, len);
+  else WarpBitonic<K, WCAP / 32>::sort(stage, len);
+}
+
+// One CTA sorts x[0, L) (WCAP < L <= CAPB, gathered in shared memory) into
+// dst: H11 for one level-1 bucket as a second, in-shared-memory partition level
+// (the quicksort recursion, Appendix B; R17).
+// is_sorted first.  Then one sub-bucket per warp: the 15
+// splitters are every o2-th key of a regular sample of kResS2 keys, sorted by
+// counting ranks (the sample-based pivot choice); every key is
+// classified by a 4-level Eytzinger tree, counted per warp, and moved to its
+// sub-bucket's region of y; each warp sorts its sub-bucket in registers (the
+// "insertion sort below alpha" step) and writes it to dst.
+// Sub-buckets above WCAP keys or regions that do not fit y (heavy duplicates,
+// skew) send the bucket to the run + merge sort above.
+template <typename K, int NT>
+__device__ __noinline__ void res_bucket_sort2(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
+                                 unsigned long long* prof = nullptr) {
+  constexpr int NW = NT / 32;
+  constexpr int SB = kResSB, DEPTH = 4;
+  constexpr int WCAP = ResSmem<K>::WCAP;
+  constexpr int UC = 8;  // keys per thread per classification round
+  static_assert(SB == NW && (1 << DEPTH) == SB && NT % kResS2 == 0, "one sub-bucket per warp, whole threads per sample");
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned long long tprev = (prof && tid == 0) ? res_now() : 0;
+  auto mark = [&](int k) {
+    if (prof && tid == 0) {
+      const unsigned long long t = res_now();
+      prof[k] += t - tprev;
+      tprev = t;
+    }
+  };
+  int unsorted = 0;
+  for (int i = tid; i + 1 < L; i += NT) unsorted |= e.x[i + 1] < e.x[i];
+  if (tid < kResS2) e.samp[tid] = e.x[(int)(((int64_t)(2 * tid + 1) * L) / (2 * kResS2))];
+  if (!__syncthreads_or(unsorted)) {
+    for (int i = tid; i < L; i += NT) dst[i] = e.x[i];
+    return;
+  }
+  {  // rank of sample q = position in the stably sorted sample; four threads per sample
+    constexpr int TPS = NT / kResS2, PART = kResS2 / TPS;
+    const int q = tid / TPS, h = tid % TPS;
+    const K v = e.samp[q];
+    int r = 0;
+#pragma unroll 8
+    for (int j = h * PART; j < (h + 1) * PART; j++) {
+      const K u = e.samp[j];
+      r += (u < v) || (u == v && j < q);
+    }
+#pragma unroll
+    for (int o = 1; o < TPS; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (h == 0) e.y[r] = v;  // y is free until the move
+    if (tid < NW * SB) (&e.wcnt[0][0])[tid] = 0u;
+  }
+  __syncthreads();
+  if (tid > 0 && tid < SB) {  // Eytzinger node i <- splitter pos = sorted sample o2 (pos + 1)
+    const int d = 31 - __clz(tid);
+    const int pos = ((2 * (tid - (1 << d)) + 1) << (DEPTH - 1 - d)) - 1;
+    e.tree[tid] = e.y[kResO2 * (pos + 1)];
+  }
+  __syncthreads();
+  mark(0);
+  auto classify = [&](K x) {
+    int j = 1;
+#pragma unroll
+    for (int l = 0; l < DEPTH; l++) j = 2 * j + (e.tree[j] < x ? 1 : 0);
+    return j - SB;
+  };
+  for (int i0 = 0; i0 < L; i0 += NT * UC) {  // per-warp counts
+#pragma unroll
+    for (int u = 0; u < UC; u++) {
+      const int i = i0 + u * NT + tid;
+      if (i < L) {
+        const int b = classify(e.x[i]);
+        e.bin[i] = (uint8_t)b;
+        atomicAdd(&e.wcnt[w][b], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (w == 0) {  // totals -> output starts and footprint-sized regions; cursors
+    uint32_t cb = 0;
+    if (lane < SB)
+#pragma unroll
+      for (int v = 0; v < NW; v++) cb += e.wcnt[v][lane];
+    const int fp = lane < SB ? res_footprint((int)cb) : 0;
+    uint32_t oi = cb, ri = (uint32_t)fp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t1 = __shfl_up_sync(0xffffffffu, oi, o), t2 = __shfl_up_sync(0xffffffffu, ri, o);
+      if (lane >= o) { oi += t1; ri += t2; }
+    }
+    if (lane < SB) {
+      e.ost[lane] = oi - cb;
+      e.reg[lane] = ri - fp;
+      uint32_t run = ri - fp;
+#pragma unroll
+      for (int v = 0; v < NW; v++) {
+        const uint32_t c = e.wcnt[v][lane];
+        e.wcnt[v][lane] = run;
+        run += c;
+      }
+    }
+    const int bad = (lane < SB && cb > (uint32_t)WCAP) || (lane == SB - 1 && ri > (uint32_t)ResSmem<K>::CAPB);
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) e.ost[SB] = anybad ? 0xffffffffu : (uint32_t)L;
+  }
+  __syncthreads();
+  if (e.ost[SB] == 0xffffffffu) {  // heavy duplicates / skew: the general run + merge sort
+    res_bucket_sort<K, NT>(dst, L, e, nullptr);
+    return;
+  }
+  for (int i0 = 0; i0 < L; i0 += NT * UC) {  // move to the sub-bucket regions (same key <-> warp map)
+#pragma unroll
+    for (int u = 0; u < UC; u++) {
+      const int i = i0 + u * NT + tid;
+      if (i < L) {
+        e.y[atomicAdd(&e.wcnt[w][e.bin[i]], 1u)] = e.x[i];
+      }
+    }
+  }
+  __syncthreads();
+  mark(1);
+  {
+    const int o = (int)e.ost[w], len = (int)e.ost[w + 1] - o;
+    K* ks = e.y + e.reg[w];
+    if (len > 1) res_warp_sort<K, WCAP>(ks, len);
+    for (int i = lane; i < len; i += 32) dst[o + i] = ks[i];
+  }
+  __syncthreads();
+  mark(2);
+}
+
+static_assert(sizeof(ResSmem<int32_t>) <= 227 * 1024 && sizeof(ResSmem<int64_t>) <= 227 * 1024,
+              "one CTA per SM: the shared-memory layout must fit the 227 KB opt-in limit");
 static_assert(offsetof(ResSmem<int32_t>, u) % 16 == 0 && offsetof(ResSmem<int64_t>, u) % 16 == 0,
               "vectorised sort buffers need 16-byte alignment");
 
@@ -341,21 +565,25 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
 
   // ================= A: H1 tile scan; level-1 sample ranked by every CTA =================
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[0] = res_now();
-  // level-1 sample: two halves of S1/2, each gathered and sorted by one of the
-  // last two CTAs (they scan the fewest tiles); every CTA later picks the
-  // splitters from the two sorted halves by merge-path selection
-  const int S1 = a.S1, H1 = S1 / 2;
+  if (c == 0) {  // control block (statistics, counters, bucket totals): first used after the grid sync
+    uint32_t* z = reinterpret_cast<uint32_t*>(a.st);
+    for (int i = tid; i < a.ctrl_words; i += NT) z[i] = 0u;
+  }
+  // level-1 sample: kResSamplers pieces, each gathered and sorted by one of the
+  // last CTAs (they scan one tile); every CTA merges them pairwise into two
+  // halves and picks the splitters by merge-path selection (R14)
+  const int S1 = a.S1, QS = S1 / kResSamplers, H1 = S1 / 2;
   constexpr int B1MAX = SM::B1MAX;
-  constexpr int SG = SM::S1MAX / 2 / NT;
-  const int half1 = P - 1 - c;
-  const bool sampler = half1 < 2;
+  constexpr int SG = SM::S1MAX / kResSamplers / NT;
+  const int quarter = P - 1 - c;  // this sampler's piece of the sample
+  const bool sampler = quarter < kResSamplers;
   K sx[SG];
   if (sampler) {  // gathers issued first, so they overlap the scan
     const int log2S = __ffs(S1) - 1;
 #pragma unroll
     for (int r = 0; r < SG; r++) {
       const int q = r * NT + tid;
-      sx[r] = q < H1 ? a.keys[sample_position(0, n, S1, (int64_t)half1 * H1 + q, log2S)] : K(0);
+      sx[r] = q < QS ? a.keys[sample_position(0, n, S1, (int64_t)quarter * QS + q, log2S)] : K(0);
     }
   }
   constexpr int UA = 16;  // keys per thread per load round
@@ -365,23 +593,22 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     int cd = 0, ca = 0, cv = 0;
     int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
     for (int64_t base = t0; base < t1; base += NT * UA) {
-      K x[UA], nx[UA];
+      K x[UA], h1[UA], h2[UA];
 #pragma unroll
       for (int u = 0; u < UA; u++) {
         const int64_t i = base + u * NT + tid;
         x[u] = i < n ? a.keys[i] : K(0);
-        nx[u] = (lane == 31 && i + 1 < n) ? a.keys[i + 1] : K(0);  // next warp's first key
+        load_halo<K>(a.keys, n, i, lane, h1[u], h2[u]);
       }
 #pragma unroll
       for (int u = 0; u < UA; u++) {
         const int64_t i = base + u * NT + tid;
-        K y = __shfl_down_sync(0xffffffffu, x[u], 1);
-        const K pv = __shfl_up_sync(0xffffffffu, x[u], 1), n2 = __shfl_down_sync(0xffffffffu, x[u], 2);
-        if (lane == 31) y = nx[u];
+        K y, pv, n2;
+        warp_neighbours<K>(x[u], h1[u], h2[u], lane, y, pv, n2);
         if (i < t1 && i + 1 < n) {
           if (y < x[u]) {
             cd++; fd = min(fd, (int)i); ld = max(ld, (int)i);
-            cv += straddle_violation<K>(a.keys, n, i, lane, pv, n2);
+            cv += straddle_regs<K>(n, i, pv, n2);
           }
           if (x[u] < y) { ca++; fa = min(fa, (int)i); la = max(la, (int)i); }  // keys only: non-increasing runs
         }
@@ -419,26 +646,76 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
 #pragma unroll
     for (int r = 0; r < SG; r++) {
       const int q = r * NT + tid;
-      if (q < H1) sm.u.samp1[q] = sx[r];
+      if (q < QS) sm.u.samp1[q] = sx[r];
     }
     __syncthreads();
-    BitonicSort<K, NT, SM::S1MAX / 2 / NT>::sort(sm.u.samp1, H1);
-    for (int q = tid; q < H1; q += NT) a.samp[(int64_t)half1 * H1 + q] = sm.u.samp1[q];
+    BitonicSort<K, NT, SG>::sort(sm.u.samp1, QS);
+    for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = sm.u.samp1[q];
   }
   SR_RES_STAMP(1);
   grid.sync();
 
   // ================= C: route (every CTA); splitters; tile-local bucket grouping =================
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[1] = res_now();
-  int64_t route;
-  if (c == 0)
-    route = presort_resolve_block<K, NT, true>(a.keys, n, a.sums, a.G, a.lmin, a.asc, a.desc, a.st, a.force,
-                                                a.merge_ok);
-  else
-    route = presort_resolve_block<K, NT, false>(a.keys, n, a.sums, a.G, a.lmin, a.asc, a.desc, a.st, a.force,
-                                                 a.merge_ok);
+  typename SM::SP& sp = sm.u.sp;
+  {  // tile summaries and the sorted sample pieces into shared memory
+    const int4* src = reinterpret_cast<const int4*>(a.sums);
+    int4* dst = reinterpret_cast<int4*>(sp.ts);
+    for (int i = tid; i < 2 * a.G; i += NT) dst[i] = __ldcg(src + i);
+    constexpr int SI = SM::S1MAX / NT;
+    K v[SI];
+#pragma unroll
+    for (int r = 0; r < SI; r++) v[r] = r * NT + tid < S1 ? __ldcg(a.samp + r * NT + tid) : K(0);
+#pragma unroll
+    for (int r = 0; r < SI; r++)
+      if (r * NT + tid < S1) sp.q[r * NT + tid] = v[r];
+  }
+  __syncthreads();
+  __shared__ int64_t s_route;
+  __shared__ K* s_halves;
+  if (w == 0) {  // H1 resolve by one warp (CTA 0 also writes the statistics and run lists)
+    const int64_t r = c == 0 ? presort_resolve_warp<K, true>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
+                                                             a.force, a.merge_ok)
+                             : presort_resolve_warp<K, false>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
+                                                              a.force, a.merge_ok);
+    if (lane == 0) s_route = r;
+  } else {  // meanwhile: merge the sorted sample pieces pairwise until two halves remain
+    const int wt = tid - 32, nth = NT - 32;
+    const int per = (S1 + nth - 1) / nth;  // outputs per thread per round
+    const int d0 = wt * per;
+    K* src = sp.q;
+    K* dst = sp.mrg;
+    for (int R = QS; R < H1; R *= 2) {
+      for (int d = d0; d < d0 + per && d < S1;) {
+        const int m = d / (2 * R);  // which pairwise merge
+        const K* A = src + m * 2 * R;
+        const K* B = A + R;
+        const int dm = d - m * 2 * R;
+        const int cnt = min(d0 + per, (m + 1) * 2 * R) - d;
+        int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, dm);
+        int j = dm - i;
+        for (int k = 0; k < cnt; k++) {
+          const bool tA = j >= R || (i < R && !(B[j] < A[i]));
+          dst[d + k] = tA ? A[i] : B[j];
+          i += tA;
+          j += !tA;
+        }
+        d += cnt;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NT - 32) : "memory");  // the merging warps only
+      K* t = src;
+      src = dst;
+      dst = t;
+    }
+    if (wt == 0) s_halves = src;
+  }
+  __syncthreads();
+  const int64_t route = s_route;
   SR_RES_STAMP(2);
-  if (route == kRouteSorted) return;
+  if (route == kRouteSorted) {
+    res_exit(a);
+    return;
+  }
   if (route == kRouteReversed) {
     const int64_t half = n / 2;
     for (int64_t p = (int64_t)c * NT + tid; p < half; p += (int64_t)P * NT) {
@@ -446,30 +723,23 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       a.keys[p] = y;
       a.keys[n - 1 - p] = x;
     }
+    res_exit(a);
     return;
   }
-  if (route != kRoutePartition) return;  // MERGE / undecided: the host planner continues
+  if (route != kRoutePartition) {  // MERGE / undecided: the host planner continues
+    res_exit(a);
+    return;
+  }
   const int m1 = a.B1 - 1;
   const int depth1 = tree_depth(m1);
-  {  // splitter j = element 8(j+1) of the merged halves (R9), with its gamma flag
-    K* hs = sm.u.samp1;  // [0, H1) half 0, [H1, S1) half 1
-    {
-      constexpr int SI = SM::S1MAX / NT;
-      K v[SI];
-#pragma unroll
-      for (int r = 0; r < SI; r++) v[r] = r * NT + tid < S1 ? __ldcg(a.samp + r * NT + tid) : K(0);
-#pragma unroll
-      for (int r = 0; r < SI; r++)
-        if (r * NT + tid < S1) hs[r * NT + tid] = v[r];
-    }
-    __syncthreads();
-    const K* A0 = hs;
-    const K* A1 = hs + H1;
-    for (int j = tid; j < B1MAX; j += NT) {
+  {  // splitter j = element O1 (j+1) of the merged halves (R9, R14), with its gamma flag
+    const K* A0 = s_halves;
+    const K* A1 = s_halves + H1;
+    for (int j = tid; j < B1MAX; j += NT) {  // the splitter copy at tree1[B1MAX + j] lives outside the union
       K t = KeyTraits<K>::max_key();
       uint8_t f = 0;
       if (j < m1) {
-        const int r = (j + 1) * kResO1;
+        const int r = (j + 1) * ResCfg<K>::O1;
         const int d0 = r - 2 > 0 ? r - 2 : 0;
         int i0 = merge_path_search<K>([&](int i) { return A0[i]; }, H1, [&](int i) { return A1[i]; }, H1, d0);
         int i1 = d0 - i0;
@@ -495,12 +765,15 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   res_build_tree<K, B1MAX>(depth1, sm.tree1);
   __syncthreads();
   SR_RES_STAMP(3);
+  const int ngm = a.NG > c ? (a.NG - 1 - c) / P + 1 : 0;  // groups of this CTA: t = c + k P, k < ngm <= GPC
   {
     typename SM::CT& ct = sm.u.ct;
     constexpr int U = kResGrp / NT;
-    for (int t = c; t < a.NG; t += P) {
-      const int64_t t0 = (int64_t)t * kResGrp;
-      const int64_t t1 = t0 + kResGrp < n ? t0 + kResGrp : n;
+    for (int k = 0; k < ngm; k++) {
+      const int t = c + k * P;
+      const int64_t t0 = (int64_t)t * a.tile;
+      const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
+      SR_RES_SUB(0);
       for (int b = tid; b < nbins; b += NT) ct.cnt[b] = 0;
       K x[U];
       int bin[U];
@@ -510,6 +783,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         x[u] = i < t1 ? a.keys[i] : K(0);
       }
       res_classify<K, B1MAX, U>(x, bin, sm.tree1, sm.eq1, m1, depth1);
+      SR_RES_SUB(1);
       __syncthreads();
       uint32_t rk[U];
 #pragma unroll
@@ -530,29 +804,44 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         }
         if (!valid) bin[u] = -1;
       }
+      SR_RES_SUB(2);
       __syncthreads();
-      for (int b = tid; b < nbins; b += NT) ct.lst[b] = ct.cnt[b];
+      uint32_t* lst = ct.lst[k];
+      {  // unrolled: all of a thread's atomics in flight together
+        constexpr int BI = (SM::NB1 + NT - 1) / NT;
+        uint32_t go[BI];
+#pragma unroll
+        for (int r = 0; r < BI; r++) {
+          const int b = r * NT + tid;
+          const uint32_t cb = b < nbins ? ct.cnt[b] : 0u;
+          if (b < nbins) lst[b] = cb;
+          // this group's piece of bucket b starts at offset goff inside the bucket
+          // (pieces of different groups in arbitrary order: the bucket is sorted later)
+          go[r] = cb ? atomicAdd(&a.tot[b], cb) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < BI; r++)
+          if (r * NT + tid < nbins) a.goff[(size_t)t * nbins + r * NT + tid] = go[r];
+      }
+      if (tid == 0) lst[nbins] = (uint32_t)(t1 - t0);
+      SR_RES_SUB(3);
       __syncthreads();
-      smem_scan<NT>(ct.lst, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+      smem_scan<NT>(lst, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+      SR_RES_SUB(4);
 #pragma unroll
       for (int u = 0; u < U; u++)
-        if (bin[u] >= 0) ct.stk[ct.lst[bin[u]] + rk[u]] = x[u];
-      for (int b = tid; b < nbins; b += NT) {  // this tile's bucket table + the global totals
-        const uint32_t cb = ct.cnt[b];
-        a.mcnt[(size_t)t * nbins + b] = cb;
-        a.mlst[(size_t)t * nbins + b] = ct.lst[b];
-        if (cb) atomicAdd(&a.tot[b], cb);
-      }
+        if (bin[u] >= 0) {
+          ct.stk[k][lst[bin[u]] + rk[u]] = x[u];
+          ct.stb[k][lst[bin[u]] + rk[u]] = (uint16_t)bin[u];
+        }
       __syncthreads();
-      for (int i = tid; i < (int)(t1 - t0); i += NT) a.ws[t0 + i] = ct.stk[i];  // contiguous, coalesced
-      __syncthreads();
+      SR_RES_SUB(5);
     }
   }
   SR_RES_STAMP(4);
   grid.sync();
 
-  // ================= E: bucket starts; fills and per-CTA bucket sorts =================
-  if (a.tstamp && c == 0 && tid == 0) a.tstamp[2] = res_now();
+  // ================= D: bucket starts; pieces written to their buckets in ws =================
   uint32_t* start = sm.start;
   {
     constexpr int BI = (SM::NB1 + NT - 1) / NT;
@@ -567,13 +856,98 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   smem_scan<NT>(start, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
   if (tid == 0) start[nbins] = (uint32_t)n;
   __syncthreads();
-  for (int b = tid; b < nbins; b += NT) {
-    const uint32_t cnt = start[b + 1] - start[b];
-    sm.upre[b] = (b & 1) ? (cnt + kResFill - 1) / kResFill : (cnt > 0 ? 1u : 0u);
+  {  // every key of a held group to its bucket in ws (runs of the same bucket are
+     // consecutive, so the stores coalesce per piece); equality buckets are
+     // filled in E
+    typename SM::CT& ct = sm.u.ct;
+    for (int k = 0; k < ngm; k++) {
+      const int t = c + k * P;
+      {
+        constexpr int BI = (SM::NB1 + NT - 1) / NT;
+        uint32_t go[BI];
+#pragma unroll
+        for (int r = 0; r < BI; r++)
+          go[r] = r * NT + tid < nbins ? __ldcg(a.goff + (size_t)t * nbins + r * NT + tid) : 0u;
+#pragma unroll
+        for (int r = 0; r < BI; r++)
+          if (r * NT + tid < nbins) ct.cnt[r * NT + tid] = start[r * NT + tid] + go[r];
+      }
+      __syncthreads();
+      const uint32_t* lst = ct.lst[k];
+      const int len = (int)lst[nbins];
+      constexpr int UD = kResGrp / NT;
+#pragma unroll
+      for (int u = 0; u < UD; u++) {
+        const int i = u * NT + tid;
+        if (i < len) {
+          const int b = ct.stb[k][i];
+          if (!(b & 1)) a.ws[ct.cnt[b] + (uint32_t)i - lst[b]] = ct.stk[k][i];
+        }
+      }
+      __syncthreads();
+    }
   }
-  if (tid == 0) sm.upre[nbins] = 0;
+  SR_RES_STAMP(5);
+  grid.sync();
+
+  // ================= E: bucket sorts and equality fills =================
+  // Units: CTA units first (range buckets above WCAP: one CTA each, in-shared-
+  // memory partition + warp sorts), then warp units (range buckets <= WCAP:
+  // one warp's register network; equality fills of kResWarpFill keys).  Every
+  // CTA derives both lists from the bucket starts, so no hand-off is needed.
+  if (a.tstamp && c == 0 && tid == 0) a.tstamp[2] = res_now();
+  constexpr int WCAP = SM::WCAP;
+  int nbig = 0;
+  {  // unit counts per bin -> exclusive prefixes (each thread scans BPT consecutive bins)
+    constexpr int BPT = (SM::NB1 + 1 + NT - 1) / NT;
+    uint32_t ca[BPT], cb[BPT], sa = 0, sb = 0;
+#pragma unroll
+    for (int r = 0; r < BPT; r++) {
+      const int b = tid * BPT + r;
+      const uint32_t cnt = b < nbins ? start[b + 1] - start[b] : 0u;
+      const bool rng = b < nbins && !(b & 1);
+      ca[r] = rng && cnt > (uint32_t)(WCAP / 2) && cnt <= (uint32_t)WCAP;
+      cb[r] = b >= nbins ? 0u : (b & 1) ? (cnt + kResWarpFill - 1) / kResWarpFill : (cnt > 0 && cnt <= (uint32_t)(WCAP / 2));
+      nbig += rng && cnt > (uint32_t)WCAP;
+      sa += ca[r];
+      sb += cb[r];
+    }
+    uint32_t ta, tb;
+    uint32_t* red = reinterpret_cast<uint32_t*>(sm.red);
+    uint32_t pa = block_exclusive_sum<NT>(sa, red, &ta);
+    uint32_t pb = block_exclusive_sum<NT>(sb, red, &tb);
+#pragma unroll
+    for (int r = 0; r < BPT; r++) {
+      const int b = tid * BPT + r;
+      if (b <= nbins) {
+        sm.upa[b] = (uint16_t)pa;
+        sm.upb[b] = (uint16_t)pb;
+      }
+      pa += ca[r];
+      pb += cb[r];
+    }
+  }
   __syncthreads();
-  smem_scan<NT>(sm.upre, nbins + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  int NC = 0;
+  if (__syncthreads_or(nbig)) {  // compact the big buckets (bucket order) into cbin
+    constexpr int BPT = (SM::NB1 + NT - 1) / NT;
+    int f = 0;
+    for (int r = 0; r < BPT; r++) {
+      const int b = tid * BPT + r;
+      f += b < nbins && !(b & 1) && start[b + 1] - start[b] > (uint32_t)WCAP;
+    }
+    int tot;
+    int o = block_exclusive_sum<NT>(f, sm.red, &tot);
+    for (int r = 0; r < BPT; r++) {
+      const int b = tid * BPT + r;
+      if (b < nbins && !(b & 1) && start[b + 1] - start[b] > (uint32_t)WCAP) {
+        sm.cbin[o] = (uint16_t)b;
+        o++;
+      }
+    }
+    NC = tot;
+    __syncthreads();
+  }
   if (c == 0) {  // statistics
     long long noneq = 0, eqk = 0;
     for (int b = tid; b < nbins; b += NT) {
@@ -585,103 +959,111 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     if (tid == 0) {
       a.st->noneq_total = noneq;
       a.st->eq_keys = eqk;
-      a.st->n_items = sm.upre[nbins];
+      a.st->n_items = (int64_t)sm.upa[nbins] + sm.upb[nbins] + NC;
     }
   }
-  SR_RES_STAMP(5);
-  const uint32_t UE = sm.upre[nbins];
   __shared__ uint32_t s_unit;
-  for (;;) {  // units handed out dynamically (bucket sizes vary)
-    if (tid == 0) s_unit = atomicAdd(a.unit_counter, 1u);
-    __syncthreads();
-    const uint32_t u = s_unit;
-    __syncthreads();
-    if (u >= UE) break;
-    int lo = 0, hi = nbins - 1;  // last bin with upre <= u
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sm.upre[mid] <= u) lo = mid; else hi = mid - 1;
-    }
-    const int b = lo;
-    const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
-    if (b & 1) {  // equality bucket: fill
-      const K key = sm.tree1[B1MAX + (b - 1) / 2];
-      const int f0 = (int)(u - sm.upre[b]) * kResFill;
-      const int f1 = f0 + kResFill < len ? f0 + kResFill : len;
-      for (int i = f0 + tid; i < f1; i += NT) a.keys[s + i] = key;
-      continue;
-    }
-    // gather the bucket's per-tile pieces (tile t: ws[t*T + mlst[t][b], + mcnt[t][b])):
-    // piece metadata in shared memory, then each warp copies every 16th piece
-    // with all of its lanes' loads issued before the stores
-    typename SM::E& e = sm.u.e;
-    const unsigned long long tg0 = (a.tstamp && c == 0 && tid == 0) ? res_now() : 0;
-    const bool fits = len <= a.capb;
-    for (int t = tid; t < a.NG; t += NT) {
-      e.piece[t] = __ldcg(a.mcnt + (size_t)t * nbins + b);
-      e.pbase[t] = (uint32_t)t * (uint32_t)kResGrp + __ldcg(a.mlst + (size_t)t * nbins + b);
-    }
-    if (tid == 0) e.piece[a.NG] = 0;
-    __syncthreads();
-    smem_scan<NT>(e.piece, a.NG + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
-    K* gdst = fits ? e.x : a.keys + s;  // too large for one CTA: gathered unsorted into its final range
-    {
-      constexpr int PB = 8;  // pieces per warp in flight
-      for (int t0 = w; t0 < a.NG; t0 += kResWarps * PB) {
-        K v[PB];
-        int dpos[PB];
+  typename SM::E& e = sm.u.e;
+  if (NC > 0) {
+    for (;;) {  // CTA units, handed out dynamically
+      if (tid == 0) s_unit = atomicAdd(a.unit_counter, 1u);
+      __syncthreads();
+      const uint32_t u = s_unit;
+      __syncthreads();
+      if (u >= (uint32_t)NC) break;
+      // a big bucket beyond the in-kernel cap: copied unsorted into its final
+      // range and listed for the host's next level
+      const int b = (int)sm.cbin[u];
+      const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
+      const unsigned long long tg0 = (a.tstamp && c == 0 && tid == 0) ? res_now() : 0;
+      const bool fits = len <= a.capb;
+      K* gdst = fits ? e.x : a.keys + s;
+      {
+        constexpr int UL = 8;
+        for (int i0 = 0; i0 < len; i0 += NT * UL) {
+          K v[UL];
 #pragma unroll
-        for (int k = 0; k < PB; k++) {
-          const int t = t0 + k * kResWarps;
-          dpos[k] = -1;
-          if (t < a.NG) {
-            const int po = (int)e.piece[t], pl = (int)(e.piece[t + 1] - e.piece[t]);
-            if (lane < pl) {
-              v[k] = __ldcg(a.ws + e.pbase[t] + lane);
-              dpos[k] = po + lane;
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < PB; k++)
-          if (dpos[k] >= 0) gdst[dpos[k]] = v[k];
-      }
-      for (int t = w; t < a.NG; t += kResWarps) {  // pieces longer than a warp (presorted inputs)
-        const int po = (int)e.piece[t], pl = (int)(e.piece[t + 1] - e.piece[t]);
-        for (int i0 = 32; i0 < pl; i0 += 32 * PB) {
-          K v[PB];
-#pragma unroll
-          for (int k = 0; k < PB; k++) {
-            const int i = i0 + k * 32 + lane;
-            v[k] = i < pl ? __ldcg(a.ws + e.pbase[t] + i) : K(0);
+          for (int uu = 0; uu < UL; uu++) {
+            const int i = i0 + uu * NT + tid;
+            v[uu] = i < len ? __ldcg(a.ws + s + i) : K(0);
           }
 #pragma unroll
-          for (int k = 0; k < PB; k++) {
-            const int i = i0 + k * 32 + lane;
-            if (i < pl) gdst[po + i] = v[k];
+          for (int uu = 0; uu < UL; uu++) {
+            const int i = i0 + uu * NT + tid;
+            if (i < len) gdst[i] = v[uu];
           }
         }
       }
-    }
-    __syncthreads();
-    if (!fits) {
-      if (tid == 0) {
-        const unsigned long long k = atomicAdd((unsigned long long*)&a.st->n_ovf, 1ull);
-        OvfSeg o;
-        o.start = s;
-        o.len = len;
-        a.ovf[k] = o;
-        atomicAdd((unsigned long long*)&a.st->ovf_keys, (unsigned long long)len);
+      __syncthreads();
+      if (!fits) {
+        if (tid == 0) {
+          const unsigned long long k = atomicAdd((unsigned long long*)&a.st->n_ovf, 1ull);
+          OvfSeg o;
+          o.start = s;
+          o.len = len;
+          a.ovf[k] = o;
+          atomicAdd((unsigned long long*)&a.st->ovf_keys, (unsigned long long)len);
+        }
+        continue;
       }
-      continue;
+      unsigned long long* prof = (a.tstamp && c == 0) ? a.tstamp + 8 + 8 * (size_t)P : nullptr;
+      if (prof && tid == 0) { prof[5] += res_now() - tg0; prof[7] += 1; }
+      res_bucket_sort2<K, NT>(a.keys + s, len, e, prof);
+      __syncthreads();
     }
-    unsigned long long* prof = (a.tstamp && c == 0) ? a.tstamp + 8 + 8 * (size_t)P : nullptr;
-    if (prof && tid == 0) { prof[5] += res_now() - tg0; prof[7] += 1; }
-    res_bucket_sort<K, NT>(a.keys + s, len, e, prof);
-    __syncthreads();
+  }
+  {  // warp units
+    // largest first (class A), so that the last units handed out are short
+    const uint32_t UA = sm.upa[nbins], UW = UA + sm.upb[nbins];
+    K* stage = e.x + w * WCAP;  // x and y are adjacent: kResWarps * WCAP keys
+    for (;;) {
+      uint32_t u = 0;
+      if (lane == 0) u = atomicAdd(a.unit_counter + 2, 1u);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= UW) break;
+      const uint16_t* up = u < UA ? sm.upa : sm.upb;
+      const uint32_t v = u < UA ? u : u - UA;
+      int lo = 0, hi = nbins - 1;  // last bin with up <= v
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (up[mid] <= v) lo = mid; else hi = mid - 1;
+      }
+      const int b = lo;
+      const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
+      if (b & 1) {  // equality bucket: fill
+        const K key = sm.tree1[B1MAX + (b - 1) / 2];
+        const int f0 = (int)(v - up[b]) * kResWarpFill;
+        const int f1 = f0 + kResWarpFill < len ? f0 + kResWarpFill : len;
+        for (int i = f0 + lane; i < f1; i += 32) a.keys[s + i] = key;
+        continue;
+      }
+      {  // coalesced load into the warp's staging area
+        constexpr int UL = 8;
+        for (int i0 = 0; i0 < len; i0 += 32 * UL) {
+          K v[UL];
+#pragma unroll
+          for (int uu = 0; uu < UL; uu++) {
+            const int i = i0 + uu * 32 + lane;
+            v[uu] = i < len ? __ldcg(a.ws + s + i) : K(0);
+          }
+#pragma unroll
+          for (int uu = 0; uu < UL; uu++) {
+            const int i = i0 + uu * 32 + lane;
+            if (i < len) stage[i] = v[uu];
+          }
+        }
+      }
+      __syncwarp();
+      int unsorted = 0;  // is_sorted
+      for (int i = lane; i + 1 < len; i += 32) unsorted |= stage[i + 1] < stage[i];
+      if (__any_sync(0xffffffffu, unsorted)) res_warp_sort<K, WCAP>(stage, len);
+      for (int i = lane; i < len; i += 32) a.keys[s + i] = stage[i];
+      __syncwarp();
+    }
   }
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[3] = res_now();
   SR_RES_STAMP(6);
+  res_exit(a);
 }
 
 }  // namespace sr

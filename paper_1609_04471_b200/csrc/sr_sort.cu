@@ -10,6 +10,7 @@
 //   long natural runs     -> MERGE if its simulated bytes beat PARTITION
 //   otherwise             -> PARTITION (levels until every bucket <= kCap)
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -61,11 +62,16 @@ struct ThreadState {
   size_t up_bytes = 0;
   cudaEvent_t up_done = nullptr;
   bool up_pending = false;
+  // host-mapped completion record of the resident kernel (resident.cuh ResDone)
+  sr::ResDone* done_h = nullptr;
+  sr::ResDone* done_d = nullptr;
+  uint32_t done_seq = 0;
   ~ThreadState() {
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
     if (up) cudaFreeHost(up);
     if (up_done) cudaEventDestroy(up_done);
+    if (done_h) cudaFreeHost(done_h);
   }
 };
 thread_local ThreadState t_state;
@@ -245,6 +251,33 @@ struct Ctx {
     if (!ts.up_done) cudaEventCreateWithFlags(&ts.up_done, cudaEventDisableTiming);
     cudaEventRecord(ts.up_done, st);  // the next call reuses the staging area once this copy is done
     ts.up_pending = true;
+  }
+  // Wait for a kernel's host-mapped completion record (spin; the stream is
+  // polled now and then so that a failed or lost launch cannot hang the host).
+  DevStats await_done(const sr::ResDone* d, uint32_t seq) {
+    auto t0 = std::chrono::steady_clock::now();
+    t_enqueue += std::chrono::duration<double>(t0 - t_mark).count();
+    for (uint32_t spin = 1;; spin++) {
+      if (d->seq == seq) break;
+      if ((spin & 1023) == 0) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) {
+          if (d->seq == seq) break;
+          fail(SR_ERR_INTERNAL, "resident kernel finished without its completion record");
+        }
+        if (e != cudaErrorNotReady) check_cuda(e, "resident kernel");
+        // watchdog: a sort of <= 2^22 keys takes well under a millisecond
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+          fail(SR_ERR_CUDA, "resident kernel did not complete within 20 s");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    DevStats r;
+    std::memcpy(&r, (const void*)&d->st, sizeof(DevStats));
+    plan.host_syncs++;
+    t_mark = std::chrono::steady_clock::now();
+    t_wait += std::chrono::duration<double>(t_mark - t0).count();
+    return r;
   }
   // Readback of `bytes` from device into pinned memory + synchronise (the planner's host sync).
   double t_enqueue = 0, t_wait = 0;  // host seconds (SR_TIMING diagnostics)
@@ -947,26 +980,32 @@ struct Sorter {
     if (HAS_V || !g_resident || n <= kCap || n > ResCfg<K>::MAXN) return false;
     if (g_force_route == SR_ROUTE_MERGE && !nested) return false;  // forced merge: the multi-kernel planner
     const int P = resident_grid();
-    return P >= 16;
+    // every CTA holds <= GPC tiles, the samplers one
+    return P >= 16 && n <= (int64_t)(ResSmem<K>::GPC * P - kResSamplers) * kResGrp;
   }
 
   void run_resident() {
     c.plan.n = n;
-    const int64_t T = choose_tile(n);
-    const int64_t G = ceil_div<int64_t>(n, T);
+    const int64_t T = choose_tile(n);  // L_min of the run detection (R5)
     const int P = resident_grid();
-    if (T != kResTile) fail(SR_ERR_INTERNAL, "resident tile mismatch");
+    // scan / grouping tile: a multiple of the CTA width, sized so that every
+    // CTA gets <= GPC tiles and the last kResSamplers CTAs (the samplers) one
+    // (each held tile costs a pass over the bucket tables: as few per CTA as fit)
+    const int64_t gpc = std::min<int64_t>(ResSmem<K>::GPC, ceil_div<int64_t>(n, (int64_t)(P - kResSamplers) * kResGrp));
+    const int64_t slots = gpc * P - kResSamplers;
+    const int64_t tile = std::min<int64_t>(kResGrp, ceil_div<int64_t>(ceil_div<int64_t>(n, slots), kResNT) * kResNT);
+    const int64_t G = ceil_div<int64_t>(n, tile);
     constexpr int CAPB = ResCfg<K>::CAPB;
-    const int B1 = (int)std::min<int64_t>(ResCfg<K>::B1MAX, std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(n, CAPB / 4))));
-    const int NG = (int)ceil_div<int64_t>(n, kResGrp);
-    const int S1 = B1 * kResO1;
+    const int B1 = (int)std::min<int64_t>(ResCfg<K>::B1MAX, std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(n, ResCfg<K>::TARGET))));
+    const int NG = (int)G;
+    const int S1 = B1 * ResCfg<K>::O1;
     const int nbins = 2 * B1 + 1;
     const int64_t n_ovf = B1 + 1;
-    if (NG > kResMaxNG) fail(SR_ERR_INTERNAL, "resident group count");
+    if (NG > slots || G > kResMaxG) fail(SR_ERR_INTERNAL, "resident tile count");
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
       c.reserve((size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
-                         r(S1 * kw) + 2 * r(4 * (int64_t)NG * nbins) + r(16 * n_ovf) + 8 * 256));
+                         r(S1 * kw) + r(16 * n_ovf) + r(4 * (int64_t)NG * nbins) + 8 * 256));
     }
     hostprof("reserved");
     ensure_ws();
@@ -974,25 +1013,32 @@ struct Sorter {
     a.keys = keys;
     a.ws = wk;
     a.n = n;
-    a.tile = (int)T;
+    a.tile = (int)tile;
     a.G = (int)G;
     a.sums = c.alloc<TileSummary>(G);
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
-    {  // control block: statistics + unit counter + bucket totals, zeroed together
+    {  // control block: statistics + unit/done counters + bucket totals, zeroed by the kernel
       const size_t bytes = sizeof(DevStats) + 16 + 4 * (size_t)nbins;
       unsigned char* cb = c.alloc<unsigned char>((int64_t)bytes);
-      c.memset0(cb, bytes);
       a.st = reinterpret_cast<DevStats*>(cb);
       a.unit_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
       a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 16);
+      a.ctrl_words = (int)(bytes / 4);
     }
+    ThreadState& ts = t_state;
+    if (!ts.done_h) {
+      check_cuda(cudaHostAlloc((void**)&ts.done_h, sizeof(ResDone), cudaHostAllocMapped), "cudaHostAlloc(mapped)");
+      check_cuda(cudaHostGetDevicePointer((void**)&ts.done_d, ts.done_h, 0), "cudaHostGetDevicePointer");
+      ts.done_h->seq = 0;
+    }
+    a.done = ts.done_d;
+    a.seq = ++ts.done_seq == 0 ? ++ts.done_seq : ts.done_seq;
     a.S1 = S1;
     a.B1 = B1;
     a.samp = c.alloc<K>(S1);
+    a.goff = c.alloc<uint32_t>((int64_t)NG * nbins);
     a.NG = NG;
-    a.mcnt = c.alloc<uint32_t>((int64_t)NG * nbins);
-    a.mlst = c.alloc<uint32_t>((int64_t)NG * nbins);
     a.ovf = c.alloc<OvfSeg>(n_ovf);
     a.lmin = T;
     a.force = forced();
@@ -1001,8 +1047,8 @@ struct Sorter {
     a.merge_ok = route_ok() | kOutlierStrict;
     a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
-    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P + 8) : nullptr;
-    if (stamps) c.memset0(a.tstamp, 64 * (P + 2));
+    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P + 16) : nullptr;
+    if (stamps) c.memset0(a.tstamp, 64 * (P + 3));
     const size_t smem = sizeof(ResSmem<K>);
     hostprof("prepared");
     const int h = c.launch("resident", n * kw, [&] {
@@ -1010,16 +1056,22 @@ struct Sorter {
       check_cuda(cudaLaunchCooperativeKernel((void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
     hostprof("launched");
-    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(a.st, sizeof(DevStats)));
+    DevStats hs = c.await_done(ts.done_h, a.seq);
     hostprof("read back");
     if (stamps) {
-      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 2)));
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 3)));
+      {
+        const unsigned long long* q = t + 8 + 8 * P + 8;
+        if (q[0] && q[5])
+          fprintf(stderr, "[sr_resident] C group0 us: classify %.1f count %.1f tables+atomics %.1f scan %.1f scatter %.1f\n",
+                  (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3, (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3);
+      }
       {
         const unsigned long long* e = t + 8 + 8 * P;
-        fprintf(stderr, "[sr_resident] CTA0 %llu buckets, us: gather %.1f is_sorted+pad %.1f runs %.1f merges %.1f\n",
+        fprintf(stderr, "[sr_resident] CTA0 %llu buckets, us: load %.1f is_sorted+sample %.1f classify+move %.1f warp sorts %.1f\n",
                 e[7], e[5] * 1e-3, e[0] * 1e-3, e[1] * 1e-3, e[2] * 1e-3);
       }
-      static const char* what[8] = {"A.scan", "A.end", "C.route", "C.tree", "C.end", "E.start", "E.end", "-"};
+      static const char* what[8] = {"A.scan", "A.end", "C.route", "C.tree", "C.end", "D.end", "E.end", "-"};
       for (int k = 0; k < 7; k++) {
         std::vector<double> v;
         for (int q = 0; q < P; q++)
@@ -1050,11 +1102,9 @@ struct Sorter {
         c.plan.route = SR_ROUTE_PARTITION;
         c.plan.levels = 2;  // the global level and the in-CTA level
         c.plan.equal_keys += hs.eq_keys;
-        // scan (read) + grouping (read, written to the workspace by tile, bucket
-        // tables written) + bucket sorts (range keys gathered and written, tables
-        // read) + equality fills (written)
-        c.replan(h, n * kw + 2 * n * kw + 2 * hs.noneq_total * kw + hs.eq_keys * kw +
-                        2 * 2 * 4 * (int64_t)NG * nbins);
+        // scan (read) + classification (read) + range keys written to their
+        // buckets in ws, read back and written sorted + equality fills (written)
+        c.replan(h, 2 * n * kw + 3 * hs.noneq_total * kw + hs.eq_keys * kw);
         if (hs.n_ovf > 0) {  // ranges left unsorted in keys (beyond the in-kernel caps): further levels
           const OvfSeg* o = reinterpret_cast<const OvfSeg*>(c.readback(a.ovf, sizeof(OvfSeg) * hs.n_ovf));
           std::vector<OvfSeg> next(o, o + hs.n_ovf);
