@@ -133,6 +133,83 @@ __device__ __forceinline__ void warp_neighbours(K x, K h1, K h2, int lane, K& ne
   if (lane == 0) prev = h1;
 }
 
+// Running H1 statistics of one thread (reduced over the CTA by the caller).
+struct ScanAcc {
+  int cd = 0, ca = 0, cv = 0;                       // descents, descending-run breaks, straddle violations
+  int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;  // first / last descent, first / last break
+};
+
+// H1 over the pairs (i, i+1), i in [t0, t1), with 16-byte vector loads: each
+// thread owns V = 16 / sizeof(K) consecutive keys per vector, so V - 1 of its
+// pairs are in registers and only three shuffles per vector reach the
+// neighbours (lane 0 / lane 31 load the halo across warps).  The per-pair
+// flags become bit masks; counts are popcounts and first / last positions
+// come from ffs / clz once per vector.  Requires keys 16-byte aligned and
+// t0 a multiple of V; keys beyond n are never read.
+template <typename K, bool STRICT, int NT, int R>
+__device__ __forceinline__ void scan_range_vec(const K* __restrict__ keys, int64_t n, int64_t t0, int64_t t1,
+                                               ScanAcc& acc) {
+  constexpr int V = 16 / (int)sizeof(K);
+  const int tid = threadIdx.x & (NT - 1), lane = threadIdx.x & 31;
+  for (int64_t vb = t0 / V; vb * V < t1; vb += (int64_t)NT * R) {
+    K x[R][V], hp[R], hn0[R], hn1[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t i0 = (vb + (int64_t)r * NT + tid) * V;
+      if (i0 + V <= n) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(keys + i0));
+        memcpy(&x[r][0], &v, 16);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; j++) x[r][j] = i0 + j < n ? keys[i0 + j] : K(0);
+      }
+      hp[r] = (lane == 0 && i0 >= 1 && i0 - 1 < n) ? keys[i0 - 1] : K(0);
+      hn0[r] = (lane == 31 && i0 + V < n) ? keys[i0 + V] : K(0);
+      hn1[r] = (lane == 31 && i0 + V + 1 < n) ? keys[i0 + V + 1] : K(0);
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t i0 = (vb + (int64_t)r * NT + tid) * V;
+      K e[V + 3];  // e[0] = a[i0-1], e[1 .. V] = the vector, e[V+1], e[V+2] = a[i0+V], a[i0+V+1]
+      e[0] = __shfl_up_sync(0xffffffffu, x[r][V - 1], 1);
+      e[V + 1] = __shfl_down_sync(0xffffffffu, x[r][0], 1);
+      e[V + 2] = __shfl_down_sync(0xffffffffu, x[r][1], 1);
+      if (lane == 0) e[0] = hp[r];
+      if (lane == 31) { e[V + 1] = hn0[r]; e[V + 2] = hn1[r]; }
+#pragma unroll
+      for (int j = 0; j < V; j++) e[j + 1] = x[r][j];
+      // valid pairs: i < t1 and i + 1 < n
+      const int64_t lim64 = (t1 < n - 1 ? t1 : n - 1) - i0;
+      const int lim = lim64 <= 0 ? 0 : (lim64 >= V ? V : (int)lim64);
+      const unsigned valid = (1u << lim) - 1u;
+      unsigned dm = 0, am = 0, sm = 0;
+#pragma unroll
+      for (int j = 0; j < V; j++) {
+        const K a = e[j + 1], b = e[j + 2];
+        dm |= (unsigned)(b < a) << j;
+        am |= (unsigned)(STRICT ? !(b < a) : (a < b)) << j;
+        // straddle: a[i-1] > a[i+2], defined for 1 <= i and i + 2 < n
+        const bool inr = (j > 0 || i0 >= 1) && (i0 + j + 2 < n);
+        sm |= (unsigned)(inr && e[j] > e[j + 3]) << j;
+      }
+      dm &= valid;
+      am &= valid;
+      sm &= dm;
+      acc.cd += __popc(dm);
+      acc.ca += __popc(am);
+      acc.cv += __popc(sm);
+      if (dm) {
+        acc.fd = min(acc.fd, (int)i0 + __ffs(dm) - 1);
+        acc.ld = max(acc.ld, (int)i0 + 31 - __clz(dm));
+      }
+      if (am) {
+        acc.fa = min(acc.fa, (int)i0 + __ffs(am) - 1);
+        acc.la = max(acc.la, (int)i0 + 31 - __clz(am));
+      }
+    }
+  }
+}
+
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
 // break rule: a_i <= a_{i+1} (pairs: only strictly descending runs may be
 // reversed, "the reversely sorted subsequence cannot contain equal
@@ -165,6 +242,11 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   }
   int cd = 0, ca = 0, cv = 0;
   int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
+  if (!FUSE && (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0) {
+    ScanAcc acc;
+    scan_range_vec<K, STRICT, NT, (sizeof(K) == 4 ? 2 : 4)>(keys, n, t0, t1, acc);
+    cd = acc.cd; ca = acc.ca; cv = acc.cv; fd = acc.fd; ld = acc.ld; fa = acc.fa; la = acc.la;
+  } else
   for (int64_t base = t0; base < t1; base += NT * U) {
     K x[U], h1[U], h2[U];
 #pragma unroll
@@ -516,25 +598,31 @@ __global__ void __launch_bounds__(NT) k_reverse(K* __restrict__ keys, uint32_t* 
     c0 = ((int64_t)blockIdx.x - chunk_prefix[r]) * CH;
   }
   const int64_t half = len / 2;
-  K a[U], b[U];
-  uint32_t va[U], vb[U];
+  // the whole-array launch is grid-strided (a bounded grid keeps the gated,
+  // speculative launch cheap when another route is taken)
+  const int64_t stride = ranges ? INT64_MAX : (int64_t)gridDim.x * CH;
+  for (; c0 < half; c0 += stride) {
+    K a[U], b[U];
+    uint32_t va[U], vb[U];
 #pragma unroll
-  for (int u = 0; u < U; u++) {
-    int64_t p = c0 + u * NT + threadIdx.x;
-    if (p < half) {
-      a[u] = keys[s + p];
-      b[u] = keys[s + len - 1 - p];
-      if (HAS_V) { va[u] = vals[s + p]; vb[u] = vals[s + len - 1 - p]; }
+    for (int u = 0; u < U; u++) {
+      int64_t p = c0 + u * NT + threadIdx.x;
+      if (p < half) {
+        a[u] = keys[s + p];
+        b[u] = keys[s + len - 1 - p];
+        if (HAS_V) { va[u] = vals[s + p]; vb[u] = vals[s + len - 1 - p]; }
+      }
     }
-  }
 #pragma unroll
-  for (int u = 0; u < U; u++) {
-    int64_t p = c0 + u * NT + threadIdx.x;
-    if (p < half) {
-      keys[s + p] = b[u];
-      keys[s + len - 1 - p] = a[u];
-      if (HAS_V) { vals[s + p] = vb[u]; vals[s + len - 1 - p] = va[u]; }
+    for (int u = 0; u < U; u++) {
+      int64_t p = c0 + u * NT + threadIdx.x;
+      if (p < half) {
+        keys[s + p] = b[u];
+        keys[s + len - 1 - p] = a[u];
+        if (HAS_V) { vals[s + p] = vb[u]; vals[s + len - 1 - p] = va[u]; }
+      }
     }
+    if (stride == INT64_MAX) break;
   }
 }
 

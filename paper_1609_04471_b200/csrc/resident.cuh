@@ -592,6 +592,11 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
     int cd = 0, ca = 0, cv = 0;
     int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
+    if ((reinterpret_cast<uintptr_t>(a.keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0) {
+      ScanAcc acc;
+      scan_range_vec<K, false, NT, (sizeof(K) == 4 ? 4 : 8)>(a.keys, n, t0, t1, acc);
+      cd = acc.cd; ca = acc.ca; cv = acc.cv; fd = acc.fd; ld = acc.ld; fa = acc.fa; la = acc.la;
+    } else
     for (int64_t base = t0; base < t1; base += NT * UA) {
       K x[UA], h1[UA], h2[UA];
 #pragma unroll

@@ -395,7 +395,7 @@ struct Sorter {
     K* kk = keys;
     uint32_t* vv = vals;
     if (ranges.size() == 1 && ranges[0].start == 0 && ranges[0].len == n) {  // whole array: no upload
-      const int64_t blocks = std::max<int64_t>(1, ceil_div<int64_t>(n / 2, CH));
+      const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n / 2, CH)));
       const int64_t nn = n;
       return c.launch("reverse", 2 * n * (kw + vw), [&] {
         k_reverse<K, HAS_V, NT><<<(unsigned)blocks, NT, 0, c.st>>>(kk, vv, nullptr, nullptr, 0, gate, nn);
