@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
 }
 
 // ---------------------------------------------------------------------------
-// K11w (keys only): every warp finishes whole items of up to 32*VT keys with
+// K11w (keys only): every warp finishes whole items of (min_len, 32*VT] keys with
 // the warp-register bitonic sort: coalesced load into the warp's staging
 // area, is_sorted check, sort, coalesced store into the
 // caller's keys.  Fills (equality buckets) are written here too.
@@ -741,7 +741,8 @@ template <typename K, int VT, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS) k_finish_warp(const Item* __restrict__ items,
                                                              const int64_t* __restrict__ count_ptr, K* __restrict__ keys,
                                                              const K* __restrict__ ws_k,
-                                                             const DevStats* __restrict__ gate, int64_t gate_route) {
+                                                             const DevStats* __restrict__ gate, int64_t gate_route,
+                                                             int min_len, int fills) {
   if (gate && gate->route != gate_route) return;  // speculative launch on another route
   using WB = WarpBitonic<K, VT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -755,10 +756,14 @@ __global__ void __launch_bounds__(32 * WARPS) k_finish_warp(const Item* __restri
     const int len = item.len;
     K* dk = keys + s;
     if ((item.kind & 0xf) == kItemFill) {
+      if (!fills) continue;
       const K key = (K)item.key;
       for (int i = lane; i < len; i += 32) dk[i] = key;
       continue;
     }
+    // size class of this launch: (min_len, 32 VT] (narrow networks use fewer
+    // registers, so the common small items run at a higher occupancy)
+    if (len <= min_len || len > 32 * VT) continue;
     const K* sk = (from_ws ? ws_k : keys) + s;
     // all loads in flight at once (striped, coalesced), then stage in smem
     {

@@ -315,7 +315,9 @@ constexpr int kFinSmallNT = 128;                         // K11 small items (pai
 constexpr int kWarpItemsPerCta = 4;                      // K11w (keys only): warps per CTA
 constexpr int kPackKeys = 128;                           // keys only: buckets <= this are packed into items
 constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
-constexpr int kScatKNT = 1024, kScatKVT = 8;             // K10 (keys only)
+constexpr int kScatKNT = 1024;                           // K10 (keys only)
+template <typename K>
+constexpr int scat_kvt() { return sizeof(K) == 4 ? 16 : 8; }  // 16K-key (int32) / 8K-key (int64) sub-tiles
 constexpr int kScanNT1 = 1024;                           // K1
 constexpr int kCountNT = 1024;                           // K8
 constexpr int64_t kAtomicMaxEntries = 2 << 20;  // keys-only count-matrix threshold (entries)
@@ -622,9 +624,9 @@ struct Sorter {
     const int64_t noneq = hs ? hs->noneq_total : keys_in;
     const DevStats* gate = hs ? nullptr : L.d_st;
     if (!HAS_V) {
-      using SM = ScatterKeysSmem<K, kScatKNT, kScatKVT>;
+      using SM = ScatterKeysSmem<K, kScatKNT, scat_kvt<K>()>;
       size_t smem = sizeof(SM);
-      auto kern = k_scatter_keys<K, kScatKNT, kScatKVT>;
+      auto kern = k_scatter_keys<K, kScatKNT, scat_kvt<K>()>;
       set_smem(kern, smem);
       return c.launch("scatter", keys_in * kw + noneq * kw, [&] {
         kern<<<(unsigned)L.total_chunks, kScatKNT, smem, c.st>>>(sk, dk, L.d_segs, L.d_chunk_seg, L.chunk_size,
@@ -648,24 +650,30 @@ struct Sorter {
   // keys only: the small list (items <= 32*kWarpVT keys, and fills) goes to the
   // warp-register kernel
   template <int VT>
-  int finish_warp(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
+  int finish_warp(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate, int min_len, int fills,
+                  int max_grid) {
     constexpr int W = kWarpItemsPerCta;
     auto kern = k_finish_warp<K, VT, W>;
     const size_t smem = sizeof(K) * 32 * VT * W;
     set_smem(kern, smem);
-    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(max_items, W), gate ? 148 * 6 : 148 * 32);
+    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(max_items, W), gate ? 148 * 6 : max_grid);
     K* kk = keys;
     const K* wkk = wk;
     const int64_t* cnt = &L.d_st->n_items;
     return c.launch("finish_small", bytes, [&] {
-      kern<<<grid, 32 * W, smem, c.st>>>(L.d_items, cnt, kk, wkk, gate, kRoutePartition);
+      kern<<<grid, 32 * W, smem, c.st>>>(L.d_items, cnt, kk, wkk, gate, kRoutePartition, min_len, fills);
     });
   }
+  // keys only: two launches over the small item list, by size class -- items
+  // <= 512 keys (and fills) with the 16-key-per-lane network, larger ones with
+  // the widest network the level allows
   int finish_small(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
     if (HAS_V) return finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, max_items, bytes, gate, kRoutePartition);
     if (max_items <= 0) return -1;
-    if (L.warp_vt == 64 && sizeof(K) == 4) return finish_warp<64>(L, max_items, bytes, gate);
-    return finish_warp<32>(L, max_items, bytes, gate);
+    const int h = finish_warp<16>(L, max_items, bytes, gate, 0, 1, 148 * 64);
+    if (L.warp_vt == 64 && sizeof(K) == 4) finish_warp<64>(L, max_items, 0, gate, 512, 0, 148 * 16);
+    else finish_warp<32>(L, max_items, 0, gate, 512, 0, 148 * 16);
+    return h;
   }
 
   int level_finish(Level& L, const DevStats* hs) {
