@@ -234,6 +234,50 @@ __global__ void __launch_bounds__(NT) k_sample_sort(const K* __restrict__ src, c
 }
 
 // ---------------------------------------------------------------------------
+// Vectorised key loads for the count / scatter passes: thread t takes the
+// G = U / 4 groups of 4 consecutive positions s0 + 4 (g NT + t) .. + 3, with
+// s0 = sub rounded down to a multiple of 4 (16-byte int32 / 32-byte int64
+// vectors when the base is aligned; scalar loads at the array end).
+// Positions outside [lo, hi) are loaded as 0 and reported invalid.  The
+// partition passes are order-agnostic within a sub-tile (keys only), so the
+// position <-> thread map only has to be the same for the keys and their
+// bucket ids.
+template <typename K, int U, int NT>
+__device__ __forceinline__ uint32_t load_keys_vec4(const K* __restrict__ src, int64_t s0, int64_t lo, int64_t hi,
+                                                   K (&x)[U]) {
+  static_assert(U % 4 == 0 && U <= 32, "");
+  uint32_t valid = 0;
+#pragma unroll
+  for (int g = 0; g < U / 4; g++) {
+    const int64_t p0 = s0 + 4 * ((int64_t)g * NT + threadIdx.x);
+    if (p0 >= lo && p0 + 4 <= hi) {
+      if (sizeof(K) == 4) {
+        const int4 v = *reinterpret_cast<const int4*>(src + p0);
+        memcpy(&x[4 * g], &v, 16);
+      } else {
+        const int4 v0 = reinterpret_cast<const int4*>(src + p0)[0], v1 = reinterpret_cast<const int4*>(src + p0)[1];
+        memcpy(&x[4 * g], &v0, 16);
+        memcpy(&x[4 * g + 2], &v1, 16);
+      }
+      valid |= 0xfu << (4 * g);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const bool ok = p0 + j >= lo && p0 + j < hi;
+        x[4 * g + j] = ok ? src[p0 + j] : K(0);
+        valid |= (uint32_t)ok << (4 * g + j);
+      }
+    }
+  }
+  return valid;
+}
+// position of slot u of load_keys_vec4
+template <int NT>
+__device__ __forceinline__ int64_t vec4_pos(int64_t s0, int u) {
+  return s0 + 4 * ((int64_t)(u >> 2) * NT + threadIdx.x) + (u & 3);
+}
+
+// ---------------------------------------------------------------------------
 // K8: bucket histogram of one chunk (levels >= 2; level 1 fuses it into K1).
 template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const SegDesc* __restrict__ segs,
@@ -258,22 +302,48 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
   load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, s_spl, s_eq);
   for (int b = threadIdx.x; b < seg.nbins; b += NT) s_hist[b] = 0;
   __syncthreads();
+  build_guide<K>(s_spl + kMaxBuckets, m, csm.guide);
+  __syncthreads();
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
-  for (int64_t base = c0; base < c1; base += NT * U) {
+  const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(bins_out) & 7) == 0;
+  for (int64_t base = vec ? (c0 & ~int64_t(3)) : c0; base < c1; base += NT * U) {
     K x[U];
+    uint32_t valid = 0;
+    if (vec) {
+      valid = load_keys_vec4<K, U, NT>(src, base, c0, c1, x);
+    } else {
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      int64_t i = base + u * NT + threadIdx.x;
-      x[u] = i < c1 ? src[i] : K(0);
+      for (int u = 0; u < U; u++) {
+        const int64_t i = base + u * NT + threadIdx.x;
+        x[u] = i < c1 ? src[i] : K(0);
+        valid |= (uint32_t)(i < c1) << u;
+      }
     }
     int bin[U];
-    classify_keys<K, U>(x, bin, s_spl, s_eq, m, depth);
+    classify_keys_guided<K, U>(x, bin, s_spl + kMaxBuckets, s_eq, csm.guide);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int64_t i = base + u * NT + threadIdx.x;
-      hist_add(s_hist, bin[u], i < c1);
-      if (bins_out && i < c1) bins_out[i] = (uint16_t)bin[u];  // reused by the scatter
+    for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], (valid >> u) & 1);
+    if (bins_out) {  // reused by the scatter
+      if (vec) {
+#pragma unroll
+        for (int g = 0; g < U / 4; g++) {
+          const int64_t p0 = vec4_pos<NT>(base, 4 * g);
+          if (((valid >> (4 * g)) & 0xf) == 0xf) {
+            const uint2 w = make_uint2((uint32_t)bin[4 * g] | ((uint32_t)bin[4 * g + 1] << 16),
+                                       (uint32_t)bin[4 * g + 2] | ((uint32_t)bin[4 * g + 3] << 16));
+            *reinterpret_cast<uint2*>(bins_out + p0) = w;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+              if ((valid >> (4 * g + j)) & 1) bins_out[p0 + j] = (uint16_t)bin[4 * g + j];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; u++)
+          if ((valid >> u) & 1) bins_out[base + u * NT + threadIdx.x] = (uint16_t)bin[u];
+      }
     }
   }
   __syncthreads();
@@ -680,24 +750,26 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
   if (!bins_in) load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
+  // (scalar loads: 16-byte vector loads and evict-first hints measured slower here)
   for (int64_t sub = c0; sub < c1; sub += ST) {
     for (int b = tid; b < nb; b += NT) sm.cnt[b] = 0;
     __syncthreads();
     K x[VTS];
     int bin[VTS];
     uint32_t rk[VTS];
+    uint32_t valid = 0;
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
-      int64_t pos = sub + i * NT + tid;
-      x[i] = pos < c1 ? src[pos] : K(0);
-      if (bins_in) bin[i] = pos < c1 ? (int)bins_in[pos] : 0;
+      const int64_t p = sub + i * NT + tid;
+      x[i] = p < c1 ? src[p] : K(0);
+      if (bins_in) bin[i] = p < c1 ? (int)bins_in[p] : 0;
+      valid |= (uint32_t)(p < c1) << i;
     }
     if (!bins_in) classify_keys<K, VTS>(x, bin, sm.spl, sm.eq, m, depth);
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
-      int64_t pos = sub + i * NT + tid;
       // range buckets only; equality buckets are filled later
-      if (pos >= c1 || (bin[i] & 1)) bin[i] = -1;
+      if (!((valid >> i) & 1) || (bin[i] & 1)) bin[i] = -1;
       else rk[i] = atomicAdd(&sm.cnt[bin[i]], 1u);
     }
     __syncthreads();

@@ -86,12 +86,101 @@ __device__ __forceinline__ void load_splitters_smem(const K* spl, const uint8_t*
   }
 }
 
+// Guide table for the classification: the sorted splitters' order-preserving
+// unsigned images u(t) are covered by kGuideCells equal cells of width
+// 2^shift starting at u(t_0); tab[c] = #{t_j : u(t_j) < u(t_0) + c 2^shift}.
+// A key's bucket #{t_j < x} then lies in [tab[c], tab[c+1]] for its cell c and
+// is found by bisecting that (usually tiny) range of the sorted splitters --
+// the same lower_bound as the tree walk, with a few shared-memory loads
+// instead of depth ones.
+constexpr int kGuideCells = 4096;
+struct Guide {
+  uint64_t u0, u1;  // u(t_0), u(t_{m-1})
+  int shift, m;
+  uint16_t tab[kGuideCells + 1];
+};
+
+template <typename K>
+__device__ __forceinline__ uint64_t key_u(K x) {  // order-preserving unsigned image
+  return sizeof(K) == 4 ? (uint64_t)((uint32_t)x ^ 0x80000000u) : ((uint64_t)x ^ 0x8000000000000000ull);
+}
+
+// All threads: the guide of the m sorted splitters spl[0, m) (shared memory).
+template <typename K>
+__device__ __forceinline__ void build_guide(const K* spl, int m, Guide& g) {
+  if (m <= 0) {
+    if (threadIdx.x == 0) { g.m = 0; g.shift = 0; g.u0 = 0; g.u1 = 0; }
+    return;
+  }
+  const uint64_t u0 = key_u<K>(spl[0]), u1 = key_u<K>(spl[m - 1]);
+  const uint64_t span = u1 - u0;
+  int shift = 0;
+  while (shift < 64 && (span >> shift) >= (uint64_t)kGuideCells) shift++;
+  for (int c = threadIdx.x; c <= kGuideCells; c += blockDim.x) {
+    int r;
+    if (c == 0) r = 0;
+    else if (c == kGuideCells || (uint64_t)c > (span >> shift)) r = m;  // the cell start lies beyond u1
+    else {
+      const uint64_t v = u0 + ((uint64_t)c << shift);
+      int lo = 0, hi = m;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_u<K>(spl[mid]) < v) lo = mid + 1; else hi = mid;
+      }
+      r = lo;
+    }
+    g.tab[c] = (uint16_t)r;
+  }
+  if (threadIdx.x == 0) { g.u0 = u0; g.u1 = u1; g.shift = shift; g.m = m; }
+}
+
+// Bucket ids of U keys through the guide (sorted splitters at spl): lockstep
+// bisection over the per-key ranges, then the 3-way id 2 i + [x equals an
+// equality splitter].  Same result as classify_keys.
+template <typename K, int U>
+__device__ __forceinline__ void classify_keys_guided(const K (&x)[U], int (&bin)[U], const K* spl, const uint8_t* eqf,
+                                                     const Guide& g) {
+  const int m = g.m;
+  const uint64_t u0 = g.u0, u1 = g.u1;
+  const int shift = g.shift;
+  int lo[U], hi[U];
+  int span = 0;
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const uint64_t v = key_u<K>(x[u]);
+    if (v <= u0) { lo[u] = 0; hi[u] = 0; }          // x <= t_0
+    else if (v > u1) { lo[u] = m; hi[u] = m; }      // x > t_{m-1}
+    else {
+      const int c = (int)((v - u0) >> shift);
+      lo[u] = g.tab[c];
+      hi[u] = g.tab[c + 1];
+    }
+    span = max(span, hi[u] - lo[u]);
+  }
+  while (span > 0) {  // interval lengths at least halve every step
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (lo[u] < hi[u]) {
+        const int mid = (lo[u] + hi[u]) >> 1;
+        if (spl[mid] < x[u]) lo[u] = mid + 1; else hi[u] = mid;
+      }
+    }
+    span >>= 1;
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int i = lo[u];
+    bin[u] = 2 * i + ((i < m && spl[i] == x[u] && eqf[i]) ? 1 : 0);
+  }
+}
+
 // Shared memory of the histogram passes (K1 fused, K8): dynamic, > 48 KB for int64.
 template <typename K>
 struct ClassifySmem {
   K tree[2 * kMaxBuckets];
   uint32_t hist[kMaxBins];
   uint8_t eq[kMaxBuckets];
+  Guide guide;
 };
 
 // Shared-memory histogram increment (hardware-serialised on conflicts).
