@@ -131,17 +131,21 @@ NCU_NAMES = {"presort_scan": "k_presort_scan", "presort_resolve": "k_presort_res
              "merge": "k_merge<", "scan": "k_scan_u32", "resident": "k_resident"}
 
 
-def ncu_traffic(kernel: str, dtype_name: str):
+def ncu_traffic(kernel: str, dtype_name: str, workload: str):
     """DRAM read+write bytes per launch of `kernel` from the newest committed
-    ncu --set full summary (profiles/*_ncu_summary.json), else None."""
+    ncu --set full summary of the same workload (profiles/*_ncu_summary.json,
+    "workload" field), else None."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
     pref = NCU_NAMES.get(kernel)
     for f in reversed(files):
         try:
-            full = json.load(open(f)).get("full", {})
+            summ = json.load(open(f))
         except Exception:
             continue
+        if summ.get("workload") != workload:
+            continue
+        full = summ.get("full", {})
         for name, d in full.items():
             if pref and name.startswith(pref) and f"<{dtype_name}" in name.replace(" ", ""):
                 r, w = d.get("dram_bytes_read") or 0, d.get("dram_bytes_write") or 0
@@ -357,7 +361,7 @@ def main():
     bytes_per_launch = d["bytes"] / d["launches"]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     kern_total = sum(v["ms"] for v in kern.values())
-    tr = ncu_traffic(dname, "int" if dtype == np.int32 else "long")
+    tr = ncu_traffic(dname, "int" if dtype == np.int32 else "long", wl)
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": tr["bytes"] if tr else None,
                 "traffic_source": tr, "algorithmic_bytes_per_launch": int(bytes_per_launch),

@@ -4,7 +4,8 @@ kernel, from --metrics gpu__time_duration.sum) and the --set full capture
 import csv, collections, json, subprocess, sys
 
 tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
-out = {"tag": tag, "launch_list": {}, "full": {}}
+workload = sys.argv[4] if len(sys.argv) > 4 else None  # bench --workload the captures belong to
+out = {"tag": tag, "workload": workload, "launch_list": {}, "full": {}}
 rows = list(csv.reader(open(launches)))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 h = rows[hi]; ix = {k: i for i, k in enumerate(h)}
@@ -23,7 +24,8 @@ for k, d in sorted(per.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"])
                              "dram_write_MB": round(d.get("dram__bytes_write.sum", 0) / 1e6, 3)}
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(raw.splitlines())); H = rr[0]; U = rr[1]; IX = {k: i for i, k in enumerate(H)}
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+         "ns": 1e-3, "us": 1, "ms": 1e3}
 def f(r, k):
     try:
         v = float(r[IX[k]].replace(",", ""))
