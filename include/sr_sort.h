@@ -29,7 +29,14 @@
 extern "C" {
 #endif
 
-enum { SR_INT32 = 0, SR_INT64 = 1 }; /* key dtype; values are 4-byte opaque payloads */
+/* Key dtype; values are 4-byte opaque payloads.  SR_INT32 / SR_INT64: signed
+ * numeric order.  SR_FLOAT32 / SR_FLOAT64 (sr_sort_keys, sr_sort_pairs,
+ * sr_sort_host only, the paper's "random double"
+ * class): IEEE 754 totalOrder -- -NaN (larger payload first) <
+ * -inf < negative < -0 < +0 < positive < +inf < +NaN (larger payload last);
+ * keys equal in that order are bit-identical, so the output is unique.  The
+ * float sort costs two extra in-place passes over the keys (fkeys.cuh). */
+enum { SR_INT32 = 0, SR_INT64 = 1, SR_FLOAT32 = 2, SR_FLOAT64 = 3 };
 
 enum {
   SR_OK = 0,
@@ -57,8 +64,8 @@ enum {
 
 /* ------------------------------------------------------------------ sort */
 
-/* Sort keys[0..n) ascending in place.  dtype: SR_INT32 / SR_INT64.  keys must
- * be aligned to the key size.  Work is enqueued on `stream`; the call blocks
+/* Sort keys[0..n) ascending in place.  dtype: SR_INT32 / SR_INT64 /
+ * SR_FLOAT32 / SR_FLOAT64.  keys must be aligned to the key size.  Work is enqueued on `stream`; the call blocks
  * the host on small statistics readbacks (one for sorted / reversed /
  * single-level inputs) and returns before the GPU finishes; synchronise the
  * stream before reading keys.  Scratch: about n*(key bytes) + O(n/8) bytes,
@@ -122,7 +129,8 @@ int32_t sr_set_option(int32_t key, int64_t value);
 int32_t sr_last_profile(const char **names, float *ms, int64_t *bytes, int32_t cap);
 
 /* ------------------------------------------------------------------ step-level entry points
- * One per hot-path row; used by the parity tests.  All are
+ * One per hot-path row; used by the parity tests.  Integer
+ * dtypes only (SR_ERR_UNSUPPORTED_DTYPE otherwise).  All are
  * synchronous (they synchronise `stream` before returning) and take device
  * pointers for array data and host pointers for small results. */
 

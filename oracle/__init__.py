@@ -61,6 +61,8 @@ def lib():
         L.or_count.restype = c64
         L.or_stable_rank.argtypes = [vp, c64, ci, c64]
         L.or_stable_rank.restype = c64
+        L.or_sort_float.argtypes = [vp, vp, c64, ci]
+        L.or_sort_float.restype = ci
         _lib = L
     return _lib
 
@@ -77,10 +79,17 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+def _fs(a: np.ndarray) -> int:
+    return {np.dtype(np.float32): 4, np.dtype(np.float64): 8}.get(a.dtype, 0)
+
+
 def sort_keys(keys: np.ndarray) -> np.ndarray:
-    """Ascending signed sort (plain stable mergesort). Returns a new array."""
+    """Ascending sort (plain stable mergesort): signed order for integers,
+    IEEE 754 totalOrder for float32/float64.  Returns a new array."""
     out = np.ascontiguousarray(keys).copy()
-    if lib().or_sort(_p(out), None, out.size, _ks(out)) != 0:
+    rc = lib().or_sort_float(_p(out), None, out.size, _fs(out)) if _fs(out) else \
+        lib().or_sort(_p(out), None, out.size, _ks(out))
+    if rc != 0:
         raise MemoryError("oracle sort: out of host memory")
     return out
 
@@ -90,7 +99,8 @@ def sort_pairs(keys: np.ndarray, vals: np.ndarray):
     k = np.ascontiguousarray(keys).copy()
     v = np.ascontiguousarray(vals).view(np.uint32).copy()
     assert k.size == v.size
-    if lib().or_sort(_p(k), _p(v), k.size, _ks(k)) != 0:
+    rc = lib().or_sort_float(_p(k), _p(v), k.size, _fs(k)) if _fs(k) else lib().or_sort(_p(k), _p(v), k.size, _ks(k))
+    if rc != 0:
         raise MemoryError("oracle sort: out of host memory")
     return k, v.view(vals.dtype)
 

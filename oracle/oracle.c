@@ -40,10 +40,16 @@
  *                      (e): presortedness not disturbed)
  *   or_count           #{x < v}, #{x <= v}  (rank) for sampled checks
  *   or_stable_rank     #{j: k_j < k_i} + #{j < i: k_j = k_i}
+ *   or_sort_float      the same stable mergesort over float32 / float64 keys
+ *                      ordered by IEEE 754-2008 §5.10 totalOrder, written out
+ *                      case by case from that definition (the paper's
+ *                      "random double" class; SURVEY.md §8(f)
+ *                      NEXT #2)
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 typedef struct {
     int64_t key;
@@ -294,4 +300,88 @@ int64_t or_stable_rank(const void *keys, int64_t n, int ks, int64_t i) {
         r += (x < v) || (x == v && j < i);
     }
     return r;
+}
+
+/* ---- floating-point keys: IEEE 754 totalOrder ("double") -------- */
+
+typedef struct {
+    double v;        /* numeric value (exact for float32) */
+    uint64_t raw;    /* the key's bit pattern (float32 widened unsigned) */
+    uint64_t pay;    /* NaN: the magnitude bits (quiet bit + payload) */
+    int neg, nan;
+    uint32_t val;
+} frec_t;
+
+/* totalOrder(a, b), i.e. "a <= b", from its definition:
+ *  - a negative sign orders first (this includes -0 < +0 and -NaN < all);
+ *  - same sign, neither NaN: numeric order;
+ *  - same sign, one NaN: a positive NaN is above every number, a negative NaN
+ *    below every number;
+ *  - same sign, both NaN: positive NaNs ascend with their magnitude bits
+ *    (signalling below quiet, then payload), negative NaNs descend. */
+static int tot_le(const frec_t *a, const frec_t *b) {
+    if (a->neg != b->neg) return a->neg;
+    if (!a->nan && !b->nan) return a->v <= b->v;
+    if (a->nan && b->nan) return a->neg ? a->pay >= b->pay : a->pay <= b->pay;
+    if (a->nan) return a->neg;   /* -NaN <= everything; +NaN <= nothing but NaNs */
+    return !b->neg;              /* b is NaN: +NaN above a, -NaN below a */
+}
+
+static void fmerge(const frec_t *a, int64_t na, const frec_t *b, int64_t nb, frec_t *out) {
+    int64_t i = 0, j = 0, k = 0;
+    while (i < na && j < nb) {
+        if (tot_le(&a[i], &b[j])) out[k++] = a[i++]; /* A wins ties: stable */
+        else out[k++] = b[j++];
+    }
+    while (i < na) out[k++] = a[i++];
+    while (j < nb) out[k++] = b[j++];
+}
+
+static void fmsort(frec_t *a, frec_t *tmp, int64_t lo, int64_t hi) {
+    if (hi - lo <= 1) return;
+    int64_t mid = lo + (hi - lo) / 2;
+    fmsort(a, tmp, lo, mid);
+    fmsort(a, tmp, mid, hi);
+    fmerge(a + lo, mid - lo, a + mid, hi - mid, tmp + lo);
+    memcpy(a + lo, tmp + lo, (size_t)(hi - lo) * sizeof(frec_t));
+}
+
+/* keys: float32 (fs=4) or float64 (fs=8), sorted in place by totalOrder; vals
+ * (may be NULL) travel with their keys; equal keys keep their input order. */
+int or_sort_float(void *keys, uint32_t *vals, int64_t n, int fs) {
+    if (n <= 1) return 0;
+    frec_t *r = (frec_t *)malloc((size_t)n * sizeof(frec_t));
+    frec_t *tmp = (frec_t *)malloc((size_t)n * sizeof(frec_t));
+    if (!r || !tmp) { free(r); free(tmp); return -1; }
+    for (int64_t i = 0; i < n; i++) {
+        if (fs == 4) {
+            float f; uint32_t u;
+            memcpy(&f, (const char *)keys + 4 * i, 4);
+            memcpy(&u, &f, 4);
+            r[i].v = (double)f;
+            r[i].raw = u;
+            r[i].neg = (int)(u >> 31);
+            r[i].nan = isnan(f) ? 1 : 0;
+            r[i].pay = u & 0x7fffffu;
+        } else {
+            double d; uint64_t u;
+            memcpy(&d, (const char *)keys + 8 * i, 8);
+            memcpy(&u, &d, 8);
+            r[i].v = d;
+            r[i].raw = u;
+            r[i].neg = (int)(u >> 63);
+            r[i].nan = isnan(d) ? 1 : 0;
+            r[i].pay = u & 0xfffffffffffffull;
+        }
+        r[i].val = vals ? vals[i] : (uint32_t)i;
+    }
+    fmsort(r, tmp, 0, n);
+    for (int64_t i = 0; i < n; i++) {
+        if (fs == 4) { uint32_t u = (uint32_t)r[i].raw; memcpy((char *)keys + 4 * i, &u, 4); }
+        else memcpy((char *)keys + 8 * i, &r[i].raw, 8);
+        if (vals) vals[i] = r[i].val;
+    }
+    free(r);
+    free(tmp);
+    return 0;
 }

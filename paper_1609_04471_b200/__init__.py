@@ -14,7 +14,7 @@ import numpy as np
 
 from . import build as _build
 
-SR_INT32, SR_INT64 = 0, 1
+SR_INT32, SR_INT64, SR_FLOAT32, SR_FLOAT64 = 0, 1, 2, 3  # include/sr_sort.h
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "size out of range", 4: "misaligned pointer",
           5: "out of device memory", 6: "CUDA error", 7: "internal error"}
 ROUTES = {0: "none", 1: "sorted", 2: "reversed", 3: "merge", 4: "partition", 5: "tile", 6: "outlier"}
@@ -96,7 +96,11 @@ def _dtype_code(t) -> int:
         return SR_INT32
     if t.dtype == torch.int64:
         return SR_INT64
-    raise TypeError(f"keys must be int32 or int64, got {t.dtype}")
+    if t.dtype == torch.float32:
+        return SR_FLOAT32
+    if t.dtype == torch.float64:
+        return SR_FLOAT64
+    raise TypeError(f"keys must be int32, int64, float32 or float64, got {t.dtype}")
 
 
 def _stream(t):
@@ -124,7 +128,8 @@ def _vals_ok(v):
 # ----------------------------------------------------------------------------- sort
 
 def sort_keys(keys):
-    """Sort a CUDA int32/int64 tensor ascending in place (sr_sort_keys)."""
+    """Sort a CUDA int32/int64 (signed order) or float32/float64 (IEEE totalOrder)
+    tensor ascending in place (sr_sort_keys)."""
     _dev(keys, "keys")
     _check(lib().sr_sort_keys(_ptr(keys), keys.numel(), _dtype_code(keys), _stream(keys)))
     return keys
@@ -143,12 +148,11 @@ def sort_pairs(keys, vals):
 
 def sort_host(keys: np.ndarray, vals: np.ndarray | None = None, stream: int = 0):
     """End-to-end sort of HOST numpy arrays in place (sr_sort_host)."""
-    if keys.dtype == np.int32:
-        code = SR_INT32
-    elif keys.dtype == np.int64:
-        code = SR_INT64
-    else:
-        raise TypeError("keys must be int32 or int64")
+    codes = {np.dtype(np.int32): SR_INT32, np.dtype(np.int64): SR_INT64,
+             np.dtype(np.float32): SR_FLOAT32, np.dtype(np.float64): SR_FLOAT64}
+    if keys.dtype not in codes:
+        raise TypeError("keys must be int32, int64, float32 or float64")
+    code = codes[keys.dtype]
     assert keys.flags.c_contiguous and (vals is None or (vals.flags.c_contiguous and vals.itemsize == 4))
     vp = None if vals is None else vals.ctypes.data_as(ctypes.c_void_p)
     _check(lib().sr_sort_host(keys.ctypes.data_as(ctypes.c_void_p), vp, keys.size, code, ctypes.c_void_p(stream)))

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/sr_sort.h"
+#include "fkeys.cuh"
 #include "merge.cuh"
 #include "outlier.cuh"
 #include "partition.cuh"
@@ -1468,12 +1469,15 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+bool dtype_ok(int32_t dtype) { return dtype == SR_INT32 || dtype == SR_INT64 || dtype == SR_FLOAT32 || dtype == SR_FLOAT64; }
+int64_t key_bytes(int32_t dtype) { return (dtype == SR_INT32 || dtype == SR_FLOAT32) ? 4 : 8; }
+
 int32_t validate(const void* keys, const void* vals, int64_t n, int32_t dtype, bool pairs) {
   if (n < 0) return SR_ERR_INVALID_ARGUMENT;
-  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (!dtype_ok(dtype)) return SR_ERR_UNSUPPORTED_DTYPE;
   if (n > INT32_MAX) return SR_ERR_SIZE;
   if (n <= 1) return SR_OK;
-  const int64_t kw = dtype == SR_INT32 ? 4 : 8;
+  const int64_t kw = key_bytes(dtype);
   if (!keys || (pairs && !vals)) return SR_ERR_INVALID_ARGUMENT;
   if ((uintptr_t)keys % kw) return SR_ERR_ALIGNMENT;
   if (pairs && (uintptr_t)vals % 4) return SR_ERR_ALIGNMENT;
@@ -1516,12 +1520,29 @@ int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream
     c.plan.n = n;
     if (n <= 1) return;
     init_pool();
-    if (dtype == SR_INT32) {
+    // floating-point keys: totalOrder -> signed integer order, in place, and
+    // back after the integer sort (fkeys.cuh)
+    const bool fl = dtype == SR_FLOAT32 || dtype == SR_FLOAT64;
+    const bool w4 = key_bytes(dtype) == 4;
+    auto flip = [&]() {
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n, 256 * 4)));
+      c.launch("fkey_flip", 2 * n * key_bytes(dtype), [&] {
+        if (w4) k_fkey_flip<int32_t><<<grid, 256, 0, c.st>>>((int32_t*)keys, n);
+        else k_fkey_flip<int64_t><<<grid, 256, 0, c.st>>>((int64_t*)keys, n);
+      });
+    };
+    if (fl) flip();
+    if (w4) {
       if (pairs) Sorter<int32_t, true>(c, (int32_t*)keys, (uint32_t*)vals, n).run();
       else Sorter<int32_t, false>(c, (int32_t*)keys, nullptr, n).run();
     } else {
       if (pairs) Sorter<int64_t, true>(c, (int64_t*)keys, (uint32_t*)vals, n).run();
       else Sorter<int64_t, false>(c, (int64_t*)keys, nullptr, n).run();
+    }
+    if (fl) {  // the integer sort's launches count in the plan; the flips are added
+      const int launches = c.plan.launches;
+      flip();
+      c.plan.launches = launches + 1;
     }
   });
 }
@@ -1541,11 +1562,11 @@ int32_t sr_sort_pairs(void* keys, void* vals, int64_t n, int32_t dtype, void* st
 
 int32_t sr_sort_host(void* host_keys, void* host_vals, int64_t n, int32_t dtype, void* stream) {
   if (n < 0) return SR_ERR_INVALID_ARGUMENT;
-  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (!dtype_ok(dtype)) return SR_ERR_UNSUPPORTED_DTYPE;
   if (n > INT32_MAX) return SR_ERR_SIZE;
   if (n <= 1) return SR_OK;
   if (!host_keys) return SR_ERR_INVALID_ARGUMENT;
-  const int64_t kw = dtype == SR_INT32 ? 4 : 8;
+  const int64_t kw = key_bytes(dtype);
   cudaStream_t st = (cudaStream_t)stream;
   void *dk = nullptr, *dv = nullptr;
   int32_t rc = guarded([&] {

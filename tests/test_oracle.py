@@ -345,3 +345,72 @@ def test_count_and_stable_rank():
     assert oracle.count(k, 3) == (1, 3)
     assert oracle.count(k, 5) == (3, 6)
     assert [oracle.stable_rank(k, i) for i in range(6)] == _stable_positions(k.tolist())
+
+
+# ---- floating-point keys: IEEE 754 totalOrder --------
+
+def test_float_golden_total_order(golden_dir):
+    """F8: hand-ordered special values, keys and stable payloads (golden fixture)."""
+    d = _golden(golden_dir, "F8_float_total_order.json")
+    k = np.array([int(x, 16) for x in d["input_bits"]], np.uint32).view(np.float32)
+    exp = np.array([int(x, 16) for x in d["expected_bits"]], np.uint32)
+    assert np.array_equal(oracle.sort_keys(k).view(np.uint32), exp)
+    kk, vv = oracle.sort_pairs(k, np.array(d["pairs_vals"], np.uint32))
+    assert np.array_equal(kk.view(np.uint32), exp)
+    assert vv.tolist() == d["expected_vals"]
+    # the same special values as float64
+    k64 = k.astype(np.float64)  # NaN payloads widen; signs, zeros, infinities keep their order
+    o64 = oracle.sort_keys(k64)
+    assert np.isnan(o64[:3]).all() and np.signbit(o64[:3]).all() and np.isnan(o64[-3:]).all()
+    assert o64[3] == -np.inf and o64[-4] == np.inf
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_float_finite_matches_numpy(dtype):
+    """Finite keys without zeros: totalOrder is numeric order (numpy's sort)."""
+    k = gen.make_float("funiform", 5000, dtype, config=97) - dtype(0.5)
+    k = k[k != 0]
+    assert np.array_equal(oracle.sort_keys(k), np.sort(k))
+    b = gen.make_float("fbits", 5000, dtype, config=97)
+    b = b[np.isfinite(b) & (b != 0)]
+    assert np.array_equal(oracle.sort_keys(b), np.sort(b))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_float_random_bits_properties(dtype):
+    """Random bit patterns (all classes): a permutation of the input bits,
+    negative signs first, numeric order inside each sign class, NaNs outside."""
+    it = np.uint32 if dtype == np.float32 else np.uint64
+    k = gen.make_float("fbits", 20000, dtype, config=98)
+    k[:64] = gen.make_float("fspecial", 64, dtype, config=98)
+    o = oracle.sort_keys(k)
+    assert np.array_equal(np.sort(o.view(it)), np.sort(k.view(it)))
+    sb = np.signbit(o)
+    assert not np.any(sb[1:] & ~sb[:-1])  # no negative after a positive
+    for part in (o[sb], o[~sb]):
+        fin = part[~np.isnan(part)]
+        assert np.all(fin[1:] >= fin[:-1])
+        nanpos = np.flatnonzero(np.isnan(part))
+        if nanpos.size:  # negative NaNs lead, positive NaNs trail
+            if np.signbit(part[0]):
+                assert nanpos.tolist() == list(range(nanpos.size))
+            else:
+                assert nanpos.tolist() == list(range(part.size - nanpos.size, part.size))
+    # -0 before +0, each zero class contiguous
+    z = np.flatnonzero(o == 0)
+    if z.size:
+        zs = np.signbit(o[z])
+        assert not np.any(zs[1:] & ~zs[:-1])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_float_pairs_stable(dtype):
+    """Stability with ties (payload = input index): equal bit patterns keep input order."""
+    it = np.uint32 if dtype == np.float32 else np.uint64
+    k = gen.make_float("fspecial", 3000, dtype, config=99)
+    v = np.arange(k.size, dtype=np.uint32)
+    ok, ov = oracle.sort_pairs(k, v)
+    assert np.array_equal(ok.view(it), k.view(it)[ov])
+    same = ok.view(it)[1:] == ok.view(it)[:-1]
+    assert np.all(ov[1:][same] > ov[:-1][same])
+    assert np.array_equal(oracle.sort_keys(k).view(it), ok.view(it))

@@ -252,6 +252,45 @@ def make(order: str, n: int, dtype=np.int32, config: int = 0, instance: int = 0)
     raise KeyError(order)
 
 
+# ---- floating-point keys (the paper's "random double"
+# class).  Orders: "fbits" = uniformly random bit patterns (every
+# class: normals, subnormals, +-0, +-inf, NaNs with payloads, both signs);
+# "funiform" = uniform [0, 1) from the top 53 (24) bits of a draw (the paper's
+# random doubles); "fspecial" = a mix drawn from the special values and a few
+# ordinary numbers, with many ties; "fsorted" / "freversed" = ramps.
+FLOAT_ORDERS = {"fbits": 32, "funiform": 33, "fspecial": 34, "fsorted": 35, "freversed": 36}
+
+
+def make_float(order: str, n: int, dtype=np.float64, config: int = 0, instance: int = 0) -> np.ndarray:
+    dtype = np.dtype(dtype)
+    assert dtype in (np.float32, np.float64)
+    s = seed_for(config, FLOAT_ORDERS[order], instance)
+    d = draws(s, n)
+    if order == "fbits":
+        return (d >> np.uint64(32)).astype(np.uint32).view(np.float32) if dtype == np.float32 else d.view(np.float64)
+    if order == "funiform":
+        if dtype == np.float64:
+            return (d >> np.uint64(11)).astype(np.float64) * 2.0**-53
+        return ((d >> np.uint64(40)).astype(np.float64) * 2.0**-24).astype(np.float32)
+    if order == "fspecial":
+        it = np.uint32 if dtype == np.float32 else np.uint64
+        if dtype == np.float32:
+            bits = [0x7fc00000, 0x7fc00001, 0x7f800001, 0xffc00000, 0xffc00001, 0xff800001, 0x7f800000, 0xff800000,
+                    0x00000000, 0x80000000, 0x00000001, 0x80000001, 0x3f800000, 0xbf800000, 0x7f7fffff, 0xff7fffff]
+        else:
+            bits = [0x7ff8000000000000, 0x7ff8000000000001, 0x7ff0000000000001, 0xfff8000000000000,
+                    0xfff8000000000001, 0xfff0000000000001, 0x7ff0000000000000, 0xfff0000000000000,
+                    0x0, 0x8000000000000000, 0x1, 0x8000000000000001, 0x3ff0000000000000, 0xbff0000000000000,
+                    0x7fefffffffffffff, 0xffefffffffffffff]
+        table = np.array(bits, dtype=it).view(dtype)
+        return table[uniform_below(d, len(table))]
+    if order == "fsorted":
+        return np.arange(n, dtype=dtype) * dtype.type(0.5) - dtype.type(n // 4)
+    if order == "freversed":
+        return (np.arange(n, dtype=dtype) * dtype.type(0.5) - dtype.type(n // 4))[::-1].copy()
+    raise KeyError(order)
+
+
 def index_payload(n: int) -> np.ndarray:
     """configs[3]: payload = original index (int32, stored as 4-byte opaque)."""
     return np.arange(n, dtype=np.uint32)
