@@ -328,6 +328,8 @@ constexpr int kMergeNV = kMergeNT * kMergeVT;
 static_assert(2 * kFinNT * kFinVT == kCap, "finishing item must equal kCap");
 static_assert(kFinSmallNT * kFinVT == kSmallItem, "small finishing tile");
 
+constexpr int64_t kBigLevel1 = int64_t(64) << 20;
+constexpr int64_t kBigLevel1Buckets = 512;
 int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
   int64_t t = pow2ceil(std::max<int64_t>(1, n / 512));
   return std::min<int64_t>(65536, std::max<int64_t>(8192, t));
@@ -336,6 +338,11 @@ int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
 // below (those buckets are finished by one warp with 32 keys per lane).
 int choose_buckets(int64_t len, int level = 1) {
   int64_t b = pow2ceil(ceil_div<int64_t>(len, level > 1 ? kTargetBucket / 4 : kTargetBucket));
+  // very large arrays: fewer, larger level-1 buckets, so that the level-1
+  // scatter writes runs of >= 32 keys per 16K-key sub-tile (full DRAM sectors;
+  // shorter runs cost read-modify-writes) and the level-2 scatter writes stay
+  // within a few L2-resident segments
+  if (level == 1 && len >= kBigLevel1) b = std::min<int64_t>(b, kBigLevel1Buckets);
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
