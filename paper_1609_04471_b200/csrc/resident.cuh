@@ -1,41 +1,44 @@
 // resident.cuh -- the resident path: the whole keys-only sort of an L2-resident
-// array (kCap < n <= kResMaxN) as ONE cooperative launch of one CTA per SM.
+// array (kCap < n <= (GPC * 148 - 4) * kResGrp) as ONE cooperative launch of
+// one CTA per SM.
 //
 // The multi-kernel path (presort.cuh, partition.cuh) pays a launch plus a
 // drain per step and a one-CTA bookkeeping kernel per level; at the paper's
 // Table 1 size (n = 2,000,000) a full pass over the keys is
 // ~1.2 us of HBM time, so those fixed costs dominated.  Here the steps run as
-// three phases of one persistent kernel separated by two grid-wide barriers,
-// and the quicksort recursion (Appendix B) is two levels of
-// splitter partitioning: a global one over <= 1024 buckets, then each bucket
-// is sorted by one CTA in shared memory.
-//   A  H1 scan of every presort tile (same tiles and TileSummary as K1).
-//      Meanwhile the last two CTAs (they scan the fewest tiles) each gather
-//      and sort one half of the level-1 sample (S1 = 8 B1 jittered
+// four phases of one persistent kernel separated by three grid-wide barriers,
+// and the quicksort recursion (Appendix B) is a global
+// splitter partition into <= 2048 buckets followed by per-warp (or, for big
+// buckets, per-CTA) sorts of the buckets.
+//   A  H1 scan of every tile (vectorised, presort.cuh scan_range_vec); CTA 0
+//      zeroes the control block.  The last four CTAs (one tile each) gather
+//      and sort one quarter each of the level-1 sample (S1 = O1 B1 jittered
 //      positions, R8).
 //   -- grid sync --
-//   C  every CTA resolves the tile summaries into the device route (K2's
-//      logic; CTA 0 also writes the statistics and run lists).  SORTED exits
-//      (PAPER.md:167); REVERSED reverses in place; MERGE /
-//      undecided return to the host planner.  PARTITION: splitters t_j =
-//      element 8(j+1) of the two merged halves (merge-path selection), with
-//      their gamma flags (count > gamma = 2 in the sample; R9)
-//      -> Eytzinger tree; each tile is classified
-//      (3-way ids) and written to the same span of the
-//      workspace grouped by bucket (a tile-local counting sort: contiguous,
-//      coalesced writes), with its per-bucket counts and local starts; the
-//      bucket totals are accumulated with atomics.
+//   C  warp 0 resolves the tile summaries into the device route (K2's logic;
+//      CTA 0 also writes the statistics and run lists) while the other warps
+//      merge the sample quarters pairwise.  SORTED exits;
+//      REVERSED reverses in place; MERGE / undecided
+//      return to the host planner.  PARTITION: splitter j = element O1 (j+1)
+//      of the merged halves (merge-path selection, R14) with its gamma flag
+//      (count > gamma = 2 in the sample) -> Eytzinger tree; each
+//      held tile is classified (3-way ids) and counting-
+//      sorted by bucket in shared memory; its piece offset inside every bucket
+//      comes from one atomicAdd on the bucket total.
 //   -- grid sync --
-//   E  bucket starts = exclusive scan of the totals (every CTA).  Units:
-//      equality buckets are filled ("spared from the recursive calls",
-//      PAPER.md:158); a range bucket is gathered from its per-tile pieces
-//      into shared memory by one CTA, checked with is_sorted,
-//      and sorted there: 128-key runs by 16-lane register bitonic networks
-//      (the insertion-sort-below-alpha step), then merge-path
-//      merge rounds (the mergesort levels of §3, A wins ties),
-//      the last one writing the output.  Buckets beyond CAPB keys are
-//      gathered unsorted into their final range and listed for the host,
-//      which runs further partition levels on them.
+//   D  bucket starts (exclusive scan of the totals, every CTA); every held
+//      key goes to start[b] + offset + rank in the workspace, so each bucket
+//      is contiguous; equality keys are not written.
+//   -- grid sync --
+//   E  CTA units: range buckets above WCAP, one CTA each, partitioned in
+//      shared memory into 16 sub-buckets that the warps sort (R17); then warp
+//      units, largest first: range buckets <= WCAP sorted by one warp's
+//      register bitonic network (R15), and equality fills ("spared from the
+//      recursive calls").  Every bucket is checked with
+//      is_sorted first.  Buckets beyond the in-kernel cap are
+//      copied unsorted into their final range and listed for the host, which
+//      runs further partition levels on them.
+//   The last CTA to exit publishes the statistics to a host-mapped record.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstddef>
@@ -235,32 +238,6 @@ __device__ __forceinline__ void res_classify(const K (&x)[U], int (&bin)[U], con
     const int i = j[u] - (1 << depth);
     bin[u] = 2 * i + ((i < m && tree[BMAX + i] == x[u] && eq[i]) ? 1 : 0);
   }
-}
-
-// Rank of sample q in s[0, S): #{s_j < x} + #{s_j == x, j < q} (its position in
-// the stably sorted sample), computed by GL lanes over strided j and reduced.
-template <typename K, int GL>
-__device__ __forceinline__ int res_rank(const K* s, int S, int q, int gl) {
-  const K x = s[q];
-  int r = 0;
-  for (int j = gl; j < S; j += GL) {
-    const K y = s[j];
-    r += (y < x) || (y == x && j < q);
-  }
-#pragma unroll
-  for (int o = GL / 2; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  return r;
-}
-
-// Splitter j = sorted[(j+1) o] with the gamma flag (the value occurs more than
-// gamma = 2 times in the sample); LD reads one sorted element.
-template <typename K, typename LD>
-__device__ __forceinline__ void res_pick(LD ld, int S, int o, int j, K& t, uint8_t& f) {
-  const int r = (j + 1) * o;
-  t = ld(r);
-  const bool m1 = r >= 1 && ld(r - 1) == t, m2 = r >= 2 && ld(r - 2) == t;
-  const bool p1 = r + 1 < S && ld(r + 1) == t, p2 = r + 2 < S && ld(r + 2) == t;
-  f = ((m1 && m2) || (m1 && p1) || (p1 && p2)) ? 1 : 0;
 }
 
 // Register bitonic sort of `count` keys by a group of GL lanes holding VT keys
