@@ -85,6 +85,20 @@ int32_t sr_sort_pairs(void *keys, void *vals, int64_t n, int32_t dtype, void *st
  */
 int32_t sr_sort_host(void *host_keys, void *host_vals, int64_t n, int32_t dtype, void *stream);
 
+/* Record keys (the paper's "random 16-/64-/256-list"
+ * classes, Table 2): recs holds n records of
+ * `words` (1..1024) consecutive signed int32 values (row-major, 4-byte
+ * aligned, device memory), sorted in place in ascending lexicographic order.
+ * Records equal in every word are identical, so the result is unique.  The
+ * call refines an index permutation with the stable int64 pair sort -- round 0
+ * on the words (0, 1), round r on (run of equal prefix, word r+1) -- until no
+ * two adjacent records tie or the words are exhausted, then gathers the
+ * records (scratch ~ n*(words*4 + 28) bytes).  Synchronises the host once per
+ * refinement round.  SR_ERR_INVALID_ARGUMENT (words out of range, NULL, host
+ * pointer), SR_ERR_SIZE (n > 2^31 - 1), SR_ERR_ALIGNMENT; recs untouched on
+ * these errors. */
+int32_t sr_sort_records(void *recs, int64_t n, int32_t words, void *stream);
+
 /* ------------------------------------------------------------------ introspection */
 
 typedef struct {

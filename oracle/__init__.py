@@ -63,6 +63,8 @@ def lib():
         L.or_stable_rank.restype = c64
         L.or_sort_float.argtypes = [vp, vp, c64, ci]
         L.or_sort_float.restype = ci
+        L.or_sort_records.argtypes = [vp, c64, ci, vp]
+        L.or_sort_records.restype = ci
         _lib = L
     return _lib
 
@@ -103,6 +105,18 @@ def sort_pairs(keys: np.ndarray, vals: np.ndarray):
     if rc != 0:
         raise MemoryError("oracle sort: out of host memory")
     return k, v.view(vals.dtype)
+
+
+def sort_records(recs: np.ndarray, with_perm: bool = False):
+    """Records (rows of an (n, words) int32 array) in ascending lexicographic
+    order by a plain stable mergesort (PAPER.md:58 lists).  Returns a new array
+    (and the input row of every output row with with_perm)."""
+    r = np.ascontiguousarray(recs, dtype=np.int32).copy()
+    n, words = r.shape
+    perm = np.zeros(n, np.int64)
+    if lib().or_sort_records(_p(r), n, words, _p(perm)) != 0:
+        raise MemoryError("oracle sort: out of host memory")
+    return (r, perm) if with_perm else r
 
 
 def descents(keys: np.ndarray) -> int:

@@ -40,6 +40,10 @@
  *                      (e): presortedness not disturbed)
  *   or_count           #{x < v}, #{x <= v}  (rank) for sampled checks
  *   or_stable_rank     #{j: k_j < k_i} + #{j < i: k_j = k_i}
+ *   or_sort_records    the same stable mergesort over records of `words` int32
+ *                      compared lexicographically (the paper's 16-/64-/256-int
+ *                      lists, Table 2; SURVEY.md
+ *                      §8(f) NEXT #3)
  *   or_sort_float      the same stable mergesort over float32 / float64 keys
  *                      ordered by IEEE 754-2008 §5.10 totalOrder, written out
  *                      case by case from that definition (the paper's
@@ -383,5 +387,47 @@ int or_sort_float(void *keys, uint32_t *vals, int64_t n, int fs) {
     }
     free(r);
     free(tmp);
+    return 0;
+}
+
+/* ---- record keys: lexicographic order over int32 words (PAPER.md:58 lists) -- */
+
+static int rec_le(const int32_t *a, const int32_t *b, int words) { /* a <= b lexicographically */
+    for (int j = 0; j < words; j++) {
+        if (a[j] < b[j]) return 1;
+        if (a[j] > b[j]) return 0;
+    }
+    return 1; /* equal */
+}
+
+static void rmsort(int64_t *ix, int64_t *tmp, int64_t lo, int64_t hi, const int32_t *recs, int words) {
+    if (hi - lo <= 1) return;
+    int64_t mid = lo + (hi - lo) / 2;
+    rmsort(ix, tmp, lo, mid, recs, words);
+    rmsort(ix, tmp, mid, hi, recs, words);
+    int64_t i = lo, j = mid, k = lo;
+    while (i < mid && j < hi) {
+        if (rec_le(recs + ix[i] * words, recs + ix[j] * words, words)) tmp[k++] = ix[i++]; /* A wins ties */
+        else tmp[k++] = ix[j++];
+    }
+    while (i < mid) tmp[k++] = ix[i++];
+    while (j < hi) tmp[k++] = ix[j++];
+    memcpy(ix + lo, tmp + lo, (size_t)(hi - lo) * sizeof(int64_t));
+}
+
+/* recs: n records of `words` int32, sorted in place; perm (may be NULL)
+ * receives the input index of each output record. */
+int or_sort_records(int32_t *recs, int64_t n, int words, int64_t *perm) {
+    if (n <= 1) { if (perm && n == 1) perm[0] = 0; return 0; }
+    int64_t *ix = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *tmp = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int32_t *out = (int32_t *)malloc((size_t)n * words * sizeof(int32_t));
+    if (!ix || !tmp || !out) { free(ix); free(tmp); free(out); return -1; }
+    for (int64_t i = 0; i < n; i++) ix[i] = i;
+    rmsort(ix, tmp, 0, n, recs, words);
+    for (int64_t i = 0; i < n; i++) memcpy(out + i * words, recs + ix[i] * words, (size_t)words * sizeof(int32_t));
+    memcpy(recs, out, (size_t)n * words * sizeof(int32_t));
+    if (perm) memcpy(perm, ix, (size_t)n * sizeof(int64_t));
+    free(ix); free(tmp); free(out);
     return 0;
 }

@@ -22,7 +22,7 @@ ROUTE_MERGE, ROUTE_PARTITION, ROUTE_OUTLIER = 3, 4, 6
 OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE = 0, 1, 2, 3, 4, 5
 
 EXPORTS = [
-    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_last_plan", "sr_status_string", "sr_last_error",
+    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_last_plan", "sr_status_string", "sr_last_error",
     "sr_set_option", "sr_last_profile", "sr_presort_scan", "sr_reverse_range", "sr_tile_sort", "sr_merge_path",
     "sr_merge", "sr_splitters", "sr_partition_level",
 ]
@@ -64,6 +64,7 @@ def lib():
         L.sr_sort_keys.argtypes = [vp, i64, i32, vp]
         L.sr_sort_pairs.argtypes = [vp, vp, i64, i32, vp]
         L.sr_sort_host.argtypes = [vp, vp, i64, i32, vp]
+        L.sr_sort_records.argtypes = [vp, i64, i32, vp]
         L.sr_last_plan.argtypes = [ctypes.POINTER(Plan)]
         L.sr_status_string.argtypes = [i32]
         L.sr_status_string.restype = ctypes.c_char_p
@@ -144,6 +145,18 @@ def sort_pairs(keys, vals):
         raise ValueError("keys and vals differ in length")
     _check(lib().sr_sort_pairs(_ptr(keys), _ptr(vals), keys.numel(), _dtype_code(keys), _stream(keys)))
     return keys, vals
+
+
+def sort_records(recs):
+    """Sort the rows of a CUDA int32 tensor of shape (n, words) ascending in
+    lexicographic order, in place (sr_sort_records; record keys, the paper's
+    16-/64-/256-int lists)."""
+    import torch
+    _dev(recs, "recs")
+    if recs.dtype != torch.int32 or recs.dim() != 2:
+        raise TypeError("recs must be a 2-D int32 tensor (n, words)")
+    _check(lib().sr_sort_records(_ptr(recs), recs.shape[0], recs.shape[1], _stream(recs)))
+    return recs
 
 
 def sort_host(keys: np.ndarray, vals: np.ndarray | None = None, stream: int = 0):

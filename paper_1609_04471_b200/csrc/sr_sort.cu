@@ -23,6 +23,7 @@
 #include "../../include/sr_sort.h"
 #include "fkeys.cuh"
 #include "merge.cuh"
+#include "records.cuh"
 #include "outlier.cuh"
 #include "partition.cuh"
 #include "presort.cuh"
@@ -1554,6 +1555,56 @@ int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream
   });
 }
 
+// Record keys (records.cuh): lexicographic sort of n records of `words` int32
+// by index refinement rounds of the stable int64 pair sort, then a gather.
+void sort_records_impl(int32_t* recs, int64_t n, int words, cudaStream_t st) {
+  Ctx c(st);
+  c.plan.n = n;
+  init_pool();
+  int64_t* kA = c.alloc<int64_t>(n);
+  int64_t* kB = c.alloc<int64_t>(n);
+  uint32_t* idx = c.alloc<uint32_t>(n);
+  uint32_t* flag = c.alloc<uint32_t>(n);
+  const int64_t tiles = ceil_div<int64_t>(n, kScanNT * kScanIPT);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n, 256)));
+  c.launch("rec_init", n * (int64_t)words * 4 + n * 12, [&] {
+    k_rec_init<<<grid, 256, 0, c.st>>>(recs, n, words, kA, idx);
+  });
+  int launches = 0;
+  int rounds = 0;
+  for (int w = std::min(words, 2);; w++) {
+    {  // stable pair sort of (key, idx) on the integer path
+      Ctx sc(st);
+      Sorter<int64_t, true>(sc, kA, idx, n).run();
+      launches += sc.plan.launches;
+    }
+    rounds++;
+    if (w >= words) break;
+    // control: scan status (zeroed) + the tie flag
+    unsigned char* ctrl = c.alloc<unsigned char>(256 + 8 * tiles);
+    c.memset0(ctrl, 256 + 8 * tiles);
+    uint32_t* any_tie = reinterpret_cast<uint32_t*>(ctrl);
+    int* tile_counter = reinterpret_cast<int*>(ctrl + 128);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ctrl + 256);
+    c.launch("rec_flags", n * 12, [&] { k_rec_flags<<<grid, 256, 0, c.st>>>(kA, n, flag, any_tie); });
+    const uint32_t tie = *reinterpret_cast<const uint32_t*>(c.readback(any_tie, 4));
+    if (!tie) break;  // every record is already in place
+    c.launch("scan", n * 8, [&] {
+      k_scan_u32<kScanNT, kScanIPT><<<(unsigned)tiles, kScanNT, 0, c.st>>>(flag, n, status, tile_counter, nullptr);
+    });
+    c.launch("rec_next", n * 28, [&] { k_rec_next<<<grid, 256, 0, c.st>>>(recs, n, words, w, flag, kA, kB, idx); });
+    std::swap(kA, kB);
+  }
+  int32_t* out = c.alloc<int32_t>(n * (int64_t)words);
+  c.launch("rec_gather", 2 * n * (int64_t)words * 4, [&] {
+    k_rec_gather<<<148 * 8, 256, 0, c.st>>>(recs, n, words, idx, out);
+  });
+  check_cuda(cudaMemcpyAsync(recs, out, (size_t)n * words * 4, cudaMemcpyDeviceToDevice, c.st), "record copy");
+  c.plan.levels = rounds;
+  c.plan.launches += launches;
+  c.plan.route = SR_ROUTE_PARTITION;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1597,6 +1648,16 @@ int32_t sr_sort_host(void* host_keys, void* host_vals, int64_t n, int32_t dtype,
     rc = SR_ERR_CUDA;
   }
   return rc;
+}
+
+int32_t sr_sort_records(void* recs, int64_t n, int32_t words, void* stream) {
+  t_state.err.clear();
+  if (n < 0 || words < 1 || words > 1024) return SR_ERR_INVALID_ARGUMENT;
+  if (n > INT32_MAX || n * (int64_t)words > (int64_t(1) << 40)) return SR_ERR_SIZE;
+  if (n <= 1) return SR_OK;
+  if (!recs || !is_device_ptr(recs)) return SR_ERR_INVALID_ARGUMENT;
+  if ((uintptr_t)recs % 4) return SR_ERR_ALIGNMENT;
+  return guarded([&] { sort_records_impl((int32_t*)recs, n, words, (cudaStream_t)stream); });
 }
 
 int32_t sr_last_plan(sr_plan* out) {

@@ -414,3 +414,30 @@ def test_float_pairs_stable(dtype):
     same = ok.view(it)[1:] == ok.view(it)[:-1]
     assert np.all(ov[1:][same] > ov[:-1][same])
     assert np.array_equal(oracle.sort_keys(k).view(it), ok.view(it))
+
+
+# ---- record keys: lexicographic order --------
+
+@pytest.mark.parametrize("words", [1, 2, 3, 5])
+@pytest.mark.parametrize("order", ["lrandom", "lprefix", "lequal", "ldup"])
+def test_records_match_python_tuples(order, words):
+    """Python's sorted() on tuples is a stable lexicographic sort (library routine)."""
+    r = gen.make_list(order, 700, words, config=77)
+    o, perm = oracle.sort_records(r, with_perm=True)
+    rows = [tuple(x) for x in r.tolist()]
+    exp = sorted(range(len(rows)), key=lambda i: rows[i])
+    assert perm.tolist() == exp
+    assert np.array_equal(o, r[exp])
+
+
+def test_records_brute_force_small():
+    """All 3^4 = 81 two-word records over {-1, 0, 1} in every rotation: the output
+    is the unique ascending enumeration."""
+    vals = [-1, 0, 1]
+    allrec = np.array([(a, b) for a in vals for b in vals for _ in range(2)], np.int32)  # 18 rows, pairs of duplicates
+    for rot in range(len(allrec)):
+        r = np.roll(allrec, rot, axis=0)
+        o, perm = oracle.sort_records(r, with_perm=True)
+        assert o.tolist() == [[a, b] for a in vals for b in vals for _ in range(2)]
+        for i in range(0, len(o), 2):  # stability among identical records
+            assert perm[i] < perm[i + 1]

@@ -291,6 +291,36 @@ def make_float(order: str, n: int, dtype=np.float64, config: int = 0, instance: 
     raise KeyError(order)
 
 
+# ---- record keys: n lists of `words` int32, the
+# paper's "random 16-/64-/256-list" classes.  "lrandom" = uniform
+# words; "lprefix" = the first words drawn from `vals` values (long shared
+# prefixes, many refinement rounds); "lequal" = every record identical except
+# a few; "ldup" = random records, each repeated ~4 times.
+LIST_ORDERS = {"lrandom": 48, "lprefix": 49, "lequal": 50, "ldup": 51}
+
+
+def make_list(order: str, n: int, words: int, config: int = 0, instance: int = 0, vals: int = 3) -> np.ndarray:
+    s = seed_for(config, LIST_ORDERS[order], instance)
+    d = draws(s, n * words)
+    r = (d >> np.uint64(32)).astype(np.uint32).view(np.int32).reshape(n, words).copy()
+    if order == "lprefix":
+        few = uniform_below(draws(s ^ 1, n * words), vals).reshape(n, words).astype(np.int32) - 1
+        keep = max(1, words - 1)  # all but the last word from {-1, 0, 1}
+        r[:, :keep] = few[:, :keep]
+    elif order == "lequal":
+        base = r[0].copy()
+        r[:] = base
+        k = max(1, n // 100)
+        pos = uniform_below(draws(s ^ 2, k), n)
+        r[pos, -1] = (draws(s ^ 3, k) >> np.uint64(33)).astype(np.int32)
+    elif order == "ldup":
+        m = max(1, n // 4)
+        r = r[uniform_below(draws(s ^ 4, n), m)].copy()
+    elif order != "lrandom":
+        raise KeyError(order)
+    return r
+
+
 def index_payload(n: int) -> np.ndarray:
     """configs[3]: payload = original index (int32, stored as 4-byte opaque)."""
     return np.arange(n, dtype=np.uint32)
