@@ -47,12 +47,39 @@ WORKLOADS = {
     "c3": (16_777_216, np.int32, ["swaps_1e4", "swaps_1e3", "swaps_1e2", "swaps_1e1", "runs1024", "last1pct",
                                   "alternating"], 2),
     "c4": (16_777_216, np.int32, ["few100"], 3),
+    # report-only widenings: the paper's "random
+    # double" and "random 16-list" classes at the Table 1 size
+    "c2d": (2_000_000, np.float64, ["funiform", "fbits"], 1),
+    "c2l16": (2_000_000, ("rec", 16), ["lrandom", "lprefix"], 1),
 }
+
+
+def is_rec(dtype):
+    return isinstance(dtype, tuple)
+
+
+def elem_bytes(dtype):
+    return 4 * dtype[1] if is_rec(dtype) else np.dtype(dtype).itemsize
+
+
+def dtype_label(dtype):
+    if is_rec(dtype):
+        return f"i32x{dtype[1]}"
+    return {"int32": "i32", "int64": "i64", "float32": "f32", "float64": "f64"}[np.dtype(dtype).name]
+
+
+def oracle_sort(a):
+    import oracle
+    return oracle.sort_records(a) if a.ndim == 2 else oracle.sort_keys(a)
 
 
 def make_input(order, n, dtype, config, instance):
     if order == "nearly1000":
         return gen.swaps(n, n // 1000, dtype, gen.seed_for(config, 2, instance))
+    if is_rec(dtype):
+        return gen.make_list(order, n, dtype[1], config=config, instance=instance)
+    if np.dtype(dtype).kind == "f":
+        return gen.make_float(order, n, dtype, config=config, instance=instance)
     return gen.make(order, n, dtype, config=config, instance=instance)
 
 
@@ -191,18 +218,18 @@ def run_reference(args, wl):
     inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
     for _ in range(args.warmup):
         for a in inputs:
-            oracle.sort_keys(a)
+            oracle_sort(a)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for a in inputs:
-            oracle.sort_keys(a)
+            oracle_sort(a)
     dt = (time.perf_counter() - t0) / args.steps
     keys = m * len(orders)
     v = keys / dt / 1e6
     line = {"impl": "reference", "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types)", "value": round(v, 3),
             "unit": "Mkeys/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": np.dtype(dtype).name.replace("int", "i"), "data": "synthetic",
+            "dtype": dtype_label(dtype), "data": "synthetic",
             "config": {"workload": wl, "n": n, "orders": orders, "sample_keys_per_order": m},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
                              "sample": f"first {m} keys of instance 0 of each order, single-threaded C mergesort"},
@@ -222,9 +249,9 @@ def cpu_baseline(wl, budget_s=12.0):
     while t_sort < budget_s and rounds < 10:
         for a in inputs:
             t0 = time.perf_counter()
-            oracle.sort_keys(a)
+            oracle_sort(a)
             t_sort += time.perf_counter() - t0
-            keys += a.size
+            keys += a.shape[0]
         rounds += 1
     sample = (f"{rounds} x instance 0 of each of {orders}, " + (f"n={n}" if m == n else f"first {m} keys of n={n}"))
     return {"value": round(keys / t_sort / 1e6, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
@@ -261,8 +288,11 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     n, dtype, orders, cfg = WORKLOADS[wl]
-    tdt = torch.int32 if dtype == np.int32 else torch.int64
-    kw = np.dtype(dtype).itemsize
+    rec = is_rec(dtype)
+    tdt = torch.int32 if rec else {"int32": torch.int32, "int64": torch.int64, "float32": torch.float32,
+                                   "float64": torch.float64}[np.dtype(dtype).name]
+    kw = elem_bytes(dtype)
+    shape = (n, dtype[1]) if rec else (n,)
 
     # inputs: instance = rank * (steps+warmup) + step  (weak scaling: independent problems per rank)
     total = args.steps + args.warmup
@@ -277,7 +307,7 @@ def main():
             pristine[(o, i)] = torch.from_numpy(a).to(dev)
             if i == 0:
                 host_inputs[o] = a
-    work = torch.empty(n, dtype=tdt, device=dev)
+    work = torch.empty(shape, dtype=tdt, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     def one_sort(o, i, ev=None):
@@ -285,7 +315,10 @@ def main():
         flush.fill_(i)
         if ev:
             ev[0].record(stream)
-        sr.sort_keys(work)
+        if rec:
+            sr.sort_records(work)
+        else:
+            sr.sort_keys(work)
         if ev:
             ev[1].record(stream)
         return sr.last_plan()
@@ -323,7 +356,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         pin = {o: torch.from_numpy(host_inputs[o]).pin_memory() for o in orders}
-        hbuf = torch.empty(n, dtype=tdt).pin_memory()
+        hbuf = torch.empty(shape, dtype=tdt).pin_memory()
         hb = hbuf.numpy()
         e2e_ms = 0.0
         for s in range(args.warmup + args.steps):
@@ -332,7 +365,12 @@ def main():
                 flush.fill_(s)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                sr.sort_host(hb, None, stream.cuda_stream)
+                if rec:  # records have no host-buffer entry point: H2D, sort, D2H through torch + sr
+                    work.copy_(hbuf, non_blocking=True)
+                    sr.sort_records(work)
+                    hbuf.copy_(work, non_blocking=True)
+                else:
+                    sr.sort_host(hb, None, stream.cuda_stream)
                 b.record(stream)
                 b.synchronize()
                 if s >= args.warmup:
@@ -361,7 +399,7 @@ def main():
     bytes_per_launch = d["bytes"] / d["launches"]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     kern_total = sum(v["ms"] for v in kern.values())
-    tr = ncu_traffic(dname, "int" if dtype == np.int32 else "long", wl)
+    tr = ncu_traffic(dname, "int" if kw == 4 else "long", wl)
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": tr["bytes"] if tr else None,
                 "traffic_source": tr, "algorithmic_bytes_per_launch": int(bytes_per_launch),
@@ -377,7 +415,7 @@ def main():
         "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types); achieved HBM GB/s vs peak",
         "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms_mean, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "i32" if dtype == np.int32 else "i64", "data": "synthetic",
+        "dtype": dtype_label(dtype), "data": "synthetic",
         "config": {"workload": wl, "n": n, "orders": orders, "keys_per_step_per_gpu": n * len(orders),
                    "l2": "flushed (512 MiB write) before every sort; restore+flush outside the events",
                    "parallelism": f"independent instances per rank x{ws}",
