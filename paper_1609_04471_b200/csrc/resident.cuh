@@ -624,15 +624,15 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     __syncthreads();
   }
   SR_RES_STAMP(0);
-  if (sampler) {
+  if (sampler) {  // the quarter: 128-key register runs + merge-path rounds, written to a.samp
+    typename SM::E& e = sm.u.e;
 #pragma unroll
     for (int r = 0; r < SG; r++) {
       const int q = r * NT + tid;
-      if (q < QS) sm.u.samp1[q] = sx[r];
+      if (q < QS) e.x[q] = sx[r];
     }
     __syncthreads();
-    BitonicSort<K, NT, SG>::sort(sm.u.samp1, QS);
-    for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = sm.u.samp1[q];
+    res_bucket_sort<K, NT>(a.samp + (int64_t)quarter * QS, QS, e, nullptr);
   }
   SR_RES_STAMP(1);
   grid.sync();
