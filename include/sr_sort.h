@@ -99,6 +99,22 @@ int32_t sr_sort_host(void *host_keys, void *host_vals, int64_t n, int32_t dtype,
  * these errors. */
 int32_t sr_sort_records(void *recs, int64_t n, int32_t words, void *stream);
 
+/* Presortedness measures of
+ * keys[0..n) (device, int32 / int64, not modified), rank = stable rank
+ * (SPEC.md:201):
+ *   runs       Run(A) = #{i : a_i > a_{i+1}} + 1
+ *   inversions Inv(A) = #{(i, j) : i < j, a_i > a_j}
+ *   mono       Mono(A): fewest contiguous pieces that are each sorted or
+ *              reversely sorted (non-decreasing / non-increasing)
+ *   max_dis    max_i |rank(a_i) - i|: A is k-distance iff max_dis <= k
+ *   misplaced  #{i : rank(a_i) != i}: <= 2k for a k-exchange list
+ * Scratch ~ n*(key bytes + 12) bytes; synchronises the stream.  n = 0 gives all
+ * zeros, n = 1 runs = mono = 1.  Errors as for sr_sort_keys. */
+typedef struct {
+  int64_t n, runs, inversions, mono, max_dis, misplaced;
+} sr_measures;
+int32_t sr_presortedness(const void *keys, int64_t n, int32_t dtype, sr_measures *host_out, void *stream);
+
 /* ------------------------------------------------------------------ introspection */
 
 typedef struct {

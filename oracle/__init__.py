@@ -65,6 +65,8 @@ def lib():
         L.or_sort_float.restype = ci
         L.or_sort_records.argtypes = [vp, c64, ci, vp]
         L.or_sort_records.restype = ci
+        L.or_measures.argtypes = [vp, c64, ci, vp]
+        L.or_measures.restype = ci
         _lib = L
     return _lib
 
@@ -117,6 +119,16 @@ def sort_records(recs: np.ndarray, with_perm: bool = False):
     if lib().or_sort_records(_p(r), n, words, _p(perm)) != 0:
         raise MemoryError("oracle sort: out of host memory")
     return (r, perm) if with_perm else r
+
+
+def measures(keys: np.ndarray) -> dict:
+    """Presortedness measures: Run, Inv, Mono, Dis (max
+    |rank - i|, k-distance) and the number of misplaced elements (k-exchange)."""
+    k = np.ascontiguousarray(keys)
+    out = np.zeros(5, np.int64)
+    if lib().or_measures(_p(k), k.size, _ks(k), _p(out)) != 0:
+        raise MemoryError("oracle measures: out of host memory")
+    return dict(zip(["runs", "inversions", "mono", "max_dis", "misplaced"], out.tolist()))
 
 
 def descents(keys: np.ndarray) -> int:

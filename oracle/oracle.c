@@ -44,6 +44,13 @@
  *                      compared lexicographically (the paper's 16-/64-/256-int
  *                      lists, Table 2; SURVEY.md
  *                      §8(f) NEXT #3)
+ *   or_measures        presortedness measures of PAPER.md:62-85 from their
+ *                      definitions: Run(A) = #descents + 1 (:66), Inv(A) =
+ *                      #{i<j : a_i > a_j} (:64, counted while merging), Mono(A)
+ *                      = fewest monotone pieces (:72, greedy left to right),
+ *                      Dis(A) = max |rank(a_i) - i| (k-distance, :84) and
+ *                      #{i : rank(a_i) != i} (k-exchange, :85), rank = stable
+ *                      rank
  *   or_sort_float      the same stable mergesort over float32 / float64 keys
  *                      ordered by IEEE 754-2008 §5.10 totalOrder, written out
  *                      case by case from that definition (the paper's
@@ -429,5 +436,65 @@ int or_sort_records(int32_t *recs, int64_t n, int words, int64_t *perm) {
     memcpy(recs, out, (size_t)n * words * sizeof(int32_t));
     if (perm) memcpy(perm, ix, (size_t)n * sizeof(int64_t));
     free(ix); free(tmp); free(out);
+    return 0;
+}
+
+/* ---- presortedness measures ------- */
+
+/* Inv by a counting mergesort: when an element of the right run is output,
+ * every remaining element of the left run is greater (strictly: ties go left). */
+static int64_t inv_msort(int64_t *a, int64_t *tmp, int64_t lo, int64_t hi) {
+    if (hi - lo <= 1) return 0;
+    int64_t mid = lo + (hi - lo) / 2;
+    int64_t c = inv_msort(a, tmp, lo, mid) + inv_msort(a, tmp, mid, hi);
+    int64_t i = lo, j = mid, k = lo;
+    while (i < mid && j < hi) {
+        if (a[i] <= a[j]) tmp[k++] = a[i++];
+        else { c += mid - i; tmp[k++] = a[j++]; }
+    }
+    while (i < mid) tmp[k++] = a[i++];
+    while (j < hi) tmp[k++] = a[j++];
+    memcpy(a + lo, tmp + lo, (size_t)(hi - lo) * sizeof(int64_t));
+    return c;
+}
+
+/* out: [runs, inversions, mono, max_dis, misplaced] */
+int or_measures(const void *keys, int64_t n, int ks, int64_t *out) {
+    out[0] = out[1] = out[2] = out[3] = out[4] = 0;
+    if (n <= 0) return 0;
+    /* Run(A) */
+    out[0] = or_descents(keys, n, ks) + 1;
+    /* Mono(A): extend the current piece while it stays non-decreasing or
+     * non-increasing; its direction is fixed by its first strict step */
+    int64_t pieces = 1;
+    int dir = 0; /* 0 undetermined, 1 ascending, -1 descending */
+    for (int64_t i = 0; i + 1 < n; i++) {
+        int64_t x = load_key(keys, ks, i), y = load_key(keys, ks, i + 1);
+        int step = x < y ? 1 : (x > y ? -1 : 0);
+        if (step == 0) continue;
+        if (dir == 0) dir = step;
+        else if (step != dir) { pieces++; dir = 0; } /* a new piece starts at a_{i+1} */
+    }
+    out[2] = pieces;
+    /* stable ranks: the stable sort of (key, index) */
+    rec_t *r = (rec_t *)malloc((size_t)n * sizeof(rec_t));
+    int64_t *perm = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *tmp = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    if (!r || !perm || !tmp) { free(r); free(perm); free(tmp); return -1; }
+    for (int64_t i = 0; i < n; i++) { r[i].key = load_key(keys, ks, i); r[i].val = (uint32_t)i; }
+    if (sort_recs(r, n) != 0) { free(r); free(perm); free(tmp); return -1; }
+    int64_t dis = 0, mis = 0;
+    for (int64_t p = 0; p < n; p++) {  /* the element of input position r[p].val has rank p */
+        int64_t d = p - (int64_t)r[p].val;
+        if (d < 0) d = -d;
+        if (d > dis) dis = d;
+        if (d) mis++;
+    }
+    out[3] = dis;
+    out[4] = mis;
+    /* Inv(A) on the keys themselves */
+    for (int64_t i = 0; i < n; i++) perm[i] = load_key(keys, ks, i);
+    out[1] = inv_msort(perm, tmp, 0, n);
+    free(r); free(perm); free(tmp);
     return 0;
 }

@@ -22,7 +22,7 @@ ROUTE_MERGE, ROUTE_PARTITION, ROUTE_OUTLIER = 3, 4, 6
 OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE = 0, 1, 2, 3, 4, 5
 
 EXPORTS = [
-    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_last_plan", "sr_status_string", "sr_last_error",
+    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",
     "sr_set_option", "sr_last_profile", "sr_presort_scan", "sr_reverse_range", "sr_tile_sort", "sr_merge_path",
     "sr_merge", "sr_splitters", "sr_partition_level",
 ]
@@ -65,6 +65,7 @@ def lib():
         L.sr_sort_pairs.argtypes = [vp, vp, i64, i32, vp]
         L.sr_sort_host.argtypes = [vp, vp, i64, i32, vp]
         L.sr_sort_records.argtypes = [vp, i64, i32, vp]
+        L.sr_presortedness.argtypes = [vp, i64, i32, ctypes.POINTER(Measures), vp]
         L.sr_last_plan.argtypes = [ctypes.POINTER(Plan)]
         L.sr_status_string.argtypes = [i32]
         L.sr_status_string.restype = ctypes.c_char_p
@@ -145,6 +146,19 @@ def sort_pairs(keys, vals):
         raise ValueError("keys and vals differ in length")
     _check(lib().sr_sort_pairs(_ptr(keys), _ptr(vals), keys.numel(), _dtype_code(keys), _stream(keys)))
     return keys, vals
+
+
+class Measures(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ["n", "runs", "inversions", "mono", "max_dis", "misplaced"]]
+
+
+def presortedness(keys) -> dict:
+    """Presortedness measures of a CUDA int32/int64 tensor (sr_presortedness,
+    PAPER.md:62-85): runs, inversions, mono, max_dis, misplaced."""
+    _dev(keys, "keys")
+    m = Measures()
+    _check(lib().sr_presortedness(_ptr(keys), keys.numel(), _dtype_code(keys), ctypes.byref(m), _stream(keys)))
+    return {f: getattr(m, f) for f, _ in Measures._fields_}
 
 
 def sort_records(recs):

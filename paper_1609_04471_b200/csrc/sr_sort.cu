@@ -22,6 +22,7 @@
 
 #include "../../include/sr_sort.h"
 #include "fkeys.cuh"
+#include "measures.cuh"
 #include "merge.cuh"
 #include "records.cuh"
 #include "outlier.cuh"
@@ -1605,6 +1606,51 @@ void sort_records_impl(int32_t* recs, int64_t n, int words, cudaStream_t st) {
   c.plan.route = SR_ROUTE_PARTITION;
 }
 
+// Presortedness measures (measures.cuh): Run and Mono from the keys, Dis /
+// misplaced from the stable pair sort of (key copy, index), Inv by counting
+// merge levels over that permutation.
+template <typename K>
+void measures_impl(const K* keys, int64_t n, sr_measures* out, cudaStream_t st) {
+  Ctx c(st);
+  c.plan.n = n;
+  init_pool();
+  constexpr int NT = 256;
+  const int64_t chunk = (int64_t)NT * 64;
+  const int G = (int)std::max<int64_t>(1, ceil_div<int64_t>(n - 1, chunk));
+  K* kc = c.alloc<K>(n);
+  uint32_t* idx = c.alloc<uint32_t>(n);
+  uint32_t* idx2 = c.alloc<uint32_t>(n);
+  MonoMap* maps = c.alloc<MonoMap>(G);
+  unsigned long long* cnt = c.alloc<unsigned long long>(8);  // descents, pieces, maxdis, misplaced, inv
+  c.memset0(cnt, 8 * sizeof(unsigned long long));
+  c.launch("mono_map", n * (int64_t)sizeof(K), [&] { k_mono_map<K, NT><<<G, NT, 0, c.st>>>(keys, n, chunk, maps, cnt); });
+  c.launch("mono_final", G * (int64_t)sizeof(MonoMap), [&] { k_mono_final<<<1, 32, 0, c.st>>>(maps, G, cnt + 1); });
+  check_cuda(cudaMemcpyAsync(kc, keys, n * sizeof(K), cudaMemcpyDeviceToDevice, c.st), "key copy");
+  {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n, NT)));
+    c.launch("iota", n * 4, [&] { k_iota<<<grid, NT, 0, c.st>>>(idx, n); });
+  }
+  {  // stable ranks
+    Ctx sc(st);
+    Sorter<K, true>(sc, kc, idx, n).run();
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n, NT)));
+  c.launch("dis", n * 4, [&] { k_dis<NT><<<grid, NT, 0, c.st>>>(idx, n, cnt + 2, cnt + 3); });
+  uint32_t* a = idx;
+  uint32_t* b = idx2;
+  for (int64_t R = 1; R < n; R *= 2) {
+    c.launch("inv_level", n * 8, [&] { k_inv_level<NT><<<grid, NT, 0, c.st>>>(a, b, n, R, cnt + 4); });
+    std::swap(a, b);
+  }
+  const unsigned long long* h = reinterpret_cast<const unsigned long long*>(c.readback(cnt, 8 * sizeof(unsigned long long)));
+  out->n = n;
+  out->runs = (int64_t)h[0] + 1;
+  out->mono = (int64_t)h[1];
+  out->max_dis = (int64_t)h[2];
+  out->misplaced = (int64_t)h[3];
+  out->inversions = (int64_t)h[4];
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1658,6 +1704,26 @@ int32_t sr_sort_records(void* recs, int64_t n, int32_t words, void* stream) {
   if (!recs || !is_device_ptr(recs)) return SR_ERR_INVALID_ARGUMENT;
   if ((uintptr_t)recs % 4) return SR_ERR_ALIGNMENT;
   return guarded([&] { sort_records_impl((int32_t*)recs, n, words, (cudaStream_t)stream); });
+}
+
+int32_t sr_presortedness(const void* keys, int64_t n, int32_t dtype, sr_measures* host_out, void* stream) {
+  t_state.err.clear();
+  if (!host_out || n < 0) return SR_ERR_INVALID_ARGUMENT;
+  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (n > INT32_MAX) return SR_ERR_SIZE;
+  *host_out = sr_measures{};
+  host_out->n = n;
+  if (n == 0) return SR_OK;
+  if (n == 1) {
+    host_out->runs = host_out->mono = 1;
+    return SR_OK;
+  }
+  if (!keys || !is_device_ptr(keys)) return SR_ERR_INVALID_ARGUMENT;
+  if ((uintptr_t)keys % key_bytes(dtype)) return SR_ERR_ALIGNMENT;
+  return guarded([&] {
+    if (dtype == SR_INT32) measures_impl<int32_t>((const int32_t*)keys, n, host_out, (cudaStream_t)stream);
+    else measures_impl<int64_t>((const int64_t*)keys, n, host_out, (cudaStream_t)stream);
+  });
 }
 
 int32_t sr_last_plan(sr_plan* out) {

@@ -441,3 +441,67 @@ def test_records_brute_force_small():
         assert o.tolist() == [[a, b] for a in vals for b in vals for _ in range(2)]
         for i in range(0, len(o), 2):  # stability among identical records
             assert perm[i] < perm[i + 1]
+
+
+# ---- presortedness measures ---------
+
+def _mono_dp(a):
+    """Fewest contiguous monotone pieces by dynamic programming over all cut points
+    (an exhaustive alternative to the oracle's greedy)."""
+    n = len(a)
+    def mono(s, e):
+        seg = a[s:e]
+        return all(x <= y for x, y in zip(seg, seg[1:])) or all(x >= y for x, y in zip(seg, seg[1:]))
+    best = [0] + [n + 1] * n
+    for e in range(1, n + 1):
+        for s in range(e):
+            if mono(s, e):
+                best[e] = min(best[e], best[s] + 1)
+    return best[n]
+
+
+def test_measures_closed_forms():
+    n = 1000
+    r = oracle.measures(np.arange(n, dtype=np.int32)[::-1].copy())  # PAPER.md:68
+    assert (r["inversions"], r["runs"], r["mono"], r["max_dis"]) == (n * (n - 1) // 2, n, 1, n - 1)
+    s = oracle.measures(np.arange(n, dtype=np.int64))
+    assert (s["inversions"], s["runs"], s["mono"], s["max_dis"], s["misplaced"]) == (0, 1, 1, 0, 0)
+    assert oracle.measures(np.array([1, 2, 3, 3, 2, 1], np.int32))["mono"] == 2  # organ pipe, PAPER.md:74
+    m = 64  # k = n/2 even teeth over {1, 2}: (2,1,1,2,2,1,1,2,...), Mono = n/4 + 1 (PAPER.md:80)
+    teeth = np.array(([2, 1, 1, 2] * (m // 4)), np.int32)
+    assert oracle.measures(teeth)["mono"] == m // 4 + 1
+    for k in [1, 4, 16]:  # k-equal teeth: Run = Mono = k (PAPER.md:79)
+        t = np.tile(np.arange(1, 101, dtype=np.int32), k)
+        mm = oracle.measures(t)
+        assert mm["runs"] == k and mm["mono"] == k
+    p, q = 100, 700  # one exchange of distinct sorted values: Inv = 2 (q - p) - 1, 2 misplaced
+    a = np.arange(n, dtype=np.int32)
+    a[[p, q]] = a[[q, p]]
+    e = oracle.measures(a)
+    assert (e["inversions"], e["misplaced"], e["max_dis"]) == (2 * (q - p) - 1, 2, q - p)
+
+
+def test_measures_brute_force_small():
+    rng = np.random.default_rng(5)
+    for n in range(1, 8):
+        for _ in range(60):
+            a = rng.integers(0, 3, n).astype(np.int32)
+            m = oracle.measures(a)
+            assert m["mono"] == _mono_dp(a.tolist())
+            assert m["inversions"] == int(np.triu(a[:, None] > a[None, :], 1).sum())
+            assert m["runs"] == int((a[:-1] > a[1:]).sum()) + 1
+            rank = np.empty(n, np.int64)
+            rank[np.argsort(a, kind="stable")] = np.arange(n)  # library stable sort
+            d = np.abs(rank - np.arange(n))
+            assert m["max_dis"] == int(d.max()) and m["misplaced"] == int((d != 0).sum())
+
+
+@pytest.mark.parametrize("k", [1, 8, 256])
+def test_measures_generated_classes(k):
+    n = 20000
+    dist = gen.make("distance256", n, np.int32, config=70) if k == 256 else None
+    if dist is not None:  # k-distance list: Dis <= k (PAPER.md:84)
+        assert oracle.measures(dist)["max_dis"] <= 256
+    sw = gen.swaps(n, k, np.int32, gen.seed_for(70, 2, k))  # k-exchange: misplaced <= 2k, Mono <= 2k+1 (PAPER.md:85)
+    m = oracle.measures(sw)
+    assert m["misplaced"] <= 2 * k and m["mono"] <= 2 * k + 1
