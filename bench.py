@@ -46,12 +46,15 @@ WORKLOADS = {
     "c5c": (134_217_728, np.int64, ["random"], 4),
     "c3": (16_777_216, np.int32, ["swaps_1e4", "swaps_1e3", "swaps_1e2", "swaps_1e1", "runs1024", "last1pct",
                                   "alternating"], 2),
-    "c4": (16_777_216, np.int32, ["few100"], 3),
+    "c4": (16_777_216, np.int32, ["few100"], 3),  # stable key-value sort, payload = original index
     # report-only widenings: the paper's "random
     # double" and "random 16-list" classes at the Table 1 size
     "c2d": (2_000_000, np.float64, ["funiform", "fbits"], 1),
     "c2l16": (2_000_000, ("rec", 16), ["lrandom", "lprefix"], 1),
 }
+
+
+PAIRS = {"c4"}  # workloads sorted as (key, payload = original index) pairs
 
 
 def is_rec(dtype):
@@ -68,8 +71,10 @@ def dtype_label(dtype):
     return {"int32": "i32", "int64": "i64", "float32": "f32", "float64": "f64"}[np.dtype(dtype).name]
 
 
-def oracle_sort(a):
+def oracle_sort(a, pairs=False):
     import oracle
+    if pairs:  # payload = original index (configs[3])
+        return oracle.sort_pairs(a, gen.index_payload(a.size))
     return oracle.sort_records(a) if a.ndim == 2 else oracle.sort_keys(a)
 
 
@@ -218,11 +223,11 @@ def run_reference(args, wl):
     inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
     for _ in range(args.warmup):
         for a in inputs:
-            oracle_sort(a)
+            oracle_sort(a, wl in PAIRS)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for a in inputs:
-            oracle_sort(a)
+            oracle_sort(a, wl in PAIRS)
     dt = (time.perf_counter() - t0) / args.steps
     keys = m * len(orders)
     v = keys / dt / 1e6
@@ -249,7 +254,7 @@ def cpu_baseline(wl, budget_s=12.0):
     while t_sort < budget_s and rounds < 10:
         for a in inputs:
             t0 = time.perf_counter()
-            oracle_sort(a)
+            oracle_sort(a, wl in PAIRS)
             t_sort += time.perf_counter() - t0
             keys += a.shape[0]
         rounds += 1
@@ -289,9 +294,10 @@ def main():
     stream = torch.cuda.current_stream()
     n, dtype, orders, cfg = WORKLOADS[wl]
     rec = is_rec(dtype)
+    pairs = wl in PAIRS
     tdt = torch.int32 if rec else {"int32": torch.int32, "int64": torch.int64, "float32": torch.float32,
                                    "float64": torch.float64}[np.dtype(dtype).name]
-    kw = elem_bytes(dtype)
+    kw = elem_bytes(dtype) + (4 if pairs else 0)  # bytes per element (key + payload)
     shape = (n, dtype[1]) if rec else (n,)
 
     # inputs: instance = rank * (steps+warmup) + step  (weak scaling: independent problems per rank)
@@ -308,15 +314,22 @@ def main():
             if i == 0:
                 host_inputs[o] = a
     work = torch.empty(shape, dtype=tdt, device=dev)
+    if pairs:  # configs[3]: payload = each element's original index (int32)
+        vals_pristine = torch.from_numpy(gen.index_payload(n).view(np.int32)).to(dev)
+        work_v = torch.empty(n, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     def one_sort(o, i, ev=None):
         work.copy_(pristine[(o, i % ninst)])
+        if pairs:
+            work_v.copy_(vals_pristine)
         flush.fill_(i)
         if ev:
             ev[0].record(stream)
         if rec:
             sr.sort_records(work)
+        elif pairs:
+            sr.sort_pairs(work, work_v)
         else:
             sr.sort_keys(work)
         if ev:
@@ -358,10 +371,16 @@ def main():
         pin = {o: torch.from_numpy(host_inputs[o]).pin_memory() for o in orders}
         hbuf = torch.empty(shape, dtype=tdt).pin_memory()
         hb = hbuf.numpy()
+        if pairs:
+            hvals = torch.empty(n, dtype=torch.int32).pin_memory()
+            hv = hvals.numpy()
+            hvals_src = torch.from_numpy(gen.index_payload(n).view(np.int32)).pin_memory()
         e2e_ms = 0.0
         for s in range(args.warmup + args.steps):
             for o in orders:
                 hbuf.copy_(pin[o])
+                if pairs:
+                    hvals.copy_(hvals_src)
                 flush.fill_(s)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -370,7 +389,7 @@ def main():
                     sr.sort_records(work)
                     hbuf.copy_(work, non_blocking=True)
                 else:
-                    sr.sort_host(hb, None, stream.cuda_stream)
+                    sr.sort_host(hb, hv if pairs else None, stream.cuda_stream)
                 b.record(stream)
                 b.synchronize()
                 if s >= args.warmup:
@@ -415,8 +434,8 @@ def main():
         "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types); achieved HBM GB/s vs peak",
         "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms_mean, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": dtype_label(dtype), "data": "synthetic",
-        "config": {"workload": wl, "n": n, "orders": orders, "keys_per_step_per_gpu": n * len(orders),
+        "dtype": dtype_label(dtype) + ("+u32 payload" if pairs else ""), "data": "synthetic",
+        "config": {"workload": wl, "pairs": pairs, "n": n, "orders": orders, "keys_per_step_per_gpu": n * len(orders),
                    "l2": "flushed (512 MiB write) before every sort; restore+flush outside the events",
                    "parallelism": f"independent instances per rank x{ws}",
                    "per_order_ms_mean": {o: round(statistics.mean(v), 4) for o, v in per_order_ms.items()},
