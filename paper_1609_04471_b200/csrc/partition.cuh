@@ -603,6 +603,9 @@ struct ScatterSmem {
   uint32_t red[NT / 32 + 1];
 };
 
+constexpr int kBinBits = 13;  // bucket ids 0 .. kMaxBins (invalid) < 2^13
+static_assert(kMaxBins < (1 << kBinBits), "");
+
 template <typename K, bool HAS_V, int NT, int VTS>
 __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
                                                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v,
@@ -652,7 +655,14 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
       int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
       bool valid = pos < c1;
       int b = !valid ? kMaxBins : (bins_in ? (int)bins_in[pos] : classify_key<K>(x[i], sm.spl, sm.eq, m, depth));
-      unsigned peers = __match_any_sync(0xffffffffu, b);
+      // lanes with the same bucket: one ballot per bit of the id (cheaper than
+      // MATCH.ANY, which dominated this kernel's stalls)
+      unsigned peers = 0xffffffffu;
+#pragma unroll
+      for (int bit = 0; bit < kBinBits; bit++) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (b >> bit) & 1);
+        peers &= ((b >> bit) & 1) ? bal : ~bal;
+      }
       int base = sm.wcnt[w][b];
       rk[i] = base + __popc(peers & lt);
       bin[i] = b;

@@ -317,7 +317,9 @@ constexpr int kFinNT = 256, kFinVT = 16;                 // K11 big items (two h
 constexpr int kFinSmallNT = 128;                         // K11 small items (pairs, <= 2048 = kSmallItem)
 constexpr int kWarpItemsPerCta = 4;                      // K11w (keys only): warps per CTA
 constexpr int kPackKeys = 128;                           // keys only: buckets <= this are packed into items
-constexpr int kScatNT = 256, kScatVT = 16;               // K10 (pairs, stable)
+constexpr int kScatNT = 256;                             // K10 (pairs, stable)
+template <typename K>
+constexpr int scat_vt() { return sizeof(K) == 4 ? 32 : 16; }  // 8K-pair (int32) / 4K-pair (int64) sub-tiles
 constexpr int kScatKNT = 1024;                           // K10 (keys only)
 template <typename K>
 constexpr int scat_kvt() { return sizeof(K) == 4 ? 16 : 8; }  // 16K-key (int32) / 8K-key (int64) sub-tiles
@@ -644,9 +646,9 @@ struct Sorter {
                                                                  L.atomic ? nullptr : L.d_mat, gate);
       });
     }
-    using SM = ScatterSmem<K, HAS_V, kScatNT, kScatVT>;
+    using SM = ScatterSmem<K, HAS_V, kScatNT, scat_vt<K>()>;
     size_t smem = sizeof(SM);
-    auto kern = k_scatter<K, HAS_V, kScatNT, kScatVT>;
+    auto kern = k_scatter<K, HAS_V, kScatNT, scat_vt<K>()>;
     set_smem(kern, smem);
     int64_t bytes = keys_in * (kw + vw) + noneq * kw + keys_in * vw + L.mat_entries * 4;
     return c.launch("scatter", bytes, [&] {
