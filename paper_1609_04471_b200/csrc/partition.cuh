@@ -665,10 +665,10 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
       }
       int base = sm.wcnt[w][b];
       rk[i] = base + __popc(peers & lt);
-      bin[i] = b;
       __syncwarp();
       if (lane == __ffs(peers) - 1) sm.wcnt[w][b] = (uint16_t)(base + __popc(peers));
       __syncwarp();
+      bin[i] = b;
     }
     __syncthreads();
     for (int b = tid; b < nb; b += NT) {
@@ -920,9 +920,24 @@ __global__ void __launch_bounds__(NT) k_finish(const Item* __restrict__ items, c
     const int len = item.len;
     if (kind == kItemFill) {
       const K key = (K)item.key;
-      for (int i = threadIdx.x; i < len; i += NT) {
-        keys[s + i] = key;
-        if (HAS_V && from_ws) vals[s + i] = ws_v[s + i];
+      constexpr int UF = 8;  // payload loads in flight per thread
+      for (int i0 = 0; i0 < len; i0 += NT * UF) {
+        uint32_t pv[UF];
+        if (HAS_V && from_ws) {
+#pragma unroll
+          for (int u = 0; u < UF; u++) {
+            const int i = i0 + u * NT + threadIdx.x;
+            pv[u] = i < len ? ws_v[s + i] : 0u;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UF; u++) {
+          const int i = i0 + u * NT + threadIdx.x;
+          if (i < len) {
+            keys[s + i] = key;
+            if (HAS_V && from_ws) vals[s + i] = pv[u];
+          }
+        }
       }
       continue;
     }
