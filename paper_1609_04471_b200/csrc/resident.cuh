@@ -108,6 +108,8 @@ struct ResArgs {
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
   uint32_t* unit_counter;   // [0] CTA units, [1] CTAs done, [2] warp units (zeroed by CTA 0 in phase A)
+  uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
+  uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
   ResDone* done;            // host-mapped completion record (the last CTA to exit writes it)
   uint32_t seq;             // this call's completion sequence number
@@ -624,6 +626,15 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     __syncthreads();
   }
   SR_RES_STAMP(0);
+  // ================= route: every CTA announces its tiles and waits for all ==============
+  // (a counter, not a grid barrier: the samplers arrive before sorting their
+  // sample quarter, so sorted / reversed inputs do not wait for the sorts)
+  if (tid == 0) {  // arrive as soon as this CTA's tiles are published
+    __threadfence();
+    atomicAdd(a.arrive, 1u);
+  }
+  // the samplers sort their sample quarter meanwhile (wasted only on the
+  // sorted / reversed routes, which the other CTAs finish without them)
   if (sampler) {  // the quarter: 128-key register runs + merge-path rounds, written to a.samp
     typename SM::E& e = sm.u.e;
 #pragma unroll
@@ -635,61 +646,39 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     res_bucket_sort<K, NT>(a.samp + (int64_t)quarter * QS, QS, e, nullptr);
   }
   SR_RES_STAMP(1);
-  grid.sync();
-
-  // ================= C: route (every CTA); splitters; tile-local bucket grouping =================
+  // samplers take the route CTA 0 publishes (one more arrival) instead of
+  // resolving it themselves; the others wait for every CTA's tiles
+  const uint32_t need = sampler ? (uint32_t)P + 1u : (uint32_t)P;
+  if (tid == 0) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.arrive) : "memory");
+    } while ((uint32_t)(v - a.arrive_base) < need);
+  }
+  __syncthreads();
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[1] = res_now();
   typename SM::SP& sp = sm.u.sp;
-  {  // tile summaries and the sorted sample pieces into shared memory
+  if (!sampler) {  // tile summaries into shared memory (the samplers read the published route)
     const int4* src = reinterpret_cast<const int4*>(a.sums);
     int4* dst = reinterpret_cast<int4*>(sp.ts);
     for (int i = tid; i < 2 * a.G; i += NT) dst[i] = __ldcg(src + i);
-    constexpr int SI = SM::S1MAX / NT;
-    K v[SI];
-#pragma unroll
-    for (int r = 0; r < SI; r++) v[r] = r * NT + tid < S1 ? __ldcg(a.samp + r * NT + tid) : K(0);
-#pragma unroll
-    for (int r = 0; r < SI; r++)
-      if (r * NT + tid < S1) sp.q[r * NT + tid] = v[r];
   }
   __syncthreads();
   __shared__ int64_t s_route;
-  __shared__ K* s_halves;
-  if (w == 0) {  // H1 resolve by one warp (CTA 0 also writes the statistics and run lists)
+  if (sampler) {
+    if (tid == 0) s_route = __ldcg(reinterpret_cast<const long long*>(&a.st->route));
+  } else if (w == 0) {  // H1 resolve by one warp (CTA 0 also writes the statistics and run lists)
     const int64_t r = c == 0 ? presort_resolve_warp<K, true>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
                                                              a.force, a.merge_ok)
                              : presort_resolve_warp<K, false>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
                                                               a.force, a.merge_ok);
-    if (lane == 0) s_route = r;
-  } else {  // meanwhile: merge the sorted sample pieces pairwise until two halves remain
-    const int wt = tid - 32, nth = NT - 32;
-    const int per = (S1 + nth - 1) / nth;  // outputs per thread per round
-    const int d0 = wt * per;
-    K* src = sp.q;
-    K* dst = sp.mrg;
-    for (int R = QS; R < H1; R *= 2) {
-      for (int d = d0; d < d0 + per && d < S1;) {
-        const int m = d / (2 * R);  // which pairwise merge
-        const K* A = src + m * 2 * R;
-        const K* B = A + R;
-        const int dm = d - m * 2 * R;
-        const int cnt = min(d0 + per, (m + 1) * 2 * R) - d;
-        int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, dm);
-        int j = dm - i;
-        for (int k = 0; k < cnt; k++) {
-          const bool tA = j >= R || (i < R && !(B[j] < A[i]));
-          dst[d + k] = tA ? A[i] : B[j];
-          i += tA;
-          j += !tA;
-        }
-        d += cnt;
+    if (lane == 0) {
+      s_route = r;
+      if (c == 0) {  // the route is in a.st: tell the samplers
+        __threadfence();
+        atomicAdd(a.arrive, 1u);
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(NT - 32) : "memory");  // the merging warps only
-      K* t = src;
-      src = dst;
-      dst = t;
     }
-    if (wt == 0) s_halves = src;
   }
   __syncthreads();
   const int64_t route = s_route;
@@ -712,11 +701,43 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     res_exit(a);
     return;
   }
+  grid.sync();
+
+  // ================= C: splitters; tile-local bucket grouping =================
+  {  // the sorted quarters, merged pairwise (q0+q1 -> mrg[0, H1), q2+q3 -> mrg[H1, S1))
+    constexpr int SI = SM::S1MAX / NT;
+    K v[SI];
+#pragma unroll
+    for (int r = 0; r < SI; r++) v[r] = r * NT + tid < S1 ? __ldcg(a.samp + r * NT + tid) : K(0);
+#pragma unroll
+    for (int r = 0; r < SI; r++)
+      if (r * NT + tid < S1) sp.q[r * NT + tid] = v[r];
+    __syncthreads();
+    static_assert(kResSamplers == 4, "one pairwise merge round");
+    const int R = QS, per = (S1 + NT - 1) / NT, d0 = tid * per;
+    for (int d = d0; d < d0 + per && d < S1;) {
+      const int m = d / (2 * R);  // which pairwise merge
+      const K* A = sp.q + m * 2 * R;
+      const K* B = A + R;
+      const int dm = d - m * 2 * R;
+      const int cnt = min(d0 + per, (m + 1) * 2 * R) - d;
+      int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, dm);
+      int j = dm - i;
+      for (int k = 0; k < cnt; k++) {
+        const bool tA = j >= R || (i < R && !(B[j] < A[i]));
+        sp.mrg[d + k] = tA ? A[i] : B[j];
+        i += tA;
+        j += !tA;
+      }
+      d += cnt;
+    }
+    __syncthreads();
+  }
   const int m1 = a.B1 - 1;
   const int depth1 = tree_depth(m1);
   {  // splitter j = element O1 (j+1) of the merged halves (R9, R14), with its gamma flag
-    const K* A0 = s_halves;
-    const K* A1 = s_halves + H1;
+    const K* A0 = sp.mrg;
+    const K* A1 = sp.mrg + H1;
     for (int j = tid; j < B1MAX; j += NT) {  // the splitter copy at tree1[B1MAX + j] lives outside the union
       K t = KeyTraits<K>::max_key();
       uint8_t f = 0;

@@ -69,12 +69,15 @@ struct ThreadState {
   sr::ResDone* done_h = nullptr;
   sr::ResDone* done_d = nullptr;
   uint32_t done_seq = 0;
+  uint32_t* arrive = nullptr;  // resident route-step arrival counter (device, zeroed once, never reset)
+  uint32_t arrive_base = 0;
   ~ThreadState() {
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
     if (up) cudaFreeHost(up);
     if (up_done) cudaEventDestroy(up_done);
     if (done_h) cudaFreeHost(done_h);
+    if (arrive) cudaFree(arrive);
   }
 };
 thread_local ThreadState t_state;
@@ -1054,6 +1057,13 @@ struct Sorter {
     }
     a.done = ts.done_d;
     a.seq = ++ts.done_seq == 0 ? ++ts.done_seq : ts.done_seq;
+    if (!ts.arrive) {
+      check_cuda(cudaMalloc((void**)&ts.arrive, 256), "cudaMalloc(arrive)");
+      check_cuda(cudaMemset(ts.arrive, 0, 256), "cudaMemset(arrive)");
+      ts.arrive_base = 0;
+    }
+    a.arrive = ts.arrive;
+    a.arrive_base = ts.arrive_base;
     a.S1 = S1;
     a.B1 = B1;
     a.samp = c.alloc<K>(S1);
@@ -1075,6 +1085,7 @@ struct Sorter {
       void* args[] = {&a};
       check_cuda(cudaLaunchCooperativeKernel((void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
+    ts.arrive_base += (uint32_t)P + 1u;  // every CTA arrives once, CTA 0 once more (route published)
     hostprof("launched");
     DevStats hs = c.await_done(ts.done_h, a.seq);
     hostprof("read back");
