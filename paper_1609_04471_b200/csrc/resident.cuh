@@ -566,7 +566,10 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     }
   }
   constexpr int UA = 16;  // keys per thread per load round
-  for (int t = c; t < a.G; t += P) {
+  // tiles t = c + k PS go to the CTAs c < PS = P - kResSamplers; the samplers
+  // scan none, so their sample sorts start at once
+  const int PS = P - kResSamplers;
+  for (int t = c; c < PS && t < a.G; t += PS) {
     const int64_t t0 = (int64_t)t * a.tile;
     const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
     int cd = 0, ca = 0, cv = 0;
@@ -768,12 +771,12 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   res_build_tree<K, B1MAX>(depth1, sm.tree1);
   __syncthreads();
   SR_RES_STAMP(3);
-  const int ngm = a.NG > c ? (a.NG - 1 - c) / P + 1 : 0;  // groups of this CTA: t = c + k P, k < ngm <= GPC
+  const int ngm = (c < PS && a.NG > c) ? (a.NG - 1 - c) / PS + 1 : 0;  // groups of this CTA: t = c + k PS, k < ngm <= GPC
   {
     typename SM::CT& ct = sm.u.ct;
     constexpr int U = kResGrp / NT;
     for (int k = 0; k < ngm; k++) {
-      const int t = c + k * P;
+      const int t = c + k * PS;
       const int64_t t0 = (int64_t)t * a.tile;
       const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
       SR_RES_SUB(0);
@@ -864,7 +867,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
      // filled in E
     typename SM::CT& ct = sm.u.ct;
     for (int k = 0; k < ngm; k++) {
-      const int t = c + k * P;
+      const int t = c + k * PS;
       {
         constexpr int BI = (SM::NB1 + NT - 1) / NT;
         uint32_t go[BI];

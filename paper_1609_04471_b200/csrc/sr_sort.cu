@@ -1003,8 +1003,8 @@ struct Sorter {
     if (HAS_V || !g_resident || n <= kCap || n > ResCfg<K>::MAXN) return false;
     if (g_force_route == SR_ROUTE_MERGE && !nested) return false;  // forced merge: the multi-kernel planner
     const int P = resident_grid();
-    // every CTA holds <= GPC tiles, the samplers one
-    return P >= 16 && n <= (int64_t)(ResSmem<K>::GPC * P - kResSamplers) * kResGrp;
+    // every CTA but the samplers holds <= GPC tiles
+    return P >= 16 && n <= (int64_t)ResSmem<K>::GPC * (P - kResSamplers) * kResGrp;
   }
 
   void run_resident() {
@@ -1015,7 +1015,7 @@ struct Sorter {
     // CTA gets <= GPC tiles and the last kResSamplers CTAs (the samplers) one
     // (each held tile costs a pass over the bucket tables: as few per CTA as fit)
     const int64_t gpc = std::min<int64_t>(ResSmem<K>::GPC, ceil_div<int64_t>(n, (int64_t)(P - kResSamplers) * kResGrp));
-    const int64_t slots = gpc * P - kResSamplers;
+    const int64_t slots = gpc * (P - kResSamplers);  // the samplers hold no tile
     const int64_t tile = std::min<int64_t>(kResGrp, ceil_div<int64_t>(ceil_div<int64_t>(n, slots), kResNT) * kResNT);
     const int64_t G = ceil_div<int64_t>(n, tile);
     constexpr int CAPB = ResCfg<K>::CAPB;
