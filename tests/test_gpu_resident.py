@@ -118,3 +118,51 @@ def test_resident_stream_and_repeat():
     s.synchronize()
     for k, d in zip(ks, ds):
         assert np.array_equal(d.cpu().numpy(), oracle.sort_keys(k))
+
+
+def test_resident_host_threads_concurrent():
+    """Resident sorts from several host threads at once, each on its own stream:
+    every thread has its own completion record and arrival counters (and the
+    GPU may run only one cooperative launch at a time: they serialise, never
+    interleave their barriers)."""
+    import threading
+    ks = [gen.make(o, 700_001, np.int32, config=13, instance=i)
+          for i, o in enumerate(["random", "reversed", "few_unique", "sorted", "nearly", "organ_pipe"])]
+    outs = [None] * len(ks)
+    errs = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    d = torch.from_numpy(ks[i].copy()).cuda()
+                    sr.sort_keys(d)
+                s.synchronize()
+                outs[i] = d.cpu().numpy()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(ks))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k, o in zip(ks, outs):
+        assert np.array_equal(o, oracle.sort_keys(k))
+
+
+def test_resident_many_calls_counters():
+    """Hundreds of consecutive resident calls: the persistent arrival counters
+    advance by a fixed amount per launch and never desynchronise."""
+    k = gen.make("random", 20_000, np.int32, config=14)
+    e = oracle.sort_keys(k)
+    d = torch.empty(k.size, dtype=torch.int32, device="cuda")
+    src = torch.from_numpy(k).cuda()
+    for _ in range(300):
+        d.copy_(src)
+        sr.sort_keys(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), e)
+    assert sr.last_plan()["launches"] == 1
