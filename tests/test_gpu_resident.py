@@ -166,3 +166,23 @@ def test_resident_many_calls_counters():
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), e)
     assert sr.last_plan()["launches"] == 1
+
+
+@pytest.mark.parametrize("dtype,limit", [(np.int32, 2 * 144 * 8192), (np.int64, 144 * 8192)])
+def test_resident_size_limits(dtype, limit):
+    """At the resident limit (every tile-holding CTA full) the sort is one launch;
+    one key more goes to the multi-kernel path; both bit-exact."""
+    for n in (limit, limit + 1):
+        k = gen.make("random", n, dtype, config=15)
+        p = check(k)
+        if n == limit:
+            assert p["launches"] == 1, p
+        else:
+            assert p["launches"] > 1, p
+
+
+@pytest.mark.parametrize("n", [8193, 9000, 20_000, 70_001])
+def test_resident_few_tiles(n):
+    """Small resident sizes: fewer tiles than CTAs (most CTAs scan nothing)."""
+    for order in ["random", "reversed", "sorted", "few_unique", "organ_pipe"]:
+        check(gen.make(order, n, np.int32, config=16))
