@@ -27,13 +27,34 @@ struct BitonicSort {
 
   __device__ __forceinline__ static K kmin(K a, K b) { return min(a, b); }
   __device__ __forceinline__ static K kmax(K a, K b) { return max(a, b); }
+  // ascending compare-exchange.  int32: two IMNMX.  int64 has no 64-bit
+  // min/max instruction, so compare once and select both outputs (6
+  // instructions instead of two full min/max expansions, 8)
+  __device__ __forceinline__ static void cex(K& x, K& y) {
+    if constexpr (sizeof(K) == 8) {
+      const bool sw = y < x;
+      const K lo = sw ? y : x, hi = sw ? x : y;
+      x = lo;
+      y = hi;
+    } else {
+      const K lo = min(x, y), hi = max(x, y);
+      x = lo;
+      y = hi;
+    }
+  }
+  // the half of a compare-exchange with partner value b that this side keeps
+  // (min for the lower side, max for the upper one; ties are interchangeable)
+  __device__ __forceinline__ static K keep(K k, K b, bool lower) {
+    if constexpr (sizeof(K) == 8) return ((b < k) == lower) ? b : k;
+    else return lower ? min(k, b) : max(k, b);
+  }
 
   // partner values of a cross-thread stage are in b[]; flip pairs r with VT-1-r
   __device__ __forceinline__ static void combine(K (&k)[VT], const K (&b)[VT], bool lower, bool flip) {
 #pragma unroll
     for (int r = 0; r < VT; r++) {
       K o = flip ? b[VT - 1 - r] : b[r];
-      k[r] = lower ? kmin(k[r], o) : kmax(k[r], o);
+      k[r] = keep(k[r], o, lower);
     }
   }
 
@@ -44,14 +65,14 @@ struct BitonicSort {
       for (int r = 0; r < VT / 2; r++) {
         const K b1 = __shfl_xor_sync(0xffffffffu, k[VT - 1 - r], mask);  // partner of k[r]
         const K b2 = __shfl_xor_sync(0xffffffffu, k[r], mask);           // partner of k[VT-1-r]
-        k[r] = lower ? kmin(k[r], b1) : kmax(k[r], b1);
-        k[VT - 1 - r] = lower ? kmin(k[VT - 1 - r], b2) : kmax(k[VT - 1 - r], b2);
+        k[r] = keep(k[r], b1, lower);
+        k[VT - 1 - r] = keep(k[VT - 1 - r], b2, lower);
       }
     } else {
 #pragma unroll
       for (int r = 0; r < VT; r++) {
         const K b = __shfl_xor_sync(0xffffffffu, k[r], mask);
-        k[r] = lower ? kmin(k[r], b) : kmax(k[r], b);
+        k[r] = keep(k[r], b, lower);
       }
     }
   }
@@ -61,11 +82,7 @@ struct BitonicSort {
     for (int j = VT / 2; j > 0; j >>= 1) {
 #pragma unroll
       for (int r = 0; r < VT; r++) {
-        if ((r & j) == 0) {
-          K x = k[r], y = k[r | j];
-          k[r] = kmin(x, y);
-          k[r | j] = kmax(x, y);
-        }
+        if ((r & j) == 0) cex(k[r], k[r | j]);
       }
     }
   }
@@ -85,11 +102,7 @@ struct BitonicSort {
         int p = t * VT + i;
         k[i] = p < count ? ks[p] : KeyTraits<K>::max_key();
       }
-      batcher_network<VT>([&](int a, int b) {
-        K x = k[a], y = k[b];
-        k[a] = kmin(x, y);
-        k[b] = kmax(x, y);
-      });
+      batcher_network<VT>([&](int a, int b) { cex(k[a], k[b]); });
     }
     int parity = 0;
     __syncthreads();  // everyone has read ks before the first cross-warp stage writes it
@@ -166,11 +179,7 @@ struct WarpBitonic {
 #pragma unroll
     for (int i = 0; i < VT; i++)
       if (lane * VT + i >= count) k[i] = KeyTraits<K>::max_key();
-    batcher_network<VT>([&](int a, int b) {
-      K x = k[a], y = k[b];
-      k[a] = BT::kmin(x, y);
-      k[b] = BT::kmax(x, y);
-    });
+    batcher_network<VT>([&](int a, int b) { BT::cex(k[a], k[b]); });
     for (int tk = 2; tk <= nl; tk <<= 1) {  // lanes per merged run
       BT::shfl_stage(k, tk - 1, (lane & (tk >> 1)) == 0, true);
       for (int jt = tk >> 2; jt >= 1; jt >>= 1) BT::shfl_stage(k, jt, (lane & jt) == 0, false);

@@ -255,11 +255,7 @@ __device__ __forceinline__ void res_group_sort(const K* src, int count, K* __res
 #pragma unroll
   for (int i = 0; i < VT; i++)
     if (gl * VT + i >= count) k[i] = KeyTraits<K>::max_key();
-  batcher_network<VT>([&](int a, int b) {
-    K x = k[a], y = k[b];
-    k[a] = BT::kmin(x, y);
-    k[b] = BT::kmax(x, y);
-  });
+  batcher_network<VT>([&](int a, int b) { BT::cex(k[a], k[b]); });
 #pragma unroll
   for (int tk = 2; tk <= GL; tk <<= 1) {  // lanes per merged run
     BT::shfl_stage(k, tk - 1, (gl & (tk >> 1)) == 0, true);
