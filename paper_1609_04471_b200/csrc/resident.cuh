@@ -78,7 +78,7 @@ template <> struct ResCfg<int64_t> {
   static constexpr int CAPB = 8192;
   static constexpr int B1MAX = 1024;
   static constexpr int O1 = 8;
-  static constexpr int GPC = 1;
+  static constexpr int GPC = 2;
   static constexpr int WCAP = 1024;
   static constexpr int TARGET = 4096;
   static constexpr int64_t MAXN = int64_t(4) << 20;

@@ -168,7 +168,7 @@ def test_resident_many_calls_counters():
     assert sr.last_plan()["launches"] == 1
 
 
-@pytest.mark.parametrize("dtype,limit", [(np.int32, 2 * 144 * 8192), (np.int64, 144 * 8192)])
+@pytest.mark.parametrize("dtype,limit", [(np.int32, 2 * 144 * 8192), (np.int64, 2 * 144 * 8192)])
 def test_resident_size_limits(dtype, limit):
     """At the resident limit (every tile-holding CTA full) the sort is one launch;
     one key more goes to the multi-kernel path; both bit-exact."""
