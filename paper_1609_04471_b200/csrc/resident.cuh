@@ -382,7 +382,7 @@ __device__ __forceinline__ int res_footprint(int len) {
 // Sort stage[0, len) (16-byte aligned, res_footprint(len) keys writable) by one
 // warp's register network, the narrowest that holds it.
 template <typename K, int WCAP>
-__device__ __noinline__ void res_warp_sort(K* stage, int len) {
+__device__ __forceinline__ void res_warp_sort(K* stage, int len) {
   if (len <= 128) WarpBitonic<K, 4>::sort(stage, len);
   else if (len <= 256) WarpBitonic<K, 8>::sort(stage, len);
   else if (len <= 512) WarpBitonic<K, 16>::sort(stage, len);
@@ -402,7 +402,7 @@ __device__ __noinline__ void res_warp_sort(K* stage, int len) {
 // Sub-buckets above WCAP keys or regions that do not fit y (heavy duplicates,
 // skew) send the bucket to the run + merge sort above.
 template <typename K, int NT>
-__device__ __noinline__ void res_bucket_sort2(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
+__device__ __forceinline__ void res_bucket_sort2(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
                                  unsigned long long* prof = nullptr) {
   constexpr int NW = NT / 32;
   constexpr int SB = kResSB, DEPTH = 4;
