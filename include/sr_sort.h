@@ -69,7 +69,9 @@ enum {
  * the host on small statistics readbacks (one for sorted / reversed /
  * single-level inputs) and returns before the GPU finishes; synchronise the
  * stream before reading keys.  Scratch: about n*(key bytes) + O(n/8) bytes,
- * stream-ordered from the device memory pool, released before return.
+ * stream-ordered from the device memory pool, released before return -- except
+ * the single-launch path (keys only, n <= 2,359,296), which waits for its
+ * kernel and keeps its scratch per host thread for the next such call.
  * Equal keys are indistinguishable, so the result is unique. */
 int32_t sr_sort_keys(void *keys, int64_t n, int32_t dtype, void *stream);
 

@@ -71,12 +71,19 @@ struct ThreadState {
   uint32_t done_seq = 0;
   uint32_t* arrive = nullptr;  // resident route-step arrival counter (device, zeroed once, never reset)
   uint32_t arrive_base = 0;
+  // resident scratch kept between calls of this thread: a resident call that
+  // finishes inside its one launch leaves no work behind (the host waited for
+  // it), so the next call can reuse the arena without a cudaMallocAsync
+  unsigned char* res_arena = nullptr;
+  size_t res_arena_bytes = 0;
+  bool res_arena_busy = false;  // a call using it did not complete in-kernel
   ~ThreadState() {
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
     if (up) cudaFreeHost(up);
     if (up_done) cudaEventDestroy(up_done);
     if (done_h) cudaFreeHost(done_h);
+    if (res_arena && !res_arena_busy) cudaFree(res_arena);
     if (arrive) cudaFree(arrive);
   }
 };
@@ -186,6 +193,12 @@ struct Ctx {
     arena_size = bytes;
     arena_off = 0;
     plan.workspace_bytes += (int64_t)bytes;
+  }
+  // carve later allocations from a caller-owned arena (not freed by this Ctx)
+  void use_arena(unsigned char* p, size_t bytes) {
+    arena = p;
+    arena_size = bytes;
+    arena_off = 0;
   }
   template <typename T>
   T* alloc(int64_t count) {
@@ -1027,8 +1040,24 @@ struct Sorter {
     if (NG > slots || G > kResMaxG) fail(SR_ERR_INTERNAL, "resident tile count");
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-      c.reserve((size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
-                         r(S1 * kw) + r(16 * n_ovf) + r(4 * (int64_t)NG * nbins) + 8 * 256));
+      const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
+                                    r(S1 * kw) + r(16 * n_ovf) + r(4 * (int64_t)NG * nbins) + 8 * 256);
+      ThreadState& tsa = t_state;
+      if (tsa.res_arena && (tsa.res_arena_busy || tsa.res_arena_bytes < bytes)) {
+        // too small: freed stream-ordered (idle, the last call completed in-kernel);
+        // busy (an earlier call failed or continued on the host): left alone
+        if (!tsa.res_arena_busy) c.allocs.push_back(tsa.res_arena);
+        tsa.res_arena = nullptr;
+      }
+      if (!tsa.res_arena) {
+        void* p = nullptr;
+        check_cuda(cudaMallocAsync(&p, bytes, c.st), "cudaMallocAsync");
+        tsa.res_arena = reinterpret_cast<unsigned char*>(p);
+        tsa.res_arena_bytes = bytes;
+      }
+      c.use_arena(tsa.res_arena, tsa.res_arena_bytes);
+      c.plan.workspace_bytes += (int64_t)tsa.res_arena_bytes;
+      tsa.res_arena_busy = true;  // until the kernel is known to have finished everything
     }
     hostprof("reserved");
     ensure_ws();
@@ -1120,6 +1149,18 @@ struct Sorter {
     c.plan.asc_breaks = hs.asc_breaks;
     c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
     if (hs.error) fail(SR_ERR_INTERNAL, "resident kernel inconsistency");
+    // the one launch finished the sort unless the host continues below: then
+    // the arena's buffers feed the continuation, so it is released with this
+    // call (stream-ordered) instead of being reused
+    const bool in_kernel = hs.route == kRouteSorted || hs.route == kRouteReversed ||
+                           (hs.route == kRoutePartition && hs.n_ovf == 0);
+    if (in_kernel) {
+      t_state.res_arena_busy = false;
+    } else {
+      c.allocs.push_back(t_state.res_arena);
+      t_state.res_arena = nullptr;
+      t_state.res_arena_busy = false;
+    }
     switch (hs.route) {
       case kRouteSorted:
         c.plan.route = SR_ROUTE_SORTED;
