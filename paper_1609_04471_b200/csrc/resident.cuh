@@ -100,6 +100,9 @@ struct ResArgs {
   int S1, B1;               // level-1 sample size, buckets (power of two <= B1MAX)
   int NG;                   // grouping units = the scan tiles (NG = G)
   K* samp;                  // S1 keys: the sorted pieces of the level-1 sample
+  K* mrg;                   // S1 keys: the sample pieces merged pairwise (each sampler writes half a merge)
+  K* spl;                   // B1MAX level-1 splitters (+inf padded), written by the samplers
+  uint8_t* spf;             // B1MAX equality flags of the splitters
   uint32_t* tot;            // 2 B1 + 1 bucket totals (zeroed in phase A)
   uint32_t* goff;           // NG x nbins: offset of group t's piece inside bucket b
   OvfSeg* ovf;              // ranges of keys left unsorted for the host's next level
@@ -107,7 +110,7 @@ struct ResArgs {
   int force, merge_ok;
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
-  uint32_t* unit_counter;   // [0] CTA units, [1] CTAs done, [2] warp units (zeroed by CTA 0 in phase A)
+  uint32_t* unit_counter;   // [0] CTA units, [1] CTAs done, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
   uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
   uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
@@ -129,6 +132,12 @@ struct ResDone {
 #define SR_RES_SUB(kk)                                                                              \
   do {                                                                                              \
     if (a.tstamp && c == 0 && k == 0 && tid == 0) a.tstamp[8 + 8 * (size_t)gridDim.x + 8 + (kk)] = res_now(); \
+  } while (0)
+
+// splitter sub-steps of sampler 0, the last CTA (SR_TIMING diagnostics)
+#define SR_RES_CSUB(kk)                                                                             \
+  do {                                                                                              \
+    if (a.tstamp && c == (int)gridDim.x - 1 && tid == 0) a.tstamp[8 + 8 * (size_t)gridDim.x + 16 + (kk)] = res_now(); \
   } while (0)
 
 #define SR_RES_STAMP(k)                                                                \
@@ -178,9 +187,8 @@ struct ResSmem {
     K stk[GPC][kResGrp];           // per held group: its keys grouped by bucket
     uint16_t stb[GPC][kResGrp];    // per held group: the bucket of stk[i]
   };
-  struct alignas(16) SP {          // C: tile summaries, the sorted sample pieces, pairwise merged
+  struct alignas(16) SP {          // route step: tile summaries; samplers: sample pieces, merged halves
     K q[S1MAX];
-    K mrg[S1MAX];
     TileSummary ts[kResMaxG];
   };
   struct alignas(16) E {
@@ -687,11 +695,22 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     return;
   }
   if (route == kRouteReversed) {
-    const int64_t half = n / 2;
-    for (int64_t p = (int64_t)c * NT + tid; p < half; p += (int64_t)P * NT) {
-      const K x = a.keys[p], y = a.keys[n - 1 - p];
-      a.keys[p] = y;
-      a.keys[n - 1 - p] = x;
+    // UR pairs per thread in flight (a dependent load/store pair per thread
+    // and round would leave the reversal latency-bound)
+    constexpr int UR = 8;
+    const int64_t half = n / 2, stride = (int64_t)P * NT;
+    for (int64_t p0 = (int64_t)c * NT + tid; p0 < half; p0 += UR * stride) {
+      K x[UR], y[UR];
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int64_t p = p0 + u * stride;
+        if (p < half) { x[u] = a.keys[p]; y[u] = a.keys[n - 1 - p]; }
+      }
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int64_t p = p0 + u * stride;
+        if (p < half) { a.keys[p] = y[u]; a.keys[n - 1 - p] = x[u]; }
+      }
     }
     res_exit(a);
     return;
@@ -700,44 +719,58 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     res_exit(a);
     return;
   }
-  grid.sync();
-
-  // ================= C: splitters; tile-local bucket grouping =================
-  {  // the sorted quarters, merged pairwise (q0+q1 -> mrg[0, H1), q2+q3 -> mrg[H1, S1))
-    constexpr int SI = SM::S1MAX / NT;
-    K v[SI];
-#pragma unroll
-    for (int r = 0; r < SI; r++) v[r] = r * NT + tid < S1 ? __ldcg(a.samp + r * NT + tid) : K(0);
-#pragma unroll
-    for (int r = 0; r < SI; r++)
-      if (r * NT + tid < S1) sp.q[r * NT + tid] = v[r];
-    __syncthreads();
-    static_assert(kResSamplers == 4, "one pairwise merge round");
-    const int R = QS, per = (S1 + NT - 1) / NT, d0 = tid * per;
-    for (int d = d0; d < d0 + per && d < S1;) {
-      const int m = d / (2 * R);  // which pairwise merge
-      const K* A = sp.q + m * 2 * R;
-      const K* B = A + R;
-      const int dm = d - m * 2 * R;
-      const int cnt = min(d0 + per, (m + 1) * 2 * R) - d;
-      int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, dm);
-      int j = dm - i;
-      for (int k = 0; k < cnt; k++) {
-        const bool tA = j >= R || (i < R && !(B[j] < A[i]));
-        sp.mrg[d + k] = tA ? A[i] : B[j];
-        i += tA;
-        j += !tA;
-      }
-      d += cnt;
-    }
-    __syncthreads();
-  }
   const int m1 = a.B1 - 1;
   const int depth1 = tree_depth(m1);
-  {  // splitter j = element O1 (j+1) of the merged halves (R9, R14), with its gamma flag
-    const K* A0 = sp.mrg;
-    const K* A1 = sp.mrg + H1;
-    for (int j = tid; j < B1MAX; j += NT) {  // the splitter copy at tree1[B1MAX + j] lives outside the union
+  if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
+    static_assert(kResSamplers == 4, "four sorted sample pieces");
+    // (sampler steps are counted in unit_counter[3]: CTA 0 zeroed it before
+    // publishing the route these CTAs waited for)
+    auto step = [&](uint32_t target) {  // publish this CTA's writes, wait for the other samplers'
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(a.unit_counter + 3, 1u);
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.unit_counter + 3) : "memory");
+        } while (v < target);
+      }
+      __syncthreads();
+    };
+    step(kResSamplers);
+    SR_RES_CSUB(0);
+    {  // half h = quarter / 2 of the pairwise merges (pieces 2h, 2h+1), this sampler's
+       // part of it: merged positions [part R, (part + 1) R), written to mrg[h 2R + ...]
+      const int R = QS, h = quarter >> 1, part = quarter & 1;
+      for (int i = tid; i < 2 * R; i += NT) sp.q[i] = __ldcg(a.samp + (int64_t)h * 2 * R + i);
+      __syncthreads();
+      SR_RES_CSUB(1);
+      const K* A = sp.q;
+      const K* B = sp.q + R;
+      const int per = (R + NT - 1) / NT, d0 = part * R + tid * per, d1 = min(d0 + per, (part + 1) * R);
+      if (d0 < d1) {
+        int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, d0);
+        int j = d0 - i;
+        for (int d = d0; d < d1; d++) {
+          const bool tA = j >= R || (i < R && !(B[j] < A[i]));
+          a.mrg[(int64_t)h * 2 * R + d] = tA ? A[i] : B[j];
+          i += tA;
+          j += !tA;
+        }
+      }
+    }
+    SR_RES_CSUB(4);
+    step(2 * kResSamplers);
+    SR_RES_CSUB(2);
+    // splitter j = element O1 (j+1) of the merged halves (R9, R14),
+    // with its gamma flag (more than gamma = 2 of the elements r-2 .. r+2 equal
+    // to it); this sampler's quarter of the j range, +inf padded
+    for (int i = tid; i < S1; i += NT) sp.q[i] = __ldcg(a.mrg + i);
+    __syncthreads();
+    const K* A0 = sp.q;
+    const K* A1 = sp.q + H1;
+    constexpr int JQ = B1MAX / kResSamplers;
+    for (int j = quarter * JQ + tid; j < (quarter + 1) * JQ; j += NT) {
       K t = KeyTraits<K>::max_key();
       uint8_t f = 0;
       if (j < m1) {
@@ -759,9 +792,17 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         const bool p1e = r + 1 < S1 && win[k + 1] == t, p2e = r + 2 < S1 && win[k + 2] == t;
         f = ((m1e && m2e) || (m1e && p1e) || (p1e && p2e)) ? 1 : 0;  // count > gamma = 2
       }
-      sm.tree1[B1MAX + j] = t;
-      sm.eq1[j] = f;
+      a.spl[j] = t;
+      a.spf[j] = f;
     }
+    SR_RES_CSUB(3);
+  }
+  grid.sync();
+
+  // ================= C: splitter tree; tile-local bucket grouping =================
+  for (int j = tid; j < B1MAX; j += NT) {  // the splitter copy at tree1[B1MAX + j] lives outside the union
+    sm.tree1[B1MAX + j] = __ldcg(a.spl + j);
+    sm.eq1[j] = __ldcg(a.spf + j);
   }
   __syncthreads();
   res_build_tree<K, B1MAX>(depth1, sm.tree1);

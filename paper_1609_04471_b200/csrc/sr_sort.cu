@@ -77,7 +77,25 @@ struct ThreadState {
   unsigned char* res_arena = nullptr;
   size_t res_arena_bytes = 0;
   bool res_arena_busy = false;  // a call using it did not complete in-kernel
+  // the resident kernel as a cooperative node of an instantiated one-node CUDA
+  // graph, its parameters replaced per call: cudaGraphExecKernelNodeSetParams +
+  // cudaGraphLaunch take ~3.5 us less host time than cudaLaunchCooperativeKernel
+  // for a 148-CTA, ~210 KB-smem launch (tools/micro/coopgraph.cu)
+  struct CoopGraph {
+    const void* func = nullptr;
+    int dev = -1;
+    unsigned P = 0;
+    size_t smem = 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaGraphNode_t node = nullptr;
+  };
+  CoopGraph coop[4];
   ~ThreadState() {
+    for (auto& cg : coop) {
+      if (cg.ge) cudaGraphExecDestroy(cg.ge);
+      if (cg.g) cudaGraphDestroy(cg.g);
+    }
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
     if (up) cudaFreeHost(up);
@@ -107,6 +125,50 @@ struct SrError {
 void check_cuda(cudaError_t e, const char* what) {
   if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); fail(SR_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e)); }
   if (e != cudaSuccess) fail(SR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// cooperative launch of func through this thread's cached graph node (see
+// ThreadState::CoopGraph); SR_NO_GRAPH=1 launches it directly
+cudaError_t launch_coop(const void* func, unsigned P, unsigned NT, void** args, size_t smem, cudaStream_t st) {
+  static const bool direct = getenv("SR_NO_GRAPH") != nullptr;
+  if (direct) return cudaLaunchCooperativeKernel(func, P, NT, args, smem, st);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaKernelNodeParams kp = {};
+  kp.func = const_cast<void*>(func);
+  kp.gridDim = dim3(P);
+  kp.blockDim = dim3(NT);
+  kp.sharedMemBytes = (unsigned)smem;
+  kp.kernelParams = args;
+  ThreadState::CoopGraph* cg = nullptr;
+  for (auto& x : t_state.coop)
+    if (x.func == func && x.dev == dev && x.P == P && x.smem == smem) { cg = &x; break; }
+  if (cg) {
+    e = cudaGraphExecKernelNodeSetParams(cg->ge, cg->node, &kp);
+    if (e != cudaSuccess) return e;
+    return cudaGraphLaunch(cg->ge, st);
+  }
+  ThreadState::CoopGraph* slot = nullptr;
+  for (auto& x : t_state.coop)
+    if (!x.func) { slot = &x; break; }
+  if (!slot) return cudaLaunchCooperativeKernel(func, P, NT, args, smem, st);  // cache full
+  ThreadState::CoopGraph n;
+  cudaLaunchAttributeValue v = {};
+  v.cooperative = 1;
+  if ((e = cudaGraphCreate(&n.g, 0)) != cudaSuccess) return e;
+  if ((e = cudaGraphAddKernelNode(&n.node, n.g, nullptr, 0, &kp)) != cudaSuccess ||
+      (e = cudaGraphKernelNodeSetAttribute(n.node, cudaLaunchAttributeCooperative, &v)) != cudaSuccess ||
+      (e = cudaGraphInstantiate(&n.ge, n.g, 0)) != cudaSuccess) {
+    cudaGraphDestroy(n.g);
+    return e;
+  }
+  n.func = func;
+  n.dev = dev;
+  n.P = P;
+  n.smem = smem;
+  *slot = n;
+  return cudaGraphLaunch(slot->ge, st);
 }
 
 void* pinned(size_t bytes) {
@@ -1041,7 +1103,8 @@ struct Sorter {
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
       const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
-                                    r(S1 * kw) + r(16 * n_ovf) + r(4 * (int64_t)NG * nbins) + 8 * 256);
+                                    2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
+                                    r(4 * (int64_t)NG * nbins) + 8 * 256);
       ThreadState& tsa = t_state;
       if (tsa.res_arena && (tsa.res_arena_busy || tsa.res_arena_bytes < bytes)) {
         // too small: freed stream-ordered (idle, the last call completed in-kernel);
@@ -1096,6 +1159,9 @@ struct Sorter {
     a.S1 = S1;
     a.B1 = B1;
     a.samp = c.alloc<K>(S1);
+    a.mrg = c.alloc<K>(S1);
+    a.spl = c.alloc<K>(ResCfg<K>::B1MAX);
+    a.spf = c.alloc<uint8_t>(ResCfg<K>::B1MAX);
     a.goff = c.alloc<uint32_t>((int64_t)NG * nbins);
     a.NG = NG;
     a.ovf = c.alloc<OvfSeg>(n_ovf);
@@ -1106,25 +1172,31 @@ struct Sorter {
     a.merge_ok = route_ok() | kOutlierStrict;
     a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
-    a.tstamp = stamps ? c.alloc<unsigned long long>(8 + 8 * P + 16) : nullptr;
-    if (stamps) c.memset0(a.tstamp, 64 * (P + 3));
+    a.tstamp = stamps ? c.alloc<unsigned long long>(8 * P + 32) : nullptr;
+    if (stamps) c.memset0(a.tstamp, 64 * (P + 4));
     const size_t smem = sizeof(ResSmem<K>);
     hostprof("prepared");
     const int h = c.launch("resident", n * kw, [&] {
       void* args[] = {&a};
-      check_cuda(cudaLaunchCooperativeKernel((void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
+      check_cuda(launch_coop((const void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
     ts.arrive_base += (uint32_t)P + 1u;  // every CTA arrives once, CTA 0 once more (route published)
     hostprof("launched");
     DevStats hs = c.await_done(ts.done_h, a.seq);
     hostprof("read back");
     if (stamps) {
-      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 3)));
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 4)));
       {
         const unsigned long long* q = t + 8 + 8 * P + 8;
         if (q[0] && q[5])
           fprintf(stderr, "[sr_resident] C group0 us: classify %.1f count %.1f tables+atomics %.1f scan %.1f scatter %.1f\n",
                   (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3, (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3);
+      }
+      {
+        const unsigned long long* q = t + 8 + 8 * P + 16;
+        if (q[0] && q[2])
+          fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
+                  (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
       }
       {
         const unsigned long long* e = t + 8 + 8 * P;
