@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   }
   // the samplers sort their sample quarter meanwhile (wasted only on the
   // sorted / reversed routes, which the other CTAs finish without them)
-  if (sampler) {  // the quarter: 128-key register runs + merge-path rounds, written to a.samp
+  if (sampler) {  // the quarter, sorted and written to a.samp
     typename SM::E& e = sm.u.e;
 #pragma unroll
     for (int r = 0; r < SG; r++) {
@@ -650,7 +650,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       if (q < QS) e.x[q] = sx[r];
     }
     __syncthreads();
-    res_bucket_sort<K, NT>(a.samp + (int64_t)quarter * QS, QS, e, nullptr);
+    BitonicSort<K, NT, SG>::sort(e.x, QS);  // register / shuffle bitonic network, QS <= NT SG keys
+    for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = e.x[q];
   }
   SR_RES_STAMP(1);
   // samplers take the route CTA 0 publishes (one more arrival) instead of
