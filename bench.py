@@ -168,7 +168,7 @@ def ncu_traffic(kernel: str, dtype_name: str, workload: str):
     ncu --set full summary of the same workload (profiles/*_ncu_summary.json,
     "workload" field), else None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")))  # tags sort by round/session (r1_ < r1s2 < r1s3 < r1s3f < r1s4); mtimes do not survive a checkout
     pref = NCU_NAMES.get(kernel)
     for f in reversed(files):
         try:
