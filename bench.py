@@ -418,7 +418,7 @@ def main():
     bytes_per_launch = d["bytes"] / d["launches"]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     kern_total = sum(v["ms"] for v in kern.values())
-    tr = ncu_traffic(dname, "int" if kw == 4 else "long", wl)
+    tr = ncu_traffic(dname, "int" if elem_bytes(dtype) == 4 else "long", wl)
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": tr["bytes"] if tr else None,
                 "traffic_source": tr, "algorithmic_bytes_per_launch": int(bytes_per_launch),
