@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """bench.py -- Mkeys/s of the B200 adaptive sort on BASELINE.json's workloads.
 
-Default workload (N=1): configs[1] ("C2"): n = 2,000,000 int32 keys, four
-orders (random, reversely sorted, nearly sorted = n/100 swaps, few unique = 10
+Default line (N=1): configs[1] ("c2"): n = 2,000,000 int32 keys, four orders
+(random, reversely sorted, nearly sorted = n/100 swaps, few unique = 10
 values).  One STEP = one sort of one instance of each of the four orders
-(8,000,000 keys).  value = keys sorted / summed device time of the sorts.
+(8,000,000 keys); value = keys sorted / summed device time of the sorts.  The
+same line carries, under "c5a", configs[4]'s 256M-key int32 random sort (the
+metric's "n=2M/256M" second half), measured the same way in the same run.
 
 Timing: every sort is bracketed by CUDA events on the sort's stream.  Before
 each sort the input is restored from a pristine device copy and L2 is flushed
@@ -13,8 +15,15 @@ steps are bracketed by barrier + synchronize on both sides and the max over
 ranks is taken.  e2e: the same metric through sr_sort_host (HOST pinned
 buffers; H2D copy, sort, D2H copy and stream sync inside the events).
 
+Every timed output is checked after the timed region: on rank 0 at N=1 the
+cpu_baseline leg runs the oracle (single-threaded, pinned to one core) on the
+very instances the GPU sorted and compares bit for bit; elsewhere the output is
+checked on the device by properties (sorted, multiset fingerprints, payload
+invariants).  A failed check exits non-zero.
+
 --impl reference runs the CPU oracle (the reference arm for this tier: a plain
-single-threaded mergesort, oracle/) on a bounded sample of the same workload.
+single-threaded mergesort, oracle/) on a bounded sample of the same workload,
+and prints the same metric and config.
 """
 from __future__ import annotations
 
@@ -35,6 +44,8 @@ sys.path.insert(0, ROOT)
 from workloads import gen  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# BASELINE.json metric, printed verbatim by both arms (the driver pairs them on it)
+METRIC = "Mkeys/s sorted (int32, n=2M/256M, 4 input types); achieved HBM GB/s vs peak"
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 WORKLOADS = {
@@ -209,9 +220,37 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+def pin_one_core():
+    """Pin this process to one host core for the oracle legs (BASELINE.md §3);
+    returns (restore-set, core) or (None, None) where affinity is unsupported."""
+    try:
+        old = os.sched_getaffinity(0)
+        core = min(old)
+        os.sched_setaffinity(0, {core})
+        return old, core
+    except Exception:
+        return None, None
+
+
+def unpin(old):
+    if old:
+        try:
+            os.sched_setaffinity(0, old)
+        except Exception:
+            pass
+
+
+def ref_config(wl):
+    """The workload description both arms print (the driver pairs the arms on
+    metric + config)."""
+    n, dtype, orders, cfg = WORKLOADS[wl]
+    return {"workload": wl, "n": n, "dtype": dtype_label(dtype), "pairs": wl in PAIRS, "orders": orders,
+            "keys_per_step": n * len(orders),
+            "l2": "flushed (512 MiB write) before every sort, outside the timed region"}
+
+
 def run_reference(args, wl):
     """Reference arm: the CPU oracle on a bounded sample of the workload."""
-    import oracle
     ws, rank, _ = dist_env()
     if rank != 0:
         return
@@ -219,79 +258,89 @@ def run_reference(args, wl):
     budget = float(os.environ.get("SR_REF_BUDGET_S", "20"))
     # bounded sample: the first `m` keys of each order's instance, m chosen so a step is ~budget/(steps+warmup) s
     per_step = budget / max(1, args.steps + args.warmup)
-    m = min(n, max(10_000, int(per_step / (len(orders) * 1.2e-7) )))  # ~120 ns/key oracle estimate
+    m = min(n, max(10_000, int(per_step / (len(orders) * 1.2e-7))))  # ~120 ns/key oracle estimate
     inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
-    for _ in range(args.warmup):
-        for a in inputs:
-            oracle_sort(a, wl in PAIRS)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for a in inputs:
-            oracle_sort(a, wl in PAIRS)
-    dt = (time.perf_counter() - t0) / args.steps
+    old, core = pin_one_core()
+    try:
+        for _ in range(args.warmup):
+            for a in inputs:
+                oracle_sort(a, wl in PAIRS)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for a in inputs:
+                oracle_sort(a, wl in PAIRS)
+        dt = (time.perf_counter() - t0) / args.steps
+    finally:
+        unpin(old)
     keys = m * len(orders)
     v = keys / dt / 1e6
-    line = {"impl": "reference", "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types)", "value": round(v, 3),
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3),
             "unit": "Mkeys/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": dtype_label(dtype), "data": "synthetic",
-            "config": {"workload": wl, "n": n, "orders": orders, "sample_keys_per_order": m},
+            "dtype": dtype_label(dtype), "data": "synthetic", "config": ref_config(wl),
             "cpu_baseline": {"value": round(v, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {m} keys of instance 0 of each order, single-threaded C mergesort"},
+                             "sample": f"first {m} keys of instance 0 of each order, single-threaded C mergesort"
+                                       + (f" pinned to core {core}" if core is not None else "")},
             "e2e": {"value": round(v, 3), "unit": "Mkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(wl, budget_s=12.0):
-    """The oracle as it stands, single-threaded, on a bounded sample (whole instances while within budget)."""
-    import oracle
-    n, dtype, orders, cfg = WORKLOADS[wl]
-    m = n if n <= 4_000_000 else 4_000_000
-    inputs = [make_input(o, n, dtype, cfg, 0)[:m].copy() for o in orders]
-    keys = 0
-    t_sort = 0.0
-    rounds = 0
-    while t_sort < budget_s and rounds < 10:
-        for a in inputs:
-            t0 = time.perf_counter()
-            oracle_sort(a, wl in PAIRS)
-            t_sort += time.perf_counter() - t0
-            keys += a.shape[0]
-        rounds += 1
-    sample = (f"{rounds} x instance 0 of each of {orders}, " + (f"n={n}" if m == n else f"first {m} keys of n={n}"))
-    return {"value": round(keys / t_sort / 1e6, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
-            "sample": sample, "host_cpus": os.cpu_count()}
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
-    wl = args.workload
-
-    if args.impl == "reference":
-        run_reference(args, wl)
-        return
-
+# ----------------------------------------------------------------------------- output checks
+def _fp_dev(t):
+    """Two commutative 64-bit fingerprints of a device tensor's multiset of
+    bit patterns (wrapping int64 arithmetic; same function on input and output)."""
     import torch
-    import paper_1609_04471_b200 as sr
+    x = t.reshape(-1)
+    x = x.view(torch.int32).to(torch.int64) if x.element_size() == 4 else x.view(torch.int64)
+    h1 = (x * -7046029254386353131) ^ (x >> 29)
+    h2 = (x ^ -2889434331225346157) * -6884282663029091281
+    return int(h1.sum()), int(h2.sum())
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.current_stream()
+
+def _total_order_image(t):
+    """Signed-integer image of float keys in IEEE totalOrder (test-side check)."""
+    import torch
+    if t.dtype == torch.float32:
+        b = t.view(torch.int32)
+        return b ^ ((b >> 31) & 0x7FFFFFFF)
+    if t.dtype == torch.float64:
+        b = t.view(torch.int64)
+        return b ^ ((b >> 63) & 0x7FFFFFFFFFFFFFFF)
+    return t
+
+
+def check_props(out_k, in_k, out_v=None, in_v=None):
+    """Properties every correct output has, checked on the device (used where
+    the oracle does not run: ranks > 0, N > 1, --no-cpu-baseline): keys
+    non-decreasing (totalOrder for floats), same multiset as the input; for
+    pairs with payload = original index: out_key == in_key[out_val], the
+    payload a permutation, and increasing among equal keys (stability)."""
+    import torch
+    if out_k.dim() == 2:  # records: multiset only (the oracle leg checks order)
+        return _fp_dev(out_k) == _fp_dev(in_k)
+    img = _total_order_image(out_k)
+    if img.numel() > 1 and not bool((img[1:] >= img[:-1]).all()):
+        return False
+    if _fp_dev(out_k) != _fp_dev(in_k):
+        return False
+    if out_v is not None:
+        vi = out_v.view(torch.int32).to(torch.int64)
+        if not torch.equal(out_k, in_k[vi]):
+            return False
+        if not torch.equal(torch.sort(vi).values, torch.arange(vi.numel(), device=vi.device)):
+            return False
+        same = out_k[1:] == out_k[:-1]
+        if not bool((vi[1:] > vi[:-1])[same].all()):
+            return False
+    return True
+
+
+# ----------------------------------------------------------------------------- one workload
+def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
+    """Time K steps of workload `wl` (one step = one sort of one instance of
+    each order), then e2e through the host API, a per-kernel profile pass, and
+    the output checks.  Returns the fields of a bench line."""
+    import torch
     n, dtype, orders, cfg = WORKLOADS[wl]
     rec = is_rec(dtype)
     pairs = wl in PAIRS
@@ -299,20 +348,20 @@ def main():
                                    "float64": torch.float64}[np.dtype(dtype).name]
     kw = elem_bytes(dtype) + (4 if pairs else 0)  # bytes per element (key + payload)
     shape = (n, dtype[1]) if rec else (n,)
+    steps, warm = args.steps, args.warmup
 
-    # inputs: instance = rank * (steps+warmup) + step  (weak scaling: independent problems per rank)
-    total = args.steps + args.warmup
+    # inputs: instance = rank * (steps+warmup) + step  (weak scaling: independent problems per rank);
+    # 1 GiB workloads sort one instance per order every step
+    total = steps + warm
     big = n >= 50_000_000
     ninst = 1 if big else total
-    pristine = {}
-    host_inputs = {}
+    pristine, host_inputs = {}, {}
     ids = instance_ids(rank, total)
     for o in orders:
         for i in range(ninst):
             a = make_input(o, n, dtype, cfg, ids[i])
             pristine[(o, i)] = torch.from_numpy(a).to(dev)
-            if i == 0:
-                host_inputs[o] = a
+            host_inputs[(o, i)] = a
     work = torch.empty(shape, dtype=tdt, device=dev)
     if pairs:  # configs[3]: payload = each element's original index (int32)
         vals_pristine = torch.from_numpy(gen.index_payload(n).view(np.int32)).to(dev)
@@ -336,47 +385,116 @@ def main():
             ev[1].record(stream)
         return sr.last_plan()
 
-    for w in range(args.warmup):
+    for w in range(warm):
         for o in orders:
             one_sort(o, w)
     torch.cuda.synchronize()
 
-    # ---- timed region
+    # ---- timed region (outputs kept, untimed, for the checks after it)
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in orders]
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     plans = []
+    kept = {}          # small workloads: every timed output, on the device
+    first_big = {}     # big workloads: the first timed output per order; later ones compared to it
+    big_same = True
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clk:
         t_wall0 = time.perf_counter()
-        for s in range(args.steps):
+        for s in range(steps):
             for j, o in enumerate(orders):
-                plans.append((o, one_sort(o, args.warmup + s, evs[s][j])))
+                plans.append((o, one_sort(o, warm + s, evs[s][j])))
+                if big:
+                    if o not in first_big:
+                        first_big[o] = (work.clone(), work_v.clone() if pairs else None)
+                    else:
+                        big_same &= torch.equal(first_big[o][0], work) and (not pairs or torch.equal(first_big[o][1], work_v))
+                else:
+                    kept[(o, warm + s)] = (work.clone(), work_v.clone() if pairs else None)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     if ws > 1:
         torch.distributed.barrier()
-    per_order_ms = {o: [evs[s][j][0].elapsed_time(evs[s][j][1]) for s in range(args.steps)] for j, o in enumerate(orders)}
-    step_ms = [sum(evs[s][j][0].elapsed_time(evs[s][j][1]) for j in range(len(orders))) for s in range(args.steps)]
+    per_order_ms = {o: [evs[s][j][0].elapsed_time(evs[s][j][1]) for s in range(steps)] for j, o in enumerate(orders)}
+    step_ms = [sum(evs[s][j][0].elapsed_time(evs[s][j][1]) for j in range(len(orders))) for s in range(steps)]
     total_ms = max_over_ranks(sum(step_ms), dev)
-    keys_all = n * len(orders) * args.steps * ws
+    keys_all = n * len(orders) * steps * ws
     value = keys_all / (total_ms / 1e3) / 1e6
     launches = sum(p["launches"] for _, p in plans)
-    bytes_planned = sum(p["bytes_planned"] for _, p in plans) / args.steps
+    bytes_planned = sum(p["bytes_planned"] for _, p in plans) / steps
+    route_of = {o: p["route_name"] for o, p in plans[:len(orders)]}
+
+    # ---- output checks (untimed): exact against the oracle in the oracle leg, properties elsewhere
+    check = {"checked": 0, "failed": 0, "how": ""}
+    cpu = None
+    if big:
+        to_check = [(o, 0, first_big[o]) for o in orders]
+        check["repeat_identical"] = bool(big_same)
+    else:
+        to_check = [(o, idx, kept[(o, idx)]) for (o, idx) in kept]
+    if oracle_leg:
+        # the cpu_baseline leg: the oracle, single-threaded and pinned to one core,
+        # sorts the very instances the GPU sorted (bounded: <= ~30 s of host work);
+        # its outputs are the expected values of the exact comparison
+        old, core = pin_one_core()
+        t_sort, keys_done, n_sorts = 0.0, 0, 0
+        budget = float(os.environ.get("SR_ORACLE_BUDGET_S", "30"))
+        try:
+            for (o, idx, (gk, gv)) in to_check:
+                if t_sort > budget:
+                    break
+                a = host_inputs[(o, idx % ninst)]
+                t0 = time.perf_counter()
+                exp = oracle_sort(a, pairs)
+                t_sort += time.perf_counter() - t0
+                keys_done += n
+                n_sorts += 1
+                if pairs:
+                    ok = np.array_equal(gk.cpu().numpy(), exp[0]) and \
+                        np.array_equal(gv.cpu().numpy().view(np.uint32), exp[1].view(np.uint32))
+                else:
+                    g = gk.cpu().numpy()
+                    ok = np.array_equal(g.view(np.uint8), np.ascontiguousarray(exp).view(np.uint8))
+                check["checked"] += 1
+                check["failed"] += 0 if ok else 1
+        finally:
+            unpin(old)
+        for (o, idx, (gk, gv)) in to_check[n_sorts:]:  # beyond the oracle budget: properties
+            check["checked"] += 1
+            inp = pristine[(o, idx % ninst)]
+            check["failed"] += 0 if check_props(gk, inp, gv, vals_pristine if pairs else None) else 1
+        check["how"] = (f"{n_sorts} outputs bit-exact vs the oracle, "
+                        f"{len(to_check) - n_sorts} by properties (sorted, multiset fingerprints"
+                        + (", payload invariants" if pairs else "") + ")")
+        cpu = {"value": round(keys_done / t_sort / 1e6, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n_sorts} of the {len(to_check)} timed instances of {orders} (n={n}), "
+                         "single-threaded C mergesort" + (f" pinned to core {core}" if core is not None else ""),
+               "host_cpus": os.cpu_count()}
+    else:
+        for (o, idx, (gk, gv)) in to_check:
+            check["checked"] += 1
+            inp = pristine[(o, idx % ninst)]
+            check["failed"] += 0 if check_props(gk, inp, gv, vals_pristine if pairs else None) else 1
+        check["how"] = "properties on the device (sorted, multiset fingerprints" + (
+            ", payload invariants" if pairs else "") + ")"
+    if big and not big_same:
+        check["failed"] += 1
+    del kept, first_big, to_check
 
     # ---- e2e through the host API (pinned host buffers, copies inside the events)
     e2e = None
     if not args.no_e2e:
-        pin = {o: torch.from_numpy(host_inputs[o]).pin_memory() for o in orders}
+        pin = {o: torch.from_numpy(host_inputs[(o, 0)]).pin_memory() for o in orders}
         hbuf = torch.empty(shape, dtype=tdt).pin_memory()
         hb = hbuf.numpy()
+        hv = None
         if pairs:
             hvals = torch.empty(n, dtype=torch.int32).pin_memory()
             hv = hvals.numpy()
             hvals_src = torch.from_numpy(gen.index_payload(n).view(np.int32)).pin_memory()
         e2e_ms = 0.0
-        for s in range(args.warmup + args.steps):
+        for s in range(warm + steps):
             for o in orders:
                 hbuf.copy_(pin[o])
                 if pairs:
@@ -389,22 +507,23 @@ def main():
                     sr.sort_records(work)
                     hbuf.copy_(work, non_blocking=True)
                 else:
-                    sr.sort_host(hb, hv if pairs else None, stream.cuda_stream)
+                    sr.sort_host(hb, hv, stream.cuda_stream)
                 b.record(stream)
                 b.synchronize()
-                if s >= args.warmup:
+                if s >= warm:
                     e2e_ms += a.elapsed_time(b)
         e2e_ms = max_over_ranks(e2e_ms, dev)
         e2e = {"value": round(keys_all / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mkeys/s",
                "h2d_bytes_per_step": n * kw * len(orders), "d2h_bytes_per_step": n * kw * len(orders),
-               "ms_per_step": round(e2e_ms / args.steps, 4)}
+               "ms_per_step": round(e2e_ms / steps, 4)}
+        del pin, hbuf
 
     # ---- per-kernel device times (profile pass over the same inputs, CUDA events on the sort stream)
     sr.set_option(sr.OPT_PROFILE, 1)
     kern = {}
-    for s in range(args.steps):
+    for s in range(steps):
         for o in orders:
-            one_sort(o, args.warmup + s)
+            one_sort(o, warm + s)
             for name, ms, by in sr.last_profile():
                 d = kern.setdefault(name, {"ms": 0.0, "bytes": 0, "launches": 0})
                 d["ms"] += ms
@@ -412,8 +531,7 @@ def main():
                 d["launches"] += 1
     sr.set_option(sr.OPT_PROFILE, 0)
     hbm, hbm_src = peaks()
-    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
-    dname, d = dom
+    dname, d = max(kern.items(), key=lambda kv: kv[1]["ms"])
     avg_ms = d["ms"] / d["launches"]
     bytes_per_launch = d["bytes"] / d["launches"]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
@@ -426,37 +544,87 @@ def main():
                 "share_of_kernel_time": round(d["ms"] / kern_total, 3),
                 "kernels": {k: {"ms_per_launch": round(v["ms"] / v["launches"], 4),
                                 "GBps": round(v["bytes"] / v["launches"] / (v["ms"] / v["launches"] / 1e3) / 1e9, 1),
-                                "launches_per_step": v["launches"] / args.steps} for k, v in kern.items()}}
-    step_ms_mean = total_ms / args.steps
-    route_of = {o: p["route_name"] for o, p in plans[:len(orders)]}
-
-    line = {
-        "metric": "Mkeys/s sorted (int32, n=2M/256M, 4 input types); achieved HBM GB/s vs peak",
-        "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(step_ms_mean, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": dtype_label(dtype) + ("+u32 payload" if pairs else ""), "data": "synthetic",
-        "config": {"workload": wl, "pairs": pairs, "n": n, "orders": orders, "keys_per_step_per_gpu": n * len(orders),
-                   "l2": "flushed (512 MiB write) before every sort; restore+flush outside the events",
-                   "parallelism": f"independent instances per rank x{ws}",
-                   "per_order_ms_mean": {o: round(statistics.mean(v), 4) for o, v in per_order_ms.items()},
+                                "launches_per_step": v["launches"] / steps} for k, v in kern.items()}}
+    step_ms_mean = total_ms / steps
+    del pristine, work, flush
+    torch.cuda.empty_cache()
+    return {
+        "value": round(value, 2), "ms_per_step": round(step_ms_mean, 4), "dtype": dtype_label(dtype) + (
+            "+u32 payload" if pairs else ""),
+        "detail": {"per_order_ms_mean": {o: round(statistics.mean(v), 4) for o, v in per_order_ms.items()},
                    "total_of_order_means_ms": round(sum(statistics.mean(v) for v in per_order_ms.values()), 4),
-                   "routes": route_of, "wall_s": round(t_wall, 3)},
+                   "routes": route_of, "wall_s": round(t_wall, 3),
+                   "parallelism": f"independent instances per rank x{ws}"},
         "whole_step_hbm": {"bytes_planned_per_step": int(bytes_planned),
                            "GBps": round(bytes_planned / (step_ms_mean / 1e3) / 1e9, 1),
                            "frac_of_peak": round(bytes_planned / (step_ms_mean / 1e3) / 1e9 / hbm, 4),
                            "ideal_pass_frac": round(2 * n * kw * len(orders) / (step_ms_mean / 1e3) / 1e9 / hbm, 4)},
-        "roofline": roofline,
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
+        "verified": check, "cpu_baseline": cpu,
     }
-    if e2e:
-        line["e2e"] = e2e
-    if rank == 0 and not args.no_cpu_baseline and ws == 1:
-        line["cpu_baseline"] = cpu_baseline(wl)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--sub", default="c5a", help="second workload reported inside the same line ('none' to skip)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    wl = args.workload
+
+    if args.impl == "reference":
+        run_reference(args, wl)
+        return
+
+    import torch
+    import paper_1609_04471_b200 as sr
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    oracle_leg = rank == 0 and ws == 1 and not args.no_cpu_baseline
+
+    m = measure(wl, args, sr, dev, stream, rank, ws, oracle_leg)
+    sub = None
+    if args.sub and args.sub != "none" and args.sub != wl:
+        sm = measure(args.sub, args, sr, dev, stream, rank, ws, oracle_leg)
+        sub = {"workload": args.sub, "config": ref_config(args.sub), "value": sm["value"], "unit": "Mkeys/s",
+               "ms_per_step": sm["ms_per_step"], "dtype": sm["dtype"], **{k: sm[k] for k in (
+                   "detail", "whole_step_hbm", "roofline", "gpu_launches", "clocks", "e2e", "verified",
+                   "cpu_baseline")}}
+    failed = m["verified"]["failed"] + (sub["verified"]["failed"] if sub else 0)
+    line = {
+        "metric": METRIC, "value": m["value"], "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": m["dtype"], "data": "synthetic", "config": ref_config(wl),
+        "detail": m["detail"], "whole_step_hbm": m["whole_step_hbm"], "roofline": m["roofline"],
+        "gpu_launches": m["gpu_launches"], "clocks": m["clocks"], "verified": m["verified"],
+    }
+    if m["e2e"]:
+        line["e2e"] = m["e2e"]
+    if m["cpu_baseline"]:
+        line["cpu_baseline"] = m["cpu_baseline"]
+    if sub:
+        line[args.sub] = sub
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+    if failed:
+        print(f"bench: {failed} sorted outputs failed verification", file=sys.stderr, flush=True)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

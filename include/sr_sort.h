@@ -17,9 +17,17 @@
  *
  * Error behaviour (all entry points): arguments are validated before any
  * device work; on SR_ERR_INVALID_ARGUMENT / _UNSUPPORTED_DTYPE / _SIZE /
- * _ALIGNMENT / _OUT_OF_MEMORY the caller's buffers are untouched.  A CUDA
- * failure after the first kernel returns SR_ERR_CUDA, leaves the contents
- * unspecified and puts the CUDA message in sr_last_error().
+ * _ALIGNMENT the caller's buffers are untouched.  SR_ERR_OUT_OF_MEMORY from
+ * the first workspace reservation (made before any kernel that moves data;
+ * for float keys the in-place key map is undone) also leaves them untouched;
+ * an allocation failure of a later partition level leaves them holding a
+ * permutation of the input.  A CUDA failure after the first kernel returns
+ * SR_ERR_CUDA, leaves the contents unspecified and puts the CUDA message in
+ * sr_last_error().
+ *
+ * Devices: the call runs on the device that owns `keys` (made current for
+ * the call and restored afterwards); `stream` must belong to that device.
+ * Per-host-thread scratch is kept per device.
  */
 #ifndef SR_SORT_H
 #define SR_SORT_H
@@ -44,7 +52,7 @@ enum {
   SR_ERR_UNSUPPORTED_DTYPE = 2,
   SR_ERR_SIZE = 3,             /* n > 2^31 - 1 */
   SR_ERR_ALIGNMENT = 4,        /* keys not aligned to the key size or vals to 4 bytes */
-  SR_ERR_OUT_OF_MEMORY = 5,    /* workspace allocation failed (buffers untouched) */
+  SR_ERR_OUT_OF_MEMORY = 5,    /* workspace allocation failed (see "Error behaviour" above) */
   SR_ERR_CUDA = 6,
   SR_ERR_INTERNAL = 7          /* planner invariant violated (reported, never silent) */
 };
@@ -70,8 +78,11 @@ enum {
  * single-level inputs) and returns before the GPU finishes; synchronise the
  * stream before reading keys.  Scratch: about n*(key bytes) + O(n/8) bytes,
  * stream-ordered from the device memory pool, released before return -- except
- * the single-launch path (keys only, n <= 2,359,296), which waits for its
- * kernel and keeps its scratch per host thread for the next such call.
+ * the single-launch path (keys only, n <= 2,359,296), which keeps its scratch
+ * per (host thread, device) for the next such call.  That path blocks only
+ * until its kernel reports the outcome (route and bucket sizes known, mid-
+ * kernel) and returns while the kernel runs; a later single-launch call of the
+ * same thread on another stream waits on the device for the earlier kernel.
  * Equal keys are indistinguishable, so the result is unique. */
 int32_t sr_sort_keys(void *keys, int64_t n, int32_t dtype, void *stream);
 
@@ -150,7 +161,9 @@ enum {
   SR_OPT_RESIDENT_CAP = 4, /* resident path: largest level-1 bucket sorted in-kernel, 1..16384 (default and
                               maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
                               host-driven partition levels (tests lower it) */
-  SR_OPT_OUTLIER_ROUTE = 5 /* 0: never choose the outlier route automatically */
+  SR_OPT_OUTLIER_ROUTE = 5, /* 0: never choose the outlier route automatically */
+  SR_OPT_WS_LIMIT = 6     /* fault injection: device workspace bytes one call may take (0 = no limit); a
+                             larger reservation fails with SR_ERR_OUT_OF_MEMORY as a real one would */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

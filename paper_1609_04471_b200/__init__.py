@@ -19,7 +19,8 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "size out o
           5: "out of device memory", 6: "CUDA error", 7: "internal error"}
 ROUTES = {0: "none", 1: "sorted", 2: "reversed", 3: "merge", 4: "partition", 5: "tile", 6: "outlier"}
 ROUTE_MERGE, ROUTE_PARTITION, ROUTE_OUTLIER = 3, 4, 6
-OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE = 0, 1, 2, 3, 4, 5
+OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE, OPT_WS_LIMIT = (
+    0, 1, 2, 3, 4, 5, 6)
 
 EXPORTS = [
     "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",

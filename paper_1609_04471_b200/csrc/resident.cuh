@@ -38,7 +38,9 @@
 //      is_sorted first.  Buckets beyond the in-kernel cap are
 //      copied unsorted into their final range and listed for the host, which
 //      runs further partition levels on them.
-//   The last CTA to exit publishes the statistics to a host-mapped record.
+//   CTA 0 publishes the outcome to a host-mapped record as soon as it is known
+//   (after the route step, or on the partition route once the bucket sizes are
+//   known at the start of D), so the host call returns while the kernel runs.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstddef>
@@ -110,24 +112,27 @@ struct ResArgs {
   int force, merge_ok;
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
-  uint32_t* unit_counter;   // [0] CTA units, [1] CTAs done, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
+  uint32_t* unit_counter;   // [0] CTA units, [1] unused, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
   uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
   uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
-  ResDone* done;            // host-mapped completion record (the last CTA to exit writes it)
+  ResDone* done;            // host-mapped completion record (CTA 0 writes it once the outcome is known)
   uint32_t seq;             // this call's completion sequence number
 };
 
-// Host-mapped completion record: the statistics the planner needs, written by
-// the last CTA to leave the kernel, then the sequence number.  The host spins on
-// `seq` instead of a device->host copy + stream synchronisation (~10 us less
-// per call, tools/micro/api.cu).
+// Host-mapped completion record: the statistics the planner needs and whether
+// the launch finishes the sort by itself, then the sequence number.  CTA 0
+// writes it ONCE, as soon as the route (and, on the partition route, every
+// bucket size) is known -- long before the kernel ends -- so the host returns
+// from the call while the kernel is still running (the result is valid when
+// the stream reaches the end of the kernel).  The host spins on `seq` instead
+// of a device->host copy + stream synchronisation (tools/micro/api.cu).
 struct ResDone {
   DevStats st;
+  int32_t in_kernel;        // 1: nothing left for the host; 0: the host continues after the kernel
   volatile uint32_t seq;
-  uint32_t pad[31];
+  uint32_t pad[30];
 };
-
 // phase C sub-steps of CTA 0's first group (SR_TIMING diagnostics)
 #define SR_RES_SUB(kk)                                                                              \
   do {                                                                                              \
@@ -151,25 +156,18 @@ __device__ __forceinline__ unsigned long long res_now() {
   return t;
 }
 
-// Every CTA calls this once on its way out (the route decisions are uniform
-// per CTA); the last one publishes the statistics to the host-mapped record.
-// Classic fence + counter: every CTA's global writes (statistics atomics
-// included) precede its increment, so the last CTA sees them all.
+// Publish the early completion record (one thread of CTA 0, after this CTA
+// wrote the statistics in a.st).
 template <typename K>
-__device__ __forceinline__ void res_exit(const ResArgs<K>& a) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(a.unit_counter + 1, 1u);
-    if (prev == gridDim.x - 1 && a.done) {
-      __threadfence();
-      const unsigned long long* s = reinterpret_cast<const unsigned long long*>(a.st);
-      unsigned long long* d = reinterpret_cast<unsigned long long*>(&a.done->st);
-      for (int i = 0; i < (int)(sizeof(DevStats) / 8); i++) d[i] = __ldcg(s + i);
-      __threadfence_system();
-      a.done->seq = a.seq;
-    }
-  }
+__device__ __forceinline__ void res_publish(const ResArgs<K>& a, int in_kernel) {
+  if (!a.done) return;
+  __threadfence();
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(a.st);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(&a.done->st);
+  for (int i = 0; i < (int)(sizeof(DevStats) / 8); i++) d[i] = __ldcg(s + i);
+  a.done->in_kernel = in_kernel;
+  __threadfence_system();
+  a.done->seq = a.seq;
 }
 
 // Shared memory: the persistent bucket table + phase-local buffers in a union.
@@ -685,16 +683,16 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       if (c == 0) {  // the route is in a.st: tell the samplers
         __threadfence();
         atomicAdd(a.arrive, 1u);
+        // every route but the partition is decided here: sorted / reversed finish
+        // in this launch, merge / outlier / undecided continue on the host
+        if (r != kRoutePartition) res_publish(a, (r == kRouteSorted || r == kRouteReversed) ? 1 : 0);
       }
     }
   }
   __syncthreads();
   const int64_t route = s_route;
   SR_RES_STAMP(2);
-  if (route == kRouteSorted) {
-    res_exit(a);
-    return;
-  }
+  if (route == kRouteSorted) return;
   if (route == kRouteReversed) {
     // UR pairs per thread in flight (a dependent load/store pair per thread
     // and round would leave the reversal latency-bound)
@@ -713,13 +711,9 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         if (p < half) { a.keys[p] = y[u]; a.keys[n - 1 - p] = x[u]; }
       }
     }
-    res_exit(a);
     return;
   }
-  if (route != kRoutePartition) {  // MERGE / undecided: the host planner continues
-    res_exit(a);
-    return;
-  }
+  if (route != kRoutePartition) return;  // MERGE / undecided: the host planner continues
   const int m1 = a.B1 - 1;
   const int depth1 = tree_depth(m1);
   if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
@@ -900,6 +894,23 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   smem_scan<NT>(start, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
   if (tid == 0) start[nbins] = (uint32_t)n;
   __syncthreads();
+  if (c == 0) {  // statistics; every bucket size is known: publish the outcome early
+    long long noneq = 0, eqk = 0;
+    int over = 0;
+    for (int b = tid; b < nbins; b += NT) {
+      const uint32_t cnt = start[b + 1] - start[b];
+      if (b & 1) eqk += cnt; else noneq += cnt;
+      over |= !(b & 1) && cnt > (uint32_t)a.capb;  // listed for the host's next level
+    }
+    noneq = block_reduce_sum<NT>(noneq, reinterpret_cast<long long*>(sm.red64));
+    eqk = block_reduce_sum<NT>(eqk, reinterpret_cast<long long*>(sm.red64));
+    over = __syncthreads_or(over);
+    if (tid == 0) {
+      a.st->noneq_total = noneq;
+      a.st->eq_keys = eqk;
+      res_publish(a, over ? 0 : 1);
+    }
+  }
   {  // every key of a held group to its bucket in ws (runs of the same bucket are
      // consecutive, so the stores coalesce per piece); equality buckets are
      // filled in E
@@ -992,20 +1003,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     NC = tot;
     __syncthreads();
   }
-  if (c == 0) {  // statistics
-    long long noneq = 0, eqk = 0;
-    for (int b = tid; b < nbins; b += NT) {
-      const uint32_t cnt = start[b + 1] - start[b];
-      if (b & 1) eqk += cnt; else noneq += cnt;
-    }
-    noneq = block_reduce_sum<NT>(noneq, reinterpret_cast<long long*>(sm.red64));
-    eqk = block_reduce_sum<NT>(eqk, reinterpret_cast<long long*>(sm.red64));
-    if (tid == 0) {
-      a.st->noneq_total = noneq;
-      a.st->eq_keys = eqk;
-      a.st->n_items = (int64_t)sm.upa[nbins] + sm.upb[nbins] + NC;
-    }
-  }
+  if (c == 0 && tid == 0) a.st->n_items = (int64_t)sm.upa[nbins] + sm.upb[nbins] + NC;
   __shared__ uint32_t s_unit;
   typename SM::E& e = sm.u.e;
   if (NC > 0) {
@@ -1107,7 +1105,6 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   }
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[3] = res_now();
   SR_RES_STAMP(6);
-  res_exit(a);
 }
 
 }  // namespace sr

@@ -41,6 +41,7 @@ int g_merge_route = 1;
 int g_resident = 1;
 int g_outlier = 1;
 int g_res_cap = 16384;
+int64_t g_ws_limit = 0;  // SR_OPT_WS_LIMIT (fault injection), 0 = none
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -51,6 +52,63 @@ struct ProfEntry {
   cudaEvent_t a, b;
   int64_t bytes;
 };
+
+// Per (host thread, device) state of the resident path: every pointer here is
+// device-specific, so a thread that sorts on two GPUs keeps one set per device.
+struct DevState {
+  // host-mapped completion record of the resident kernel (resident.cuh ResDone)
+  sr::ResDone* done_h = nullptr;
+  sr::ResDone* done_d = nullptr;
+  uint32_t done_seq = 0;
+  uint32_t* arrive = nullptr;  // resident route-step arrival counter (device, zeroed once, never reset)
+  uint32_t arrive_base = 0;
+  // resident scratch kept between calls: calls from this thread on this device
+  // are ordered on the device (same stream: stream order; another stream: it
+  // waits for last_ev), so the next call reuses the arena without a
+  // cudaMallocAsync even though the host returned before the kernel finished
+  unsigned char* res_arena = nullptr;
+  size_t res_arena_bytes = 0;
+  cudaEvent_t last_ev = nullptr;       // recorded after the last resident launch
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
+  cudaEvent_t launch_ev = nullptr;     // recorded before each resident launch (watchdog start)
+  // the resident kernel as a cooperative node of an instantiated one-node CUDA
+  // graph, its parameters replaced per call: cudaGraphExecKernelNodeSetParams +
+  // cudaGraphLaunch take ~3.5 us less host time than cudaLaunchCooperativeKernel
+  // for a 148-CTA, ~210 KB-smem launch (tools/micro/coopgraph.cu)
+  struct CoopGraph {
+    const void* func = nullptr;
+    unsigned P = 0;
+    size_t smem = 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaGraphNode_t node = nullptr;
+  };
+  CoopGraph coop[4];
+  // after a failed or timed-out resident call the kernel may still run and use
+  // the arena, the counter and the record: abandon them (leaked) so that the
+  // next call starts from fresh ones
+  void abandon() {
+    done_h = nullptr;
+    done_d = nullptr;
+    arrive = nullptr;
+    res_arena = nullptr;
+    res_arena_bytes = 0;
+    has_last = false;
+  }
+  ~DevState() {
+    for (auto& cg : coop) {
+      if (cg.ge) cudaGraphExecDestroy(cg.ge);
+      if (cg.g) cudaGraphDestroy(cg.g);
+    }
+    if (last_ev) cudaEventDestroy(last_ev);
+    if (launch_ev) cudaEventDestroy(launch_ev);
+    if (done_h) cudaFreeHost(done_h);
+    if (res_arena) cudaFree(res_arena);
+    if (arrive) cudaFree(arrive);
+  }
+};
+constexpr int kMaxDevices = 64;
 
 struct ThreadState {
   sr_plan plan{};
@@ -65,44 +123,20 @@ struct ThreadState {
   size_t up_bytes = 0;
   cudaEvent_t up_done = nullptr;
   bool up_pending = false;
-  // host-mapped completion record of the resident kernel (resident.cuh ResDone)
-  sr::ResDone* done_h = nullptr;
-  sr::ResDone* done_d = nullptr;
-  uint32_t done_seq = 0;
-  uint32_t* arrive = nullptr;  // resident route-step arrival counter (device, zeroed once, never reset)
-  uint32_t arrive_base = 0;
-  // resident scratch kept between calls of this thread: a resident call that
-  // finishes inside its one launch leaves no work behind (the host waited for
-  // it), so the next call can reuse the arena without a cudaMallocAsync
-  unsigned char* res_arena = nullptr;
-  size_t res_arena_bytes = 0;
-  bool res_arena_busy = false;  // a call using it did not complete in-kernel
-  // the resident kernel as a cooperative node of an instantiated one-node CUDA
-  // graph, its parameters replaced per call: cudaGraphExecKernelNodeSetParams +
-  // cudaGraphLaunch take ~3.5 us less host time than cudaLaunchCooperativeKernel
-  // for a 148-CTA, ~210 KB-smem launch (tools/micro/coopgraph.cu)
-  struct CoopGraph {
-    const void* func = nullptr;
-    int dev = -1;
-    unsigned P = 0;
-    size_t smem = 0;
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t ge = nullptr;
-    cudaGraphNode_t node = nullptr;
-  };
-  CoopGraph coop[4];
+  DevState* dev[kMaxDevices] = {};
+  DevState& ds() {  // the current device's state
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= kMaxDevices) d = 0;
+    if (!dev[d]) dev[d] = new DevState();
+    return *dev[d];
+  }
   ~ThreadState() {
-    for (auto& cg : coop) {
-      if (cg.ge) cudaGraphExecDestroy(cg.ge);
-      if (cg.g) cudaGraphDestroy(cg.g);
-    }
+    for (auto* d : dev) delete d;
     for (auto& e : prof) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (pinned) cudaFreeHost(pinned);
     if (up) cudaFreeHost(up);
     if (up_done) cudaEventDestroy(up_done);
-    if (done_h) cudaFreeHost(done_h);
-    if (res_arena && !res_arena_busy) cudaFree(res_arena);
-    if (arrive) cudaFree(arrive);
   }
 };
 thread_local ThreadState t_state;
@@ -132,28 +166,27 @@ void check_cuda(cudaError_t e, const char* what) {
 cudaError_t launch_coop(const void* func, unsigned P, unsigned NT, void** args, size_t smem, cudaStream_t st) {
   static const bool direct = getenv("SR_NO_GRAPH") != nullptr;
   if (direct) return cudaLaunchCooperativeKernel(func, P, NT, args, smem, st);
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
   cudaKernelNodeParams kp = {};
   kp.func = const_cast<void*>(func);
   kp.gridDim = dim3(P);
   kp.blockDim = dim3(NT);
   kp.sharedMemBytes = (unsigned)smem;
   kp.kernelParams = args;
-  ThreadState::CoopGraph* cg = nullptr;
-  for (auto& x : t_state.coop)
-    if (x.func == func && x.dev == dev && x.P == P && x.smem == smem) { cg = &x; break; }
+  DevState& ds = t_state.ds();  // graphs are per device
+  DevState::CoopGraph* cg = nullptr;
+  for (auto& x : ds.coop)
+    if (x.func == func && x.P == P && x.smem == smem) { cg = &x; break; }
+  cudaError_t e;
   if (cg) {
     e = cudaGraphExecKernelNodeSetParams(cg->ge, cg->node, &kp);
     if (e != cudaSuccess) return e;
     return cudaGraphLaunch(cg->ge, st);
   }
-  ThreadState::CoopGraph* slot = nullptr;
-  for (auto& x : t_state.coop)
+  DevState::CoopGraph* slot = nullptr;
+  for (auto& x : ds.coop)
     if (!x.func) { slot = &x; break; }
   if (!slot) return cudaLaunchCooperativeKernel(func, P, NT, args, smem, st);  // cache full
-  ThreadState::CoopGraph n;
+  DevState::CoopGraph n;
   cudaLaunchAttributeValue v = {};
   v.cooperative = 1;
   if ((e = cudaGraphCreate(&n.g, 0)) != cudaSuccess) return e;
@@ -164,7 +197,6 @@ cudaError_t launch_coop(const void* func, unsigned P, unsigned NT, void** args, 
     return e;
   }
   n.func = func;
-  n.dev = dev;
   n.P = P;
   n.smem = smem;
   *slot = n;
@@ -176,24 +208,28 @@ void* pinned(size_t bytes) {
   if (ts.pinned_bytes < bytes) {
     if (ts.pinned) cudaFreeHost(ts.pinned);
     size_t sz = std::max<size_t>(bytes, 1 << 20);
-    check_cuda(cudaHostAlloc(&ts.pinned, sz, cudaHostAllocDefault), "cudaHostAlloc");
+    check_cuda(cudaHostAlloc(&ts.pinned, sz, cudaHostAllocPortable), "cudaHostAlloc");
     ts.pinned_bytes = sz;
   }
   return ts.pinned;
 }
 
-std::once_flag g_pool_once;
+// the stream-ordered pool of each device keeps its memory between calls
 void init_pool() {
-  std::call_once(g_pool_once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-  });
+  static std::mutex mu;
+  static bool done[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  done[dev] = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
 }
 
 template <typename T>
@@ -246,8 +282,14 @@ struct Ctx {
   // carve from, so a call costs one cudaMallocAsync instead of dozens.
   unsigned char* arena = nullptr;
   size_t arena_size = 0, arena_off = 0;
+  // SR_OPT_WS_LIMIT: a reservation beyond the injected limit fails as a real one would
+  void ws_check(size_t bytes) {
+    if (g_ws_limit > 0 && plan.workspace_bytes + (int64_t)bytes > g_ws_limit)
+      fail(SR_ERR_OUT_OF_MEMORY, "cudaMallocAsync: workspace limit (SR_OPT_WS_LIMIT)");
+  }
   void reserve(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
+    ws_check(bytes);
     void* p = nullptr;
     check_cuda(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
     allocs.push_back(p);
@@ -272,6 +314,7 @@ struct Ctx {
       arena_off += bytes;
       return r;
     }
+    ws_check(bytes);
     void* p = nullptr;
     check_cuda(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
     allocs.push_back(p);
@@ -319,7 +362,7 @@ struct Ctx {
       if (up_off == 0 && bytes <= (size_t(16) << 20)) {  // (re)size the staging area between calls
         if (ts.up) cudaFreeHost(ts.up);
         ts.up_bytes = std::max<size_t>(bytes, size_t(1) << 20);
-        check_cuda(cudaHostAlloc((void**)&ts.up, ts.up_bytes, cudaHostAllocDefault), "cudaHostAlloc");
+        check_cuda(cudaHostAlloc((void**)&ts.up, ts.up_bytes, cudaHostAllocPortable), "cudaHostAlloc");
       } else {  // staging full within this call: fall back to a synchronous pageable copy
         check_cuda(cudaMemcpyAsync(dst, src.data(), bytes, cudaMemcpyHostToDevice, st), "upload");
         return;
@@ -335,9 +378,16 @@ struct Ctx {
   }
   // Wait for a kernel's host-mapped completion record (spin; the stream is
   // polled now and then so that a failed or lost launch cannot hang the host).
-  DevStats await_done(const sr::ResDone* d, uint32_t seq) {
+  // Wait for a kernel's host-mapped completion record (spin; the stream is
+  // polled now and then so that a failed or lost launch cannot hang the host).
+  // The watchdog starts once `started` (recorded just before the launch) has
+  // completed, i.e. when the kernel can run, not when the host began waiting:
+  // earlier work queued on the stream does not count against it.
+  DevStats await_done(const sr::ResDone* d, uint32_t seq, cudaEvent_t started, int* in_kernel) {
     auto t0 = std::chrono::steady_clock::now();
     t_enqueue += std::chrono::duration<double>(t0 - t_mark).count();
+    bool running = false;
+    auto t_run = t0;
     for (uint32_t spin = 1;; spin++) {
       if (d->seq == seq) break;
       if ((spin & 1023) == 0) {
@@ -347,14 +397,24 @@ struct Ctx {
           fail(SR_ERR_INTERNAL, "resident kernel finished without its completion record");
         }
         if (e != cudaErrorNotReady) check_cuda(e, "resident kernel");
-        // watchdog: a sort of <= 2^22 keys takes well under a millisecond
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-          fail(SR_ERR_CUDA, "resident kernel did not complete within 20 s");
+        if (!running) {
+          const cudaError_t q = cudaEventQuery(started);
+          if (q == cudaSuccess) {
+            running = true;
+            t_run = std::chrono::steady_clock::now();
+          } else if (q != cudaErrorNotReady) {
+            check_cuda(q, "resident launch event");
+          }
+        }
+        // watchdog: a sort of <= 2^22 keys takes well under a millisecond once it runs
+        if (running && std::chrono::steady_clock::now() - t_run > std::chrono::seconds(20))
+          fail(SR_ERR_CUDA, "resident kernel did not report within 20 s of starting");
       }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     DevStats r;
     std::memcpy(&r, (const void*)&d->st, sizeof(DevStats));
+    *in_kernel = d->in_kernel;
     plan.host_syncs++;
     t_mark = std::chrono::steady_clock::now();
     t_wait += std::chrono::duration<double>(t_mark - t0).count();
@@ -378,15 +438,19 @@ struct Ctx {
 
 // Raise a kernel's dynamic shared-memory limit once per (kernel, size); the
 // attribute call is far more expensive than a launch.
+// The attribute is per device: the cache is keyed by (device, kernel).
 template <typename Kern>
 void set_smem(Kern k, size_t bytes) {
   static std::mutex mu;
-  static std::vector<std::pair<const void*, size_t>> done;
+  struct Done { int dev; const void* f; size_t bytes; };
+  static std::vector<Done> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
   for (auto& d : done)
-    if (d.first == (const void*)k && d.second >= bytes) return;
+    if (d.dev == dev && d.f == (const void*)k && d.bytes >= bytes) return;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  done.push_back({(const void*)k, bytes});
+  done.push_back({dev, (const void*)k, bytes});
 }
 
 // ------------------------------------------------------------------ tunables
@@ -1055,13 +1119,19 @@ struct Sorter {
   }
 
   // ---- resident path: the whole keys-only sort as one cooperative launch (resident.cuh)
-  static int resident_grid() {  // CTAs of the cooperative launch (one per SM), 0 if it cannot run
-    static int grid[2] = {-1, -1};
-    int& g = grid[sizeof(K) == 8];
-    if (g < 0) {
+  static int resident_grid() {  // CTAs of the cooperative launch (one per SM) on the current device, 0 if it cannot run
+    static std::mutex mu;
+    static int grid[kMaxDevices][2];
+    static bool init[kMaxDevices][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) return 0;
+    std::lock_guard<std::mutex> lk(mu);
+    int& g = grid[dev][sizeof(K) == 8];
+    if (!init[dev][sizeof(K) == 8]) {
+      init[dev][sizeof(K) == 8] = true;
       g = 0;
-      int dev = 0, sms = 0, coop = 0, per = 0;
-      cudaGetDevice(&dev);
+      int sms = 0, coop = 0, per = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
       const size_t smem = sizeof(ResSmem<K>);
@@ -1105,22 +1175,22 @@ struct Sorter {
       const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
                                     r(4 * (int64_t)NG * nbins) + 8 * 256);
-      ThreadState& tsa = t_state;
-      if (tsa.res_arena && (tsa.res_arena_busy || tsa.res_arena_bytes < bytes)) {
-        // too small: freed stream-ordered (idle, the last call completed in-kernel);
-        // busy (an earlier call failed or continued on the host): left alone
-        if (!tsa.res_arena_busy) c.allocs.push_back(tsa.res_arena);
-        tsa.res_arena = nullptr;
+      DevState& dsa = t_state.ds();
+      if (dsa.has_last && dsa.last_stream != c.st)  // the arena of the last call is in use until its kernel ends
+        check_cuda(cudaStreamWaitEvent(c.st, dsa.last_ev, 0), "cudaStreamWaitEvent");
+      c.ws_check(bytes);
+      if (dsa.res_arena && dsa.res_arena_bytes < bytes) {  // too small: freed stream-ordered
+        c.allocs.push_back(dsa.res_arena);
+        dsa.res_arena = nullptr;
       }
-      if (!tsa.res_arena) {
+      if (!dsa.res_arena) {
         void* p = nullptr;
         check_cuda(cudaMallocAsync(&p, bytes, c.st), "cudaMallocAsync");
-        tsa.res_arena = reinterpret_cast<unsigned char*>(p);
-        tsa.res_arena_bytes = bytes;
+        dsa.res_arena = reinterpret_cast<unsigned char*>(p);
+        dsa.res_arena_bytes = bytes;
       }
-      c.use_arena(tsa.res_arena, tsa.res_arena_bytes);
-      c.plan.workspace_bytes += (int64_t)tsa.res_arena_bytes;
-      tsa.res_arena_busy = true;  // until the kernel is known to have finished everything
+      c.use_arena(dsa.res_arena, dsa.res_arena_bytes);
+      c.plan.workspace_bytes += (int64_t)dsa.res_arena_bytes;
     }
     hostprof("reserved");
     ensure_ws();
@@ -1141,7 +1211,7 @@ struct Sorter {
       a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 16);
       a.ctrl_words = (int)(bytes / 4);
     }
-    ThreadState& ts = t_state;
+    DevState& ts = t_state.ds();
     if (!ts.done_h) {
       check_cuda(cudaHostAlloc((void**)&ts.done_h, sizeof(ResDone), cudaHostAllocMapped), "cudaHostAlloc(mapped)");
       check_cuda(cudaHostGetDevicePointer((void**)&ts.done_d, ts.done_h, 0), "cudaHostGetDevicePointer");
@@ -1154,6 +1224,8 @@ struct Sorter {
       check_cuda(cudaMemset(ts.arrive, 0, 256), "cudaMemset(arrive)");
       ts.arrive_base = 0;
     }
+    if (!ts.last_ev) check_cuda(cudaEventCreateWithFlags(&ts.last_ev, cudaEventDisableTiming), "cudaEventCreate");
+    if (!ts.launch_ev) check_cuda(cudaEventCreateWithFlags(&ts.launch_ev, cudaEventDisableTiming), "cudaEventCreate");
     a.arrive = ts.arrive;
     a.arrive_base = ts.arrive_base;
     a.S1 = S1;
@@ -1176,13 +1248,24 @@ struct Sorter {
     if (stamps) c.memset0(a.tstamp, 64 * (P + 4));
     const size_t smem = sizeof(ResSmem<K>);
     hostprof("prepared");
+    check_cuda(cudaEventRecord(ts.launch_ev, c.st), "cudaEventRecord");
     const int h = c.launch("resident", n * kw, [&] {
       void* args[] = {&a};
       check_cuda(launch_coop((const void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
     ts.arrive_base += (uint32_t)P + 1u;  // every CTA arrives once, CTA 0 once more (route published)
+    check_cuda(cudaEventRecord(ts.last_ev, c.st), "cudaEventRecord");
+    ts.last_stream = c.st;
+    ts.has_last = true;
     hostprof("launched");
-    DevStats hs = c.await_done(ts.done_h, a.seq);
+    int in_kernel = 0;
+    DevStats hs;
+    try {
+      hs = c.await_done(ts.done_h, a.seq, ts.launch_ev, &in_kernel);
+    } catch (...) {
+      ts.abandon();  // the kernel may still be running on these
+      throw;
+    }
     hostprof("read back");
     if (stamps) {
       const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 4)));
@@ -1221,17 +1304,16 @@ struct Sorter {
     c.plan.asc_breaks = hs.asc_breaks;
     c.plan.long_runs = hs.n_asc_runs + hs.n_desc_runs;
     if (hs.error) fail(SR_ERR_INTERNAL, "resident kernel inconsistency");
-    // the one launch finished the sort unless the host continues below: then
-    // the arena's buffers feed the continuation, so it is released with this
-    // call (stream-ordered) instead of being reused
-    const bool in_kernel = hs.route == kRouteSorted || hs.route == kRouteReversed ||
-                           (hs.route == kRoutePartition && hs.n_ovf == 0);
-    if (in_kernel) {
-      t_state.res_arena_busy = false;
-    } else {
-      c.allocs.push_back(t_state.res_arena);
-      t_state.res_arena = nullptr;
-      t_state.res_arena_busy = false;
+    // the launch finishes the sort by itself unless the record says otherwise:
+    // the host returns now, while the kernel is still running.  Otherwise the
+    // host continues once the kernel has ended, from its final statistics; the
+    // arena's buffers feed that continuation, so it is released with this call
+    // (stream-ordered) instead of being reused.
+    if (!in_kernel) {
+      hs = *reinterpret_cast<const DevStats*>(c.readback(a.st, sizeof(DevStats)));
+      c.allocs.push_back(ts.res_arena);
+      ts.res_arena = nullptr;
+      ts.res_arena_bytes = 0;
     }
     switch (hs.route) {
       case kRouteSorted:
@@ -1598,16 +1680,32 @@ struct Sorter {
 };
 
 // ------------------------------------------------------------------ validation
-bool is_device_ptr(const void* p) {
+// Device (or managed) memory; *dev receives the device that owns it.
+bool is_device_ptr(const void* p, int* dev = nullptr) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  if (dev) *dev = a.device;
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
+
+// Makes the device that owns the caller's buffers current for one call (the
+// caller's stream must belong to it) and restores the previous device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = 0;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    cudaGetLastError();
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 bool dtype_ok(int32_t dtype) { return dtype == SR_INT32 || dtype == SR_INT64 || dtype == SR_FLOAT32 || dtype == SR_FLOAT64; }
 int64_t key_bytes(int32_t dtype) { return (dtype == SR_INT32 || dtype == SR_FLOAT32) ? 4 : 8; }
 
-int32_t validate(const void* keys, const void* vals, int64_t n, int32_t dtype, bool pairs) {
+int32_t validate(const void* keys, const void* vals, int64_t n, int32_t dtype, bool pairs, int* dev = nullptr) {
   if (n < 0) return SR_ERR_INVALID_ARGUMENT;
   if (!dtype_ok(dtype)) return SR_ERR_UNSUPPORTED_DTYPE;
   if (n > INT32_MAX) return SR_ERR_SIZE;
@@ -1616,7 +1714,10 @@ int32_t validate(const void* keys, const void* vals, int64_t n, int32_t dtype, b
   if (!keys || (pairs && !vals)) return SR_ERR_INVALID_ARGUMENT;
   if ((uintptr_t)keys % kw) return SR_ERR_ALIGNMENT;
   if (pairs && (uintptr_t)vals % 4) return SR_ERR_ALIGNMENT;
-  if (!is_device_ptr(keys) || (pairs && !is_device_ptr(vals))) return SR_ERR_INVALID_ARGUMENT;
+  int dk = -1, dv = -1;
+  if (!is_device_ptr(keys, &dk) || (pairs && !is_device_ptr(vals, &dv))) return SR_ERR_INVALID_ARGUMENT;
+  if (pairs && dk != dv) return SR_ERR_INVALID_ARGUMENT;
+  if (dev) *dev = dk;
   if (pairs) {
     uintptr_t k0 = (uintptr_t)keys, k1 = k0 + n * kw, v0 = (uintptr_t)vals, v1 = v0 + n * 4;
     if (k0 < v1 && v0 < k1) return SR_ERR_INVALID_ARGUMENT;
@@ -1644,12 +1745,14 @@ int32_t guarded(F&& f) {
 
 int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream, bool pairs) {
   t_call0 = std::chrono::steady_clock::now();
-  int32_t v = validate(keys, vals, n, dtype, pairs);
+  int dev = -1;
+  int32_t v = validate(keys, vals, n, dtype, pairs, &dev);
   hostprof("validated");
   if (v != SR_OK) {
     t_state.err = sr_status_string(v);
     return v;
   }
+  DeviceGuard dg(dev);
   return guarded([&] {
     Ctx c((cudaStream_t)stream);
     c.plan.n = n;
@@ -1667,12 +1770,26 @@ int32_t sort_impl(void* keys, void* vals, int64_t n, int32_t dtype, void* stream
       });
     };
     if (fl) flip();
-    if (w4) {
-      if (pairs) Sorter<int32_t, true>(c, (int32_t*)keys, (uint32_t*)vals, n).run();
-      else Sorter<int32_t, false>(c, (int32_t*)keys, nullptr, n).run();
-    } else {
-      if (pairs) Sorter<int64_t, true>(c, (int64_t*)keys, (uint32_t*)vals, n).run();
-      else Sorter<int64_t, false>(c, (int64_t*)keys, nullptr, n).run();
+    try {
+      if (w4) {
+        if (pairs) Sorter<int32_t, true>(c, (int32_t*)keys, (uint32_t*)vals, n).run();
+        else Sorter<int32_t, false>(c, (int32_t*)keys, nullptr, n).run();
+      } else {
+        if (pairs) Sorter<int64_t, true>(c, (int64_t*)keys, (uint32_t*)vals, n).run();
+        else Sorter<int64_t, false>(c, (int64_t*)keys, nullptr, n).run();
+      }
+    } catch (const SrError& e) {
+      // The integer sort failed.  Before any data-moving kernel (out of memory
+      // while reserving the workspace, the usual case) the keys hold exactly
+      // their integer images, and the involution restores the caller's bits;
+      // after one they hold a permutation of the images, restored to a
+      // permutation of the caller's keys.  A sticky CUDA error leaves the
+      // contents unspecified (include/sr_sort.h).
+      if (fl && e.code != SR_ERR_CUDA) {
+        cudaGetLastError();
+        try { flip(); } catch (...) {}
+      }
+      throw;
     }
     if (fl) {  // the integer sort's launches count in the plan; the flips are added
       const int launches = c.plan.launches;
@@ -1892,6 +2009,10 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       return SR_OK;
     case SR_OPT_OUTLIER_ROUTE:
       g_outlier = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_WS_LIMIT:
+      if (value < 0) return SR_ERR_INVALID_ARGUMENT;
+      g_ws_limit = value;
       return SR_OK;
     case SR_OPT_RESIDENT_CAP:
       if (value < 1 || value > 16384) return SR_ERR_INVALID_ARGUMENT;

@@ -73,3 +73,30 @@ def test_float_step_entry_points_reject():
     d = torch.zeros(100, dtype=torch.float32, device="cuda")
     with pytest.raises(sr.SrError):
         sr.tile_sort(d, 64)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [100_003, 3_000_000])  # resident (one launch) and multi-kernel paths
+@pytest.mark.parametrize("pairs", [False, True])
+def test_float_oom_leaves_keys_untouched(dtype, n, pairs):
+    """SR_ERR_OUT_OF_MEMORY from the first workspace reservation (injected
+    with SR_OPT_WS_LIMIT) leaves float keys bit-identical (include/sr_sort.h
+    "Error behaviour"): the in-place totalOrder map is undone."""
+    k = gen.make_float("fbits", n, dtype, config=41)
+    d = torch.from_numpy(k.copy()).cuda()
+    v = torch.arange(n, dtype=torch.int32, device="cuda")
+    sr.set_option(sr.OPT_WS_LIMIT, 4096)
+    try:
+        with pytest.raises(sr.SrError) as ei:
+            sr.sort_pairs(d, v) if pairs else sr.sort_keys(d)
+    finally:
+        sr.set_option(sr.OPT_WS_LIMIT, 0)
+    assert ei.value.status == 5
+    torch.cuda.synchronize()
+    u = UINT[dtype]
+    assert np.array_equal(d.cpu().numpy().view(u), k.view(u))
+    assert torch.equal(v, torch.arange(n, dtype=torch.int32, device="cuda"))
+    got = d.clone()  # and the library still works afterwards
+    sr.sort_keys(got)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy().view(u), oracle.sort_keys(k).view(u))
