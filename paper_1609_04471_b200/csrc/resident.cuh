@@ -30,10 +30,11 @@
 //      key goes to start[b] + offset + rank in the workspace, so each bucket
 //      is contiguous; equality keys are not written.
 //   -- grid sync --
-//   E  CTA units: range buckets above WCAP, one CTA each, partitioned in
-//      shared memory into 16 sub-buckets that the warps sort (R17); then warp
-//      units, largest first: range buckets <= WCAP sorted by one warp's
-//      register bitonic network (R15), and equality fills ("spared from the
+//   E  CTA units: range buckets above WCAP, one CTA each (unit_sort.cuh: an
+//      in-shared-memory 3-way sample partition into 32 sub-buckets that the
+//      warps sort, R17); then warp units, largest first: range buckets <=
+//      WCAP sorted by one warp's register bitonic network, two networks and a
+//      merge above half of WCAP (R15), and equality fills ("spared from the
 //      recursive calls").  Every bucket is checked with
 //      is_sorted first.  Buckets beyond the in-kernel cap are
 //      copied unsorted into their final range and listed for the host, which
@@ -50,6 +51,7 @@
 #include "partition.cuh"
 #include "presort.cuh"
 #include "types.cuh"
+#include "unit_sort.cuh"
 
 namespace sr {
 
@@ -59,9 +61,6 @@ constexpr int kResWarps = kResNT / 32;
 constexpr int kResGrp = 8192;           // largest tile: H1 scan unit and phase C grouping unit (one
                                         // tile-local counting sort); the host picks the tile so that
                                         // every CTA gets <= GPC tiles and the samplers one
-constexpr int kResSB = kResNT / 32;     // level-2 (in-CTA) sub-buckets per bucket: one per warp
-constexpr int kResO2 = 8;               // level-2 oversampling
-constexpr int kResS2 = kResO2 * kResSB; // level-2 sample
 constexpr int kResWarpFill = 4096;      // equality fill per warp unit
 constexpr int kResSamplers = 4;         // CTAs that sort one quarter of the level-1 sample each
 constexpr int kResMaxG = 512;           // tiles (G <= GPC * gridDim.x - kResSamplers)
@@ -112,7 +111,7 @@ struct ResArgs {
   int force, merge_ok;
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
-  uint32_t* unit_counter;   // [0] CTA units, [1] unused, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
+  uint32_t* unit_counter;   // [0] CTA units, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
   uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
   uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
@@ -189,16 +188,7 @@ struct ResSmem {
     K q[S1MAX];
     TileSummary ts[kResMaxG];
   };
-  struct alignas(16) E {
-    K x[CAPB];                     // the bucket (E); warp-unit staging areas span x and y
-    K y[CAPB];                     // sub-bucket regions / merge ping-pong buffer
-    K samp[kResS2];                // level-2 sample
-    K tree[kResSB];                // level-2 Eytzinger tree [1, SB)
-    uint32_t wcnt[kResWarps][kResSB];  // per-warp sub-bucket counts, then write cursors
-    uint32_t reg[kResSB + 1];      // sub-bucket regions in y (16-byte aligned, sized for the warp network)
-    uint32_t ost[kResSB + 1];      // sub-bucket starts in the output
-    uint8_t bin[CAPB];             // sub-bucket of x[i]
-  };
+  using E = UnitSmem<K, CAPB, kResNT>;  // E: the CTA units (unit_sort.cuh); warp-unit staging spans x and y
   static_assert(kResWarps * WCAP <= 2 * CAPB, "warp-unit staging areas live in x and y");
   uint32_t start[NB1 + 1];         // level-1 bucket starts, start[nbins] = n
   uint16_t upa[NB1 + 1];           // exclusive prefix of E warp units, class A (WCAP/2 < range bucket <= WCAP)
@@ -210,7 +200,7 @@ struct ResSmem {
     K samp1[S1MAX];                // A: the sampler's piece of the sample + BitonicSort scratch
     SP sp;
     CT ct;
-    E e;
+    E e;  // (UnitSmem: aligned x / y buffers)
   } u;
   int32_t red[kResNT / 32 + 1];
   int64_t red64[kResNT / 32 + 1];
@@ -246,283 +236,6 @@ __device__ __forceinline__ void res_classify(const K (&x)[U], int (&bin)[U], con
     const int i = j[u] - (1 << depth);
     bin[u] = 2 * i + ((i < m && tree[BMAX + i] == x[u] && eq[i]) ? 1 : 0);
   }
-}
-
-// Register bitonic sort of `count` keys by a group of GL lanes holding VT keys
-// each (blocked: lane l owns [l VT, (l+1) VT)), loaded from the 16-byte
-// aligned `src` (GL * VT readable keys; slots >= count are ignored) and written
-// to dst[0, count).  All lanes of the warp call with the same VT and GL.
-template <typename K, int VT, int GL>
-__device__ __forceinline__ void res_group_sort(const K* src, int count, K* __restrict__ dst) {
-  using BT = BitonicSort<K, 32, VT>;
-  const int gl = threadIdx.x & (GL - 1);
-  K k[VT];
-  BlockSort<K, false, 32, VT>::load_vec(src + gl * VT, k);
-#pragma unroll
-  for (int i = 0; i < VT; i++)
-    if (gl * VT + i >= count) k[i] = KeyTraits<K>::max_key();
-  batcher_network<VT>([&](int a, int b) { BT::cex(k[a], k[b]); });
-#pragma unroll
-  for (int tk = 2; tk <= GL; tk <<= 1) {  // lanes per merged run
-    BT::shfl_stage(k, tk - 1, (gl & (tk >> 1)) == 0, true);
-#pragma unroll
-    for (int jt = tk >> 2; jt >= 1; jt >>= 1) BT::shfl_stage(k, jt, (gl & jt) == 0, false);
-    BT::reg_half_cleaners(k);
-  }
-#pragma unroll
-  for (int i = 0; i < VT; i++)
-    if (gl * VT + i < count) dst[gl * VT + i] = k[i];
-}
-
-// One CTA sorts x[0, L) (L <= CAPB, already gathered in shared memory) into
-// dst: H11 for one level-1 bucket.  is_sorted first;
-// then runs of 128 keys sorted by 16-lane register bitonic networks (the
-// insertion-sort-below-alpha step), then merge-path merge rounds
-// in shared memory (the paper's mergesort levels, §3; A wins ties,
-// PAPER.md:99), the last round writing straight into dst.  The tail up to a
-// whole run is padded with +inf, which sorts last and is not written.
-template <typename K, int NT>
-__device__ __noinline__ void res_bucket_sort(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
-                                unsigned long long* prof = nullptr) {
-  constexpr int VT = 8;  // merge outputs per thread
-  constexpr int RVT = 8, RGL = 16;  // runs: 16-lane groups of VT 8 (128 keys), two per warp
-  constexpr int kResRun = RGL * RVT;
-  const int tid = threadIdx.x;
-  unsigned long long tprev = (prof && tid == 0) ? res_now() : 0;
-  auto mark = [&](int k) {  // optional per-step time accumulation (thread 0 of one CTA)
-    if (prof && tid == 0) {
-      const unsigned long long t = res_now();
-      prof[k] += t - tprev;
-      tprev = t;
-    }
-  };
-  int unsorted = 0;
-  for (int i = tid; i + 1 < L; i += NT) unsorted |= e.x[i + 1] < e.x[i];
-  if (!__syncthreads_or(unsorted)) {
-    for (int i = tid; i < L; i += NT) dst[i] = e.x[i];
-    return;
-  }
-  const int nruns = (L + kResRun - 1) / kResRun;
-  const int Lp = nruns * kResRun;
-  for (int i = L + tid; i < Lp; i += NT) e.x[i] = KeyTraits<K>::max_key();
-  __syncthreads();
-  mark(0);
-  {  // both halves of a warp always take part (the shuffles span the warp); a
-     // half without a run sorts nothing
-    const int half = (tid >> 4) & 1, w = tid >> 5;
-    for (int r0 = 2 * w; r0 < nruns; r0 += NT / RGL) {
-      const int r = r0 + half < nruns ? r0 + half : r0;
-      const int cnt = r0 + half < nruns ? (nruns == 1 ? L : kResRun) : 0;
-      res_group_sort<K, RVT, RGL>(e.x + r * kResRun, cnt, nruns == 1 ? dst : e.y + r * kResRun);
-    }
-  }
-  __syncthreads();
-  mark(1);
-  if (nruns == 1) return;
-  K* src = e.y;
-  K* out = e.x;
-  for (int R = kResRun; R < Lp; R *= 2) {
-    const bool last = 2 * R >= Lp;
-    for (int o = tid * VT; o < Lp; o += NT * VT) {
-      const int p0 = (o / (2 * R)) * (2 * R);
-      const int alen = R < Lp - p0 ? R : Lp - p0;
-      const int blen = Lp - p0 - alen < R ? Lp - p0 - alen : R;
-      const K* A = src + p0;
-      const K* B = A + alen;
-      const int diag = o - p0;
-      const int i = merge_path_search<K>([&](int q) { return A[q]; }, alen, [&](int q) { return B[q]; }, blen, diag);
-      const int j = diag - i;
-      // the VT outputs are the VT smallest of A[i, i+VT) and B[j, j+VT): all
-      // loads issued together, then a half-cleaner against the reversed B
-      // window (a bitonic sequence of the VT smallest) and a bitonic merge in
-      // registers -- no dependent load chain (equal keys are interchangeable)
-      K res[VT], bw[VT];
-#pragma unroll
-      for (int k = 0; k < VT; k++) {
-        res[k] = i + k < alen ? A[i + k] : KeyTraits<K>::max_key();
-        bw[k] = j + k < blen ? B[j + k] : KeyTraits<K>::max_key();
-      }
-#pragma unroll
-      for (int k = 0; k < VT; k++) res[k] = min(res[k], bw[VT - 1 - k]);
-#pragma unroll
-      for (int h = VT / 2; h > 0; h >>= 1) {
-#pragma unroll
-        for (int k = 0; k < VT; k++) {
-          if ((k & h) == 0) {
-            const K x = res[k], y = res[k | h];
-            res[k] = min(x, y);
-            res[k | h] = max(x, y);
-          }
-        }
-      }
-      if (last) {
-#pragma unroll
-        for (int k = 0; k < VT; k++)
-          if (o + k < L) dst[o + k] = res[k];
-      } else {
-        BlockSort<K, false, 32, VT>::store_vec(out + o, res);
-      }
-    }
-    __syncthreads();
-    K* t = src;
-    src = out;
-    out = t;
-  }
-  mark(2);
-}
-
-// Footprint of WarpBitonic<K, VT>::sort for `len` keys with the VT the warp
-// units and sub-buckets use (it stores nl * VT keys, nl a power of two).
-__device__ __forceinline__ int res_vt(int len) {
-  return len <= 128 ? 4 : len <= 256 ? 8 : len <= 512 ? 16 : len <= 1024 ? 32 : 64;
-}
-__device__ __forceinline__ int res_footprint(int len) {
-  if (len <= 0) return 0;
-  const int vt = res_vt(len);
-  const int need = (len + vt - 1) / vt;
-  int nl = 1;
-  while (nl < need) nl <<= 1;
-  return vt * nl;
-}
-
-// Sort stage[0, len) (16-byte aligned, res_footprint(len) keys writable) by one
-// warp's register network, the narrowest that holds it.
-template <typename K, int WCAP>
-__device__ __forceinline__ void res_warp_sort(K* stage, int len) {
-  if (len <= 128) WarpBitonic<K, 4>::sort(stage, len);
-  else if (len <= 256) WarpBitonic<K, 8>::sort(stage, len);
-  else if (len <= 512) WarpBitonic<K, 16>::sort(stage, len);
-  else if (WCAP >= 1024 && len <= 1024) WarpBitonic<K, (WCAP >= 1024 ? 32 : 16)>::sort(stage, len);
-  else WarpBitonic<K, WCAP / 32>::sort(stage, len);
-}
-
-// One CTA sorts x[0, L) (WCAP < L <= CAPB, gathered in shared memory) into
-// dst: H11 for one level-1 bucket as a second, in-shared-memory partition level
-// (the quicksort recursion, Appendix B; R17).
-// is_sorted first.  Then one sub-bucket per warp: the 15
-// splitters are every o2-th key of a regular sample of kResS2 keys, sorted by
-// counting ranks (the sample-based pivot choice); every key is
-// classified by a 4-level Eytzinger tree, counted per warp, and moved to its
-// sub-bucket's region of y; each warp sorts its sub-bucket in registers (the
-// "insertion sort below alpha" step) and writes it to dst.
-// Sub-buckets above WCAP keys or regions that do not fit y (heavy duplicates,
-// skew) send the bucket to the run + merge sort above.
-template <typename K, int NT>
-__device__ __forceinline__ void res_bucket_sort2(K* __restrict__ dst, int L, typename ResSmem<K>::E& e,
-                                 unsigned long long* prof = nullptr) {
-  constexpr int NW = NT / 32;
-  constexpr int SB = kResSB, DEPTH = 4;
-  constexpr int WCAP = ResSmem<K>::WCAP;
-  constexpr int UC = 8;  // keys per thread per classification round
-  static_assert(SB == NW && (1 << DEPTH) == SB && NT % kResS2 == 0, "one sub-bucket per warp, whole threads per sample");
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  unsigned long long tprev = (prof && tid == 0) ? res_now() : 0;
-  auto mark = [&](int k) {
-    if (prof && tid == 0) {
-      const unsigned long long t = res_now();
-      prof[k] += t - tprev;
-      tprev = t;
-    }
-  };
-  int unsorted = 0;
-  for (int i = tid; i + 1 < L; i += NT) unsorted |= e.x[i + 1] < e.x[i];
-  if (tid < kResS2) e.samp[tid] = e.x[(int)(((int64_t)(2 * tid + 1) * L) / (2 * kResS2))];
-  if (!__syncthreads_or(unsorted)) {
-    for (int i = tid; i < L; i += NT) dst[i] = e.x[i];
-    return;
-  }
-  {  // rank of sample q = position in the stably sorted sample; four threads per sample
-    constexpr int TPS = NT / kResS2, PART = kResS2 / TPS;
-    const int q = tid / TPS, h = tid % TPS;
-    const K v = e.samp[q];
-    int r = 0;
-#pragma unroll 8
-    for (int j = h * PART; j < (h + 1) * PART; j++) {
-      const K u = e.samp[j];
-      r += (u < v) || (u == v && j < q);
-    }
-#pragma unroll
-    for (int o = 1; o < TPS; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (h == 0) e.y[r] = v;  // y is free until the move
-    if (tid < NW * SB) (&e.wcnt[0][0])[tid] = 0u;
-  }
-  __syncthreads();
-  if (tid > 0 && tid < SB) {  // Eytzinger node i <- splitter pos = sorted sample o2 (pos + 1)
-    const int d = 31 - __clz(tid);
-    const int pos = ((2 * (tid - (1 << d)) + 1) << (DEPTH - 1 - d)) - 1;
-    e.tree[tid] = e.y[kResO2 * (pos + 1)];
-  }
-  __syncthreads();
-  mark(0);
-  auto classify = [&](K x) {
-    int j = 1;
-#pragma unroll
-    for (int l = 0; l < DEPTH; l++) j = 2 * j + (e.tree[j] < x ? 1 : 0);
-    return j - SB;
-  };
-  for (int i0 = 0; i0 < L; i0 += NT * UC) {  // per-warp counts
-#pragma unroll
-    for (int u = 0; u < UC; u++) {
-      const int i = i0 + u * NT + tid;
-      if (i < L) {
-        const int b = classify(e.x[i]);
-        e.bin[i] = (uint8_t)b;
-        atomicAdd(&e.wcnt[w][b], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  if (w == 0) {  // totals -> output starts and footprint-sized regions; cursors
-    uint32_t cb = 0;
-    if (lane < SB)
-#pragma unroll
-      for (int v = 0; v < NW; v++) cb += e.wcnt[v][lane];
-    const int fp = lane < SB ? res_footprint((int)cb) : 0;
-    uint32_t oi = cb, ri = (uint32_t)fp;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t1 = __shfl_up_sync(0xffffffffu, oi, o), t2 = __shfl_up_sync(0xffffffffu, ri, o);
-      if (lane >= o) { oi += t1; ri += t2; }
-    }
-    if (lane < SB) {
-      e.ost[lane] = oi - cb;
-      e.reg[lane] = ri - fp;
-      uint32_t run = ri - fp;
-#pragma unroll
-      for (int v = 0; v < NW; v++) {
-        const uint32_t c = e.wcnt[v][lane];
-        e.wcnt[v][lane] = run;
-        run += c;
-      }
-    }
-    const int bad = (lane < SB && cb > (uint32_t)WCAP) || (lane == SB - 1 && ri > (uint32_t)ResSmem<K>::CAPB);
-    const bool anybad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) e.ost[SB] = anybad ? 0xffffffffu : (uint32_t)L;
-  }
-  __syncthreads();
-  if (e.ost[SB] == 0xffffffffu) {  // heavy duplicates / skew: the general run + merge sort
-    res_bucket_sort<K, NT>(dst, L, e, nullptr);
-    return;
-  }
-  for (int i0 = 0; i0 < L; i0 += NT * UC) {  // move to the sub-bucket regions (same key <-> warp map)
-#pragma unroll
-    for (int u = 0; u < UC; u++) {
-      const int i = i0 + u * NT + tid;
-      if (i < L) {
-        e.y[atomicAdd(&e.wcnt[w][e.bin[i]], 1u)] = e.x[i];
-      }
-    }
-  }
-  __syncthreads();
-  mark(1);
-  {
-    const int o = (int)e.ost[w], len = (int)e.ost[w + 1] - o;
-    K* ks = e.y + e.reg[w];
-    if (len > 1) res_warp_sort<K, WCAP>(ks, len);
-    for (int i = lane; i < len; i += 32) dst[o + i] = ks[i];
-  }
-  __syncthreads();
-  mark(2);
 }
 
 static_assert(sizeof(ResSmem<int32_t>) <= 227 * 1024 && sizeof(ResSmem<int64_t>) <= 227 * 1024,
@@ -1018,6 +731,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       const int b = (int)sm.cbin[u];
       const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
       const unsigned long long tg0 = (a.tstamp && c == 0 && tid == 0) ? res_now() : 0;
+      const unsigned long long tg1 = a.tstamp ? res_now() : 0;
       const bool fits = len <= a.capb;
       K* gdst = fits ? e.x : a.keys + s;
       {
@@ -1050,12 +764,15 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       }
       unsigned long long* prof = (a.tstamp && c == 0) ? a.tstamp + 8 + 8 * (size_t)P : nullptr;
       if (prof && tid == 0) { prof[5] += res_now() - tg0; prof[7] += 1; }
-      res_bucket_sort2<K, NT>(a.keys + s, len, e, prof);
-      __syncthreads();
+      unit_sort<K, SM::CAPB, NT>(a.keys + s, len, e);
+      if (a.tstamp && tid == 0) {  // SR_TIMING: longest CTA unit, count
+        unsigned long long* q = a.tstamp + 8 + 8 * (size_t)P + 24;
+        atomicMax(q + 0, res_now() - tg1);
+        atomicAdd(q + 1, 1ull);
+      }
     }
   }
-  {  // warp units
-    // largest first (class A), so that the last units handed out are short
+  {  // warp units, largest first (class A), so that the last units handed out are short
     const uint32_t UA = sm.upa[nbins], UW = UA + sm.upb[nbins];
     K* stage = e.x + w * WCAP;  // x and y are adjacent: kResWarps * WCAP keys
     for (;;) {
@@ -1063,6 +780,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       if (lane == 0) u = atomicAdd(a.unit_counter + 2, 1u);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= UW) break;
+      const unsigned long long ti0 = a.tstamp ? res_now() : 0;
       const uint16_t* up = u < UA ? sm.upa : sm.upb;
       const uint32_t v = u < UA ? u : u - UA;
       int lo = 0, hi = nbins - 1;  // last bin with up <= v
@@ -1098,9 +816,14 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       __syncwarp();
       int unsorted = 0;  // is_sorted
       for (int i = lane; i + 1 < len; i += 32) unsorted |= stage[i + 1] < stage[i];
-      if (__any_sync(0xffffffffu, unsorted)) res_warp_sort<K, WCAP>(stage, len);
-      for (int i = lane; i < len; i += 32) a.keys[s + i] = stage[i];
+      if (__any_sync(0xffffffffu, unsorted)) {
+        unit_warp_piece<K>(stage, len, a.keys + s);  // <= WCAP keys: one network, or two and a merge
+      } else {
+        for (int i = lane; i < len; i += 32) a.keys[s + i] = stage[i];
+      }
       __syncwarp();
+      if (a.tstamp && lane == 0)  // SR_TIMING: longest warp item
+        atomicMax(a.tstamp + 8 + 8 * (size_t)P + 26, res_now() - ti0);
     }
   }
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[3] = res_now();

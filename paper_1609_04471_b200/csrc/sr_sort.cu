@@ -1172,7 +1172,7 @@ struct Sorter {
     if (NG > slots || G > kResMaxG) fail(SR_ERR_INTERNAL, "resident tile count");
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-      const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 16 + 4 * nbins) +
+      const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 32 + 4 * nbins) +
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
                                     r(4 * (int64_t)NG * nbins) + 8 * 256);
       DevState& dsa = t_state.ds();
@@ -1203,12 +1203,12 @@ struct Sorter {
     a.sums = c.alloc<TileSummary>(G);
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
-    {  // control block: statistics + unit/done counters + bucket totals, zeroed by the kernel
-      const size_t bytes = sizeof(DevStats) + 16 + 4 * (size_t)nbins;
+    {  // control block: statistics | unit counters | bucket totals, zeroed by the kernel
+      const size_t bytes = sizeof(DevStats) + 32 + 4 * (size_t)nbins;
       unsigned char* cb = c.alloc<unsigned char>((int64_t)bytes);
       a.st = reinterpret_cast<DevStats*>(cb);
       a.unit_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
-      a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 16);
+      a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 32);
       a.ctrl_words = (int)(bytes / 4);
     }
     DevState& ts = t_state.ds();
@@ -1244,8 +1244,8 @@ struct Sorter {
     a.merge_ok = route_ok() | kOutlierStrict;
     a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
-    a.tstamp = stamps ? c.alloc<unsigned long long>(8 * P + 32) : nullptr;
-    if (stamps) c.memset0(a.tstamp, 64 * (P + 4));
+    a.tstamp = stamps ? c.alloc<unsigned long long>(8 * P + 64) : nullptr;
+    if (stamps) c.memset0(a.tstamp, 8 * (8 * P + 64));
     const size_t smem = sizeof(ResSmem<K>);
     hostprof("prepared");
     check_cuda(cudaEventRecord(ts.launch_ev, c.st), "cudaEventRecord");
@@ -1268,7 +1268,7 @@ struct Sorter {
     }
     hostprof("read back");
     if (stamps) {
-      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 64 * (P + 4)));
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(c.readback(a.tstamp, 8 * (8 * P + 64)));
       {
         const unsigned long long* q = t + 8 + 8 * P + 8;
         if (q[0] && q[5])
@@ -1280,6 +1280,11 @@ struct Sorter {
         if (q[0] && q[2])
           fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
                   (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
+      }
+      {
+        const unsigned long long* q = t + 8 + 8 * P + 24;
+        fprintf(stderr, "[sr_resident] E items us: longest CTA unit %.1f (%llu units), longest warp unit %.1f\n",
+                q[0] * 1e-3, q[1], q[2] * 1e-3);
       }
       {
         const unsigned long long* e = t + 8 + 8 * P;
