@@ -70,6 +70,31 @@ enum {
                              sorted, merged with the sorted remainder */
 };
 
+/* ------------------------------------------------------------------ inputs */
+
+/* On-device generator of the paper's input classes (§2, lines 56-87;
+ * SURVEY.md §8(f) NEXT #4), bit-identical to workloads/gen.py for the same
+ * seed.  out: device array of n keys (dtype SR_INT32 / SR_INT64), written on
+ * `stream`.  order / param:
+ *   SR_GEN_RANDOM      uniform over the full range (draw i, high 32 bits for int32)
+ *   SR_GEN_SORTED      0..n-1                     SR_GEN_REVERSED  n-1..0
+ *   SR_GEN_SWAPS       ramp + param random position swaps in draw order (k-exchange)
+ *   SR_GEN_FEW_UNIQUE  param distinct uniform values (first param distinct draws),
+ *                      a[i] = v[U[0,param)] from stream seed ^ 0xF00D (k-limited analogue)
+ *   SR_GEN_RUNS        ramp cut into blocks of param, blocks Fisher-Yates shuffled (BASELINE configs[2])
+ *   SR_GEN_LAST        ramp whose last param positions are uniform random (BASELINE configs[2])
+ *   SR_GEN_SHARP_TEETH / _EQUAL_TEETH / _EVEN_TEETH  param sections
+ *   SR_GEN_DISTANCE    ramp, blocks of param+1 each Fisher-Yates shuffled (k-distance)
+ *   SR_GEN_ALL_EQUAL   every key = param         SR_GEN_EXTREMES  MIN/MAX/0/-1/1/MIN+1/MAX-1 mix
+ * Sequential constructions (swaps, shuffles, rejection) run on one GPU thread
+ * (or one per block); the call returns after enqueueing.  Errors:
+ * SR_ERR_INVALID_ARGUMENT (NULL out with n > 0, n < 0, unknown order, param
+ * out of range), SR_ERR_UNSUPPORTED_DTYPE, SR_ERR_OUT_OF_MEMORY (scratch). */
+enum { SR_GEN_RANDOM = 0, SR_GEN_SORTED = 1, SR_GEN_REVERSED = 2, SR_GEN_SWAPS = 3, SR_GEN_FEW_UNIQUE = 4,
+       SR_GEN_RUNS = 5, SR_GEN_LAST = 6, SR_GEN_SHARP_TEETH = 7, SR_GEN_EQUAL_TEETH = 8, SR_GEN_EVEN_TEETH = 9,
+       SR_GEN_DISTANCE = 10, SR_GEN_ALL_EQUAL = 11, SR_GEN_EXTREMES = 12 };
+int32_t sr_generate(void *out, int64_t n, int32_t dtype, int32_t order, uint64_t seed, int64_t param, void *stream);
+
 /* ------------------------------------------------------------------ sort */
 
 /* Sort keys[0..n) ascending in place.  dtype: SR_INT32 / SR_INT64 /

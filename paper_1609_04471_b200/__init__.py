@@ -25,7 +25,7 @@ OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, O
 EXPORTS = [
     "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",
     "sr_set_option", "sr_last_profile", "sr_presort_scan", "sr_reverse_range", "sr_tile_sort", "sr_merge_path",
-    "sr_merge", "sr_splitters", "sr_partition_level",
+    "sr_merge", "sr_splitters", "sr_partition_level", "sr_generate",
 ]
 
 
@@ -68,6 +68,7 @@ def lib():
         L.sr_sort_records.argtypes = [vp, i64, i32, vp]
         L.sr_presortedness.argtypes = [vp, i64, i32, ctypes.POINTER(Measures), vp]
         L.sr_last_plan.argtypes = [ctypes.POINTER(Plan)]
+        L.sr_generate.argtypes = [vp, i64, i32, i32, ctypes.c_uint64, i64, vp]
         L.sr_status_string.argtypes = [i32]
         L.sr_status_string.restype = ctypes.c_char_p
         L.sr_last_error.argtypes = []
@@ -190,6 +191,23 @@ def sort_host(keys: np.ndarray, vals: np.ndarray | None = None, stream: int = 0)
     vp = None if vals is None else vals.ctypes.data_as(ctypes.c_void_p)
     _check(lib().sr_sort_host(keys.ctypes.data_as(ctypes.c_void_p), vp, keys.size, code, ctypes.c_void_p(stream)))
     return keys if vals is None else (keys, vals)
+
+
+GEN_ORDERS = {"random": 0, "sorted": 1, "reversed": 2, "swaps": 3, "few_unique": 4, "runs": 5, "last": 6,
+              "sharp_teeth": 7, "equal_teeth": 8, "even_teeth": 9, "distance": 10, "all_equal": 11, "extremes": 12}
+
+
+def generate(out, order: str, seed: int, param: int = 0):
+    """Fill the CUDA int32/int64 tensor `out` with an input of class `order`
+    on the device (sr_generate; bit-identical to workloads/gen.py for the same
+    seed; see include/sr_sort.h for `param`)."""
+    _dev(out, "out")
+    code = _dtype_code(out)
+    if code not in (SR_INT32, SR_INT64):
+        raise TypeError("generate: int32 or int64 tensors only")
+    _check(lib().sr_generate(_ptr(out), out.numel(), code, GEN_ORDERS[order], seed & (2**64 - 1), int(param),
+                             _stream(out)))
+    return out
 
 
 def last_plan() -> dict:

@@ -15,13 +15,16 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <mutex>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../../include/sr_sort.h"
 #include "fkeys.cuh"
+#include "generate.cuh"
 #include "measures.cuh"
 #include "merge.cuh"
 #include "records.cuh"
@@ -1971,6 +1974,61 @@ int32_t sr_presortedness(const void* keys, int64_t n, int32_t dtype, sr_measures
   return guarded([&] {
     if (dtype == SR_INT32) measures_impl<int32_t>((const int32_t*)keys, n, host_out, (cudaStream_t)stream);
     else measures_impl<int64_t>((const int64_t*)keys, n, host_out, (cudaStream_t)stream);
+  });
+}
+
+int32_t sr_generate(void* out, int64_t n, int32_t dtype, int32_t order, uint64_t seed, int64_t param, void* stream) {
+  t_state.err.clear();
+  if (n < 0 || order < SR_GEN_RANDOM || order > SR_GEN_EXTREMES) return SR_ERR_INVALID_ARGUMENT;
+  if (dtype != SR_INT32 && dtype != SR_INT64) return SR_ERR_UNSUPPORTED_DTYPE;
+  if (n == 0) return SR_OK;
+  if (!out) return SR_ERR_INVALID_ARGUMENT;
+  int dev = -1;
+  if (!is_device_ptr(out, &dev)) return SR_ERR_INVALID_ARGUMENT;
+  if ((uintptr_t)out % key_bytes(dtype)) return SR_ERR_ALIGNMENT;
+  const bool needs_k = order == SR_GEN_SWAPS || order == SR_GEN_LAST || order == SR_GEN_DISTANCE;
+  const bool needs_pos = order == SR_GEN_FEW_UNIQUE || order == SR_GEN_RUNS || order == SR_GEN_SHARP_TEETH ||
+                         order == SR_GEN_EQUAL_TEETH || order == SR_GEN_EVEN_TEETH;
+  if ((needs_k && (param < 0 || (order != SR_GEN_SWAPS && param > n))) || (needs_pos && param < 1) ||
+      (order == SR_GEN_FEW_UNIQUE && param > 65536) || (order == SR_GEN_RUNS && param > n && n > 0))
+    return SR_ERR_INVALID_ARGUMENT;
+  if (dtype == SR_INT32 && order == SR_GEN_ALL_EQUAL && (param < INT32_MIN || param > INT32_MAX))
+    return SR_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(dev);
+  return guarded([&] {
+    Ctx c((cudaStream_t)stream);
+    init_pool();
+    auto run = [&](auto* o) {
+      using K = std::remove_pointer_t<decltype(o)>;
+      K* table = nullptr;
+      int64_t* perm = nullptr;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div<int64_t>(n, 256)));
+      if (order == SR_GEN_FEW_UNIQUE) {
+        table = c.alloc<K>(param);
+        c.launch("gen_table", param * (int64_t)sizeof(K), [&] { k_gen_table<K><<<1, 32, 0, c.st>>>(table, param, seed); });
+      } else if (order == SR_GEN_EXTREMES) {
+        const K mn = std::numeric_limits<K>::min(), mx = std::numeric_limits<K>::max();
+        std::vector<K> t{mn, mx, 0, -1, 1, (K)(mn + 1), (K)(mx - 1)};
+        table = c.alloc<K>(7);
+        c.upload(table, t);
+      } else if (order == SR_GEN_RUNS) {
+        const int64_t nb = ceil_div<int64_t>(n, param);
+        perm = c.alloc<int64_t>(nb + 1);
+        c.launch("gen_perm", nb * 8, [&] { k_gen_perm<<<1, 32, 0, c.st>>>(perm, nb, seed); });
+      }
+      c.launch("gen_map", n * (int64_t)sizeof(K), [&] {
+        k_gen_map<K><<<grid, 256, 0, c.st>>>(o, n, order, seed, param, table, perm);
+      });
+      if (order == SR_GEN_SWAPS && param > 0)
+        c.launch("gen_swaps", 4 * param * (int64_t)sizeof(K), [&] { k_gen_swaps<K><<<1, 32, 0, c.st>>>(o, n, seed, param); });
+      if (order == SR_GEN_DISTANCE && param > 0) {
+        const int64_t nblocks = ceil_div<int64_t>(n, param + 1);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(nblocks, 128)));
+        c.launch("gen_distance", 2 * n * (int64_t)sizeof(K), [&] { k_gen_distance<K><<<g, 128, 0, c.st>>>(o, n, seed, param); });
+      }
+    };
+    if (dtype == SR_INT32) run((int32_t*)out);
+    else run((int64_t*)out);
   });
 }
 
