@@ -99,6 +99,22 @@ def make_input(order, n, dtype, config, instance):
     return gen.make(order, n, dtype, config=config, instance=instance)
 
 
+def make_input_dev(sr, order, n, dtype, config, instance, dev):
+    """The same input as make_input, generated on the device by sr_generate
+    (random and swap orders of integer keys), else None."""
+    import torch
+    if is_rec(dtype) or np.dtype(dtype).kind != "i":
+        return None
+    t = torch.empty(n, dtype=torch.int32 if np.dtype(dtype) == np.int32 else torch.int64, device=dev)
+    if order == "random":
+        sr.generate(t, "random", gen.seed_for(config, gen.ORDERS["random"], instance))
+    elif order == "nearly1000":
+        sr.generate(t, "swaps", gen.seed_for(config, 2, instance), n // 1000)
+    else:
+        return None
+    return t
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -359,6 +375,11 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     ids = instance_ids(rank, total)
     for o in orders:
         for i in range(ninst):
+            t = make_input_dev(sr, o, n, dtype, cfg, ids[i], dev) if big else None
+            if t is not None:  # 1 GiB inputs: built on the device (sr_generate, bit-identical to gen.py)
+                pristine[(o, i)] = t
+                host_inputs[(o, i)] = t.cpu().numpy()
+                continue
             a = make_input(o, n, dtype, cfg, ids[i])
             pristine[(o, i)] = torch.from_numpy(a).to(dev)
             host_inputs[(o, i)] = a

@@ -1989,7 +1989,7 @@ int32_t sr_generate(void* out, int64_t n, int32_t dtype, int32_t order, uint64_t
   const bool needs_k = order == SR_GEN_SWAPS || order == SR_GEN_LAST || order == SR_GEN_DISTANCE;
   const bool needs_pos = order == SR_GEN_FEW_UNIQUE || order == SR_GEN_RUNS || order == SR_GEN_SHARP_TEETH ||
                          order == SR_GEN_EQUAL_TEETH || order == SR_GEN_EVEN_TEETH;
-  if ((needs_k && (param < 0 || (order != SR_GEN_SWAPS && param > n))) || (needs_pos && param < 1) ||
+  if ((needs_k && (param < 0 || (order == SR_GEN_LAST && param > n))) || (needs_pos && param < 1) ||
       (order == SR_GEN_FEW_UNIQUE && param > 65536) || (order == SR_GEN_RUNS && param > n && n > 0))
     return SR_ERR_INVALID_ARGUMENT;
   if (dtype == SR_INT32 && order == SR_GEN_ALL_EQUAL && (param < INT32_MIN || param > INT32_MAX))

@@ -186,3 +186,22 @@ def test_resident_few_tiles(n):
     """Small resident sizes: fewer tiles than CTAs (most CTAs scan nothing)."""
     for order in ["random", "reversed", "sorted", "few_unique", "organ_pipe"]:
         check(gen.make(order, n, np.int32, config=16))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_two_devices_same_thread():
+    """One host thread sorting on two devices alternately: the resident path's
+    per-thread state (arena, arrival counter, completion record, graphs, the
+    shared-memory attribute) is kept per device, and the call runs on the
+    device that owns the keys even when another device is current."""
+    n = 1_000_000
+    k = gen.make("random", n, np.int32, config=1)
+    exp = oracle.sort_keys(k)
+    torch.cuda.set_device(0)
+    for rep in range(3):
+        for d in (0, 1):
+            t = torch.from_numpy(k.copy()).to(f"cuda:{d}")
+            sr.sort_keys(t)  # device 0 stays current; keys on device d
+            torch.cuda.synchronize(d)
+            assert np.array_equal(t.cpu().numpy(), exp), (rep, d)
+            assert sr.last_plan()["route_name"] == "partition"
