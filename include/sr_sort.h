@@ -187,8 +187,13 @@ enum {
                               maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
                               host-driven partition levels (tests lower it) */
   SR_OPT_OUTLIER_ROUTE = 5, /* 0: never choose the outlier route automatically */
-  SR_OPT_WS_LIMIT = 6     /* fault injection: device workspace bytes one call may take (0 = no limit); a
+  SR_OPT_WS_LIMIT = 6,    /* fault injection: device workspace bytes one call may take (0 = no limit); a
                              larger reservation fails with SR_ERR_OUT_OF_MEMORY as a real one would */
+  SR_OPT_TUNE = 16        /* SR_OPT_TUNE + i, i < 8: tuning knobs of the large keys-only path (A/B runs):
+                             +0 fused second level (k_bucket_sort) 1/0 (default 0: measured slower, DESIGN.md
+                             §6.3); +1 level-1 buckets for n >= 2^26 (power of two <= 2048, default 512); +2 mean sub-bucket of
+                             the fused level (16..4096, default 256); +3 cap on the level-1 buckets at
+                             any n (power of two, 0 = none; tests reach the fused level at small n) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

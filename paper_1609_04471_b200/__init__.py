@@ -21,6 +21,7 @@ ROUTES = {0: "none", 1: "sorted", 2: "reversed", 3: "merge", 4: "partition", 5: 
 ROUTE_MERGE, ROUTE_PARTITION, ROUTE_OUTLIER = 3, 4, 6
 OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE, OPT_WS_LIMIT = (
     0, 1, 2, 3, 4, 5, 6)
+OPT_TUNE = 16  # + 0 fused second level, + 1 level-1 buckets (n >= 2^26), + 2 fused mean sub-bucket
 
 EXPORTS = [
     "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",

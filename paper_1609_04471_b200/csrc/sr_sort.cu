@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "../../include/sr_sort.h"
+#include "bucket_sort.cuh"
 #include "fkeys.cuh"
 #include "generate.cuh"
 #include "measures.cuh"
@@ -45,6 +46,11 @@ int g_resident = 1;
 int g_outlier = 1;
 int g_res_cap = 16384;
 int64_t g_ws_limit = 0;  // SR_OPT_WS_LIMIT (fault injection), 0 = none
+// SR_OPT_TUNE + i: tuning knobs of the large keys-only path (A/B measurements)
+//   [0] fused level 2 (k_bucket_sort) on/off   [1] level-1 buckets for n >= kBigLevel1
+//   [2] mean sub-bucket the fused level aims for   [3] cap on the level-1 buckets at any n (0 = none; tests)
+//   [4] k_bucket_sort phase skips (timing experiments only; the output is then NOT sorted): 1 finishing, 2 scatter
+int64_t g_tune[8] = {0, 512, 256, 0, 0, 0, 0, 0};
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -491,7 +497,8 @@ int choose_buckets(int64_t len, int level = 1) {
   // scatter writes runs of >= 32 keys per 16K-key sub-tile (full DRAM sectors;
   // shorter runs cost read-modify-writes) and the level-2 scatter writes stay
   // within a few L2-resident segments
-  if (level == 1 && len >= kBigLevel1) b = std::min<int64_t>(b, kBigLevel1Buckets);
+  if (level == 1 && len >= kBigLevel1) b = std::min<int64_t>(b, g_tune[1] > 0 ? g_tune[1] : kBigLevel1Buckets);
+  if (level == 1 && g_tune[3] > 0) b = std::min<int64_t>(b, g_tune[3]);
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
@@ -850,9 +857,90 @@ struct Sorter {
   }
   int h_fin_big = -1;
 
+  // Fused level 2 + finishing (bucket_sort.cuh): keys only, the parts in the
+  // workspace, every part small enough for one CTA's level of <= B2MAX bins.
+  // A part qualifies when its B2MAX sub-buckets average at most half of what
+  // one warp sorts (larger parts, e.g. from a skewed level-1 sample, take the
+  // multi-kernel level).
+  bool bs_fits(const OvfSeg& p, int src) const {
+    return !HAS_V && src == 1 && g_tune[0] && p.len <= (int64_t)BsCfg<K>::B2MAX * (BsCfg<K>::PIECE / 2);
+  }
+  void run_bucket_sort(const std::vector<OvfSeg>& parts) {
+    using C = BsCfg<K>;
+    Level L;
+    L.src = 1;
+    L.level = 2;
+    int64_t tot = 0;
+    for (auto& p : parts) {
+      SegDesc d{};
+      d.start = p.start;
+      d.len = p.len;
+      d.nbuckets = (int)std::min<int64_t>(C::B2MAX, std::max<int64_t>(2, pow2ceil(ceil_div<int64_t>(p.len, std::max<int64_t>(16, g_tune[2])))));
+      d.nbins = 2 * d.nbuckets + 1;
+      d.sample_base = L.sample_total;
+      const int64_t S_s = std::min<int64_t>({d.len, (int64_t)d.nbuckets * kOversample, (int64_t)kMaxSample});
+      L.sample_total += S_s;
+      L.max_sample = std::max<int>(L.max_sample, (int)S_s);
+      tot += p.len;
+      L.segs.push_back(d);
+    }
+    const int64_t S = (int64_t)parts.size();
+    L.d_segs = c.alloc<SegDesc>(S);
+    L.d_spl = c.alloc<K>(S * kMaxBuckets);
+    L.d_eq = c.alloc<uint8_t>(S * kMaxBuckets);
+    L.d_m = c.alloc<int>(S);
+    // control block: stats | segment counter (zeroed together)
+    unsigned char* cb = c.alloc<unsigned char>(sizeof(DevStats) + 256);
+    c.memset0(cb, sizeof(DevStats) + 256);
+    L.d_st = reinterpret_cast<DevStats*>(cb);
+    uint32_t* d_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
+    const int64_t big_cap = S * C::B2MAX;
+    Item* d_big = c.alloc<Item>(big_cap);
+    OvfSeg* d_ovf = c.alloc<OvfSeg>(big_cap);
+    c.upload(L.d_segs, L.segs);
+    level_splitters(L);
+    auto kern = k_bucket_sort<K>;
+    const size_t smem = sizeof(BsSmem<K>);
+    set_smem(kern, smem);
+    static int grid_cache[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (!grid_cache[dev]) {
+      int per = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NT, smem);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_cache[dev] = std::max(1, per) * std::max(1, sms);
+    }
+    const int grid = (int)std::min<int64_t>(S, grid_cache[dev]);
+    K* kk = keys;
+    const K* src = wk;
+    const int nseg = (int)S;
+    c.launch("bucket_sort", 2 * tot * kw, [&] {
+      kern<<<grid, C::NT, smem, c.st>>>(src, kk, L.d_segs, nseg, L.d_spl, L.d_eq, L.d_m, d_counter, d_big, d_ovf,
+                                        L.d_st, (int)g_tune[4]);
+    });
+    const int h_big = finish(d_big, &L.d_st->n_items_big, 0, big_cap, 0);
+    DevStats hs = *reinterpret_cast<DevStats*>(c.readback(L.d_st, sizeof(DevStats)));
+    c.replan(h_big, 2 * hs.big_keys * kw);
+    c.plan.levels = 2;
+    if (hs.n_ovf > 0) {
+      const OvfSeg* h = reinterpret_cast<const OvfSeg*>(c.readback(d_ovf, sizeof(OvfSeg) * hs.n_ovf));
+      std::vector<OvfSeg> next(h, h + hs.n_ovf);
+      run_levels(next, 0, 3);
+    }
+  }
+
   // Partition levels >= 2 (segments from the previous level's oversized buckets).
-  void run_levels(std::vector<OvfSeg> parts, int src) {
-    int level = 2;
+  void run_levels(std::vector<OvfSeg> parts, int src, int level = 2) {
+    {
+      std::vector<OvfSeg> fused, rest;
+      for (auto& p : parts) (bs_fits(p, src) ? fused : rest).push_back(p);
+      if (!fused.empty()) {
+        parts.swap(rest);
+        run_bucket_sort(fused);  // (its own leftovers recurse from `keys`)
+      }
+    }
     while (!parts.empty()) {
       if (level > 12) fail(SR_ERR_INTERNAL, "partition did not converge");
       int64_t tot = 0;
@@ -2082,6 +2170,15 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       g_res_cap = (int)value;
       return SR_OK;
     default:
+      if (key >= SR_OPT_TUNE && key < SR_OPT_TUNE + 8) {
+        if (key == SR_OPT_TUNE + 1 && (value < 2 || value > kMaxBuckets || (value & (value - 1))))
+          return SR_ERR_INVALID_ARGUMENT;
+        if (key == SR_OPT_TUNE + 2 && (value < 16 || value > 4096)) return SR_ERR_INVALID_ARGUMENT;
+        if (key == SR_OPT_TUNE + 3 && (value < 0 || value > kMaxBuckets || (value & (value - 1))))
+          return SR_ERR_INVALID_ARGUMENT;
+        g_tune[key - SR_OPT_TUNE] = value;
+        return SR_OK;
+      }
       return SR_ERR_INVALID_ARGUMENT;
   }
 }
