@@ -21,6 +21,7 @@
 #include "bitonic.cuh"
 #include "block_sort.cuh"
 #include "common.cuh"
+#include "guide.cuh"
 #include "presort.cuh"
 #include "types.cuh"
 
@@ -278,31 +279,33 @@ __device__ __forceinline__ int64_t vec4_pos(int64_t s0, int u) {
 }
 
 // ---------------------------------------------------------------------------
-// K8: bucket histogram of one chunk (levels >= 2; level 1 fuses it into K1).
+// K8: bucket histogram of one chunk.  The segment's guide table (guide.cuh,
+// built once per level by k_guide_build) is copied into shared memory; each
+// key's 3-way bucket id is found by the table-narrowed,
+// branch-free bisection over the distinct splitters.
+template <typename K>
+struct CountSmem {
+  GuideTab<K> g;
+  uint32_t hist[kMaxBins];
+};
+
 template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const SegDesc* __restrict__ segs,
                                                const int* __restrict__ chunk_seg, int64_t chunk_size,
-                                               const K* __restrict__ spl_all, const uint8_t* __restrict__ eq_all,
-                                               const int* __restrict__ m_all, uint32_t* __restrict__ mat,
+                                               const GuideTab<K>* __restrict__ guides, uint32_t* __restrict__ mat,
                                                uint32_t* __restrict__ tot, uint16_t* __restrict__ bins_out,
                                                const DevStats* __restrict__ gate) {
   if (gate && gate->route != kRoutePartition) return;  // speculative launch
   constexpr int U = 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ClassifySmem<K>& csm = *reinterpret_cast<ClassifySmem<K>*>(smem_raw);
-  K* s_spl = csm.tree;
-  uint8_t* s_eq = csm.eq;
+  CountSmem<K>& csm = *reinterpret_cast<CountSmem<K>*>(smem_raw);
   uint32_t* s_hist = csm.hist;
   const int c = blockIdx.x;
   const int s = chunk_seg[c];
   const SegDesc seg = segs[s];
   const int g = c - seg.chunk_base;
-  const int m = m_all[s];
-  const int depth = tree_depth(m);
-  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, s_spl, s_eq);
+  guide_load(guides + s, csm.g);
   for (int b = threadIdx.x; b < seg.nbins; b += NT) s_hist[b] = 0;
-  __syncthreads();
-  build_guide<K>(s_spl + kMaxBuckets, m, csm.guide);
   __syncthreads();
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(NT) k_count(const K* __restrict__ src, const S
       }
     }
     int bin[U];
-    classify_keys_guided<K, U>(x, bin, s_spl + kMaxBuckets, s_eq, csm.guide);
+    guide_classify<K, U>(x, bin, csm.g);
 #pragma unroll
     for (int u = 0; u < U; u++) hist_add(s_hist, bin[u], (valid >> u) & 1);
     if (bins_out) {  // reused by the scatter

@@ -48,6 +48,7 @@
 
 #include "bitonic.cuh"
 #include "common.cuh"
+#include "guide.cuh"
 #include "partition.cuh"
 #include "presort.cuh"
 #include "types.cuh"
@@ -191,11 +192,15 @@ struct ResSmem {
   using E = UnitSmem<K, CAPB, kResNT>;  // E: the CTA units (unit_sort.cuh); warp-unit staging spans x and y
   static_assert(kResWarps * WCAP <= 2 * CAPB, "warp-unit staging areas live in x and y");
   uint32_t start[NB1 + 1];         // level-1 bucket starts, start[nbins] = n
-  uint16_t upa[NB1 + 1];           // exclusive prefix of E warp units, class A (WCAP/2 < range bucket <= WCAP)
-  uint16_t upb[NB1 + 1];           // exclusive prefix of E warp units, class B (smaller range buckets, fills)
-  uint16_t cbin[B1MAX + 8];        // E CTA units: range buckets above WCAP
-  K tree1[2 * B1MAX];              // level-1 Eytzinger tree [1, B1) + sorted splitters at [B1MAX, ...)
-  uint8_t eq1[B1MAX];
+  struct EU {                      // E: unit lists
+    uint16_t upa[NB1 + 1];         // exclusive prefix of E warp units, class A (WCAP/2 < range bucket <= WCAP)
+    uint16_t upb[NB1 + 1];         // exclusive prefix of E warp units, class B (smaller range buckets, fills)
+    uint16_t cbin[B1MAX + 8];      // E CTA units: range buckets above WCAP
+  };
+  union alignas(16) {
+    GuideTab<K, 2048, B1MAX> guide1;  // C: level-1 classification table (guide.cuh)
+    EU eu;                         // E
+  } v;
   union alignas(16) {
     K samp1[S1MAX];                // A: the sampler's piece of the sample + BitonicSort scratch
     SP sp;
@@ -428,7 +433,6 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   }
   if (route != kRoutePartition) return;  // MERGE / undecided: the host planner continues
   const int m1 = a.B1 - 1;
-  const int depth1 = tree_depth(m1);
   if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
     static_assert(kResSamplers == 4, "four sorted sample pieces");
     // (sampler steps are counted in unit_counter[3]: CTA 0 zeroed it before
@@ -508,13 +512,16 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   grid.sync();
 
   // ================= C: splitter tree; tile-local bucket grouping =================
-  for (int j = tid; j < B1MAX; j += NT) {  // the splitter copy at tree1[B1MAX + j] lives outside the union
-    sm.tree1[B1MAX + j] = __ldcg(a.spl + j);
-    sm.eq1[j] = __ldcg(a.spf + j);
+  {  // the splitters (staged in the union's phase-C buffers) -> this CTA's guide table
+    K* s_spl = sm.u.ct.stk[0];
+    uint8_t* s_eq = reinterpret_cast<uint8_t*>(sm.u.ct.stb[0]);
+    for (int j = tid; j < m1; j += NT) {
+      s_spl[j] = __ldcg(a.spl + j);
+      s_eq[j] = __ldcg(a.spf + j);
+    }
+    __syncthreads();
+    guide_build<K, NT>(s_spl, s_eq, m1, sm.v.guide1, sm.red);
   }
-  __syncthreads();
-  res_build_tree<K, B1MAX>(depth1, sm.tree1);
-  __syncthreads();
   SR_RES_STAMP(3);
   const int ngm = (c < PS && a.NG > c) ? (a.NG - 1 - c) / PS + 1 : 0;  // groups of this CTA: t = c + k PS, k < ngm <= GPC
   {
@@ -533,7 +540,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         const int64_t i = t0 + u * NT + tid;
         x[u] = i < t1 ? a.keys[i] : K(0);
       }
-      res_classify<K, B1MAX, U>(x, bin, sm.tree1, sm.eq1, m1, depth1);
+      guide_classify<K, U>(x, bin, sm.v.guide1);
       SR_RES_SUB(1);
       __syncthreads();
       uint32_t rk[U];
@@ -688,8 +695,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     for (int r = 0; r < BPT; r++) {
       const int b = tid * BPT + r;
       if (b <= nbins) {
-        sm.upa[b] = (uint16_t)pa;
-        sm.upb[b] = (uint16_t)pb;
+        sm.v.eu.upa[b] = (uint16_t)pa;
+        sm.v.eu.upb[b] = (uint16_t)pb;
       }
       pa += ca[r];
       pb += cb[r];
@@ -709,14 +716,14 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     for (int r = 0; r < BPT; r++) {
       const int b = tid * BPT + r;
       if (b < nbins && !(b & 1) && start[b + 1] - start[b] > (uint32_t)WCAP) {
-        sm.cbin[o] = (uint16_t)b;
+        sm.v.eu.cbin[o] = (uint16_t)b;
         o++;
       }
     }
     NC = tot;
     __syncthreads();
   }
-  if (c == 0 && tid == 0) a.st->n_items = (int64_t)sm.upa[nbins] + sm.upb[nbins] + NC;
+  if (c == 0 && tid == 0) a.st->n_items = (int64_t)sm.v.eu.upa[nbins] + sm.v.eu.upb[nbins] + NC;
   __shared__ uint32_t s_unit;
   typename SM::E& e = sm.u.e;
   if (NC > 0) {
@@ -728,7 +735,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       if (u >= (uint32_t)NC) break;
       // a big bucket beyond the in-kernel cap: copied unsorted into its final
       // range and listed for the host's next level
-      const int b = (int)sm.cbin[u];
+      const int b = (int)sm.v.eu.cbin[u];
       const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
       const unsigned long long tg0 = (a.tstamp && c == 0 && tid == 0) ? res_now() : 0;
       const unsigned long long tg1 = a.tstamp ? res_now() : 0;
@@ -773,7 +780,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     }
   }
   {  // warp units, largest first (class A), so that the last units handed out are short
-    const uint32_t UA = sm.upa[nbins], UW = UA + sm.upb[nbins];
+    const uint32_t UA = sm.v.eu.upa[nbins], UW = UA + sm.v.eu.upb[nbins];
     K* stage = e.x + w * WCAP;  // x and y are adjacent: kResWarps * WCAP keys
     for (;;) {
       uint32_t u = 0;
@@ -781,7 +788,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= UW) break;
       const unsigned long long ti0 = a.tstamp ? res_now() : 0;
-      const uint16_t* up = u < UA ? sm.upa : sm.upb;
+      const uint16_t* up = u < UA ? sm.v.eu.upa : sm.v.eu.upb;
       const uint32_t v = u < UA ? u : u - UA;
       int lo = 0, hi = nbins - 1;  // last bin with up <= v
       while (lo < hi) {
@@ -791,7 +798,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       const int b = lo;
       const int s = (int)start[b], len = (int)(start[b + 1] - start[b]);
       if (b & 1) {  // equality bucket: fill
-        const K key = sm.tree1[B1MAX + (b - 1) / 2];
+        const K key = __ldcg(a.spl + (b - 1) / 2);
         const int f0 = (int)(v - up[b]) * kResWarpFill;
         const int f1 = f0 + kResWarpFill < len ? f0 + kResWarpFill : len;
         for (int i = f0 + lane; i < f1; i += 32) a.keys[s + i] = key;

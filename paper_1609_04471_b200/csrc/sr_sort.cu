@@ -622,6 +622,7 @@ struct Sorter {
     uint32_t* d_rank = nullptr;
     K* d_sample = nullptr;
     uint16_t* d_bins = nullptr;  // per-key bucket ids from the count pass (indexed by position)
+    GuideTab<K>* d_guide = nullptr;  // per-segment classification tables (k_guide_build)
     int64_t sample_total = 0;
     int max_sample = 0;
   };
@@ -748,12 +749,17 @@ struct Sorter {
     const K* src = buf_k(L.src);
     int64_t keys_in = 0;
     for (auto& s : L.segs) keys_in += s.len;
+    const int S = (int)L.segs.size();
+    if (!L.d_guide) L.d_guide = c.alloc<GuideTab<K>>(S);
+    c.launch("guide_build", 0, [&] {
+      k_guide_build<K, 1024><<<S, 1024, 0, c.st>>>(L.d_spl, L.d_eq, L.d_m, L.d_guide, gate);
+    });
     auto kern = k_count<K, kCountNT>;
-    const size_t smem = sizeof(ClassifySmem<K>);
+    const size_t smem = sizeof(CountSmem<K>);
     set_smem(kern, smem);
     c.launch("count", keys_in * kw + L.mat_entries * 4, [&] {
-      kern<<<(unsigned)L.total_chunks, kCountNT, smem, c.st>>>(
-          src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_tot, L.d_bins, gate);
+      kern<<<(unsigned)L.total_chunks, kCountNT, smem, c.st>>>(src, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_guide,
+                                                               L.d_mat, L.d_tot, L.d_bins, gate);
     });
   }
 
