@@ -113,6 +113,7 @@ struct ResArgs {
   int capb;                 // largest level-1 bucket sorted in-kernel (CAPB; lowered by tests)
   unsigned long long* tstamp;  // optional: %globaltimer, [0..8) CTA 0 phase starts, then 8 per CTA
   uint32_t* unit_counter;   // [0] CTA units, [2] warp units, [3] sampler steps (zeroed by CTA 0 in phase A)
+  uint32_t* pairc;          // B1MAX: halves done per class-A warp unit (zeroed with the control block)
   uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
   uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
@@ -779,17 +780,61 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       }
     }
   }
-  {  // warp units, largest first (class A), so that the last units handed out are short
-    const uint32_t UA = sm.v.eu.upa[nbins], UW = UA + sm.v.eu.upb[nbins];
+  {  // warp units, largest first: the halves of the class-A buckets (two warps
+     // each, the second to finish merges), then class B (one warp each), so
+     // that the last units handed out are short
+    const uint32_t UA = sm.v.eu.upa[nbins], UW = 2 * UA + sm.v.eu.upb[nbins];
     K* stage = e.x + w * WCAP;  // x and y are adjacent: kResWarps * WCAP keys
+    constexpr int NET = UnitNet<K>::NET;
+    static_assert(2 * NET == WCAP, "a class-A bucket is two networks");
     for (;;) {
       uint32_t u = 0;
       if (lane == 0) u = atomicAdd(a.unit_counter + 2, 1u);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= UW) break;
       const unsigned long long ti0 = a.tstamp ? res_now() : 0;
-      const uint16_t* up = u < UA ? sm.v.eu.upa : sm.v.eu.upb;
-      const uint32_t v = u < UA ? u : u - UA;
+      if (u < 2 * UA) {  // half h of class-A bucket v (WCAP/2 < len <= WCAP): sort it in ws
+        const uint32_t v = u >> 1;
+        const int h = (int)(u & 1);
+        const uint16_t* up = sm.v.eu.upa;
+        int lo = 0, hi = nbins - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (up[mid] <= v) lo = mid; else hi = mid - 1;
+        }
+        const int s = (int)start[lo], len = (int)(start[lo + 1] - start[lo]);
+        const int h0 = h ? NET : 0, hl = h ? len - NET : NET;
+        K* hw = a.ws + s + h0;
+        for (int i = lane; i < hl; i += 32) stage[i] = __ldcg(hw + i);
+        __syncwarp();
+        int unsorted = 0;  // is_sorted
+        for (int i = lane; i + 1 < hl; i += 32) unsorted |= stage[i + 1] < stage[i];
+        if (__any_sync(0xffffffffu, unsorted)) {
+          unit_warp_sort<K>(stage, hl);
+          for (int i = lane; i < hl; i += 32) hw[i] = stage[i];
+        }
+        __threadfence();  // this half is in ws before the pair counter says so
+        __syncwarp();
+        uint32_t prev = 0;
+        if (lane == 0) prev = atomicAdd(a.pairc + v, 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == 1) {  // the other half is done too: merge both into keys (A wins ties)
+          __threadfence();
+          for (int i = lane; i < len; i += 32) stage[i] = __ldcg(a.ws + s + i);
+          __syncwarp();
+          if (stage[NET - 1] <= stage[NET]) {  // trimmed: already in order
+            for (int i = lane; i < len; i += 32) a.keys[s + i] = stage[i];
+            __syncwarp();
+          } else {
+            unit_warp_merge<K>(stage, NET, stage + NET, len - NET, a.keys + s);
+          }
+        }
+        if (a.tstamp && lane == 0)  // SR_TIMING: longest warp item
+          atomicMax(a.tstamp + 8 + 8 * (size_t)P + 26, res_now() - ti0);
+        continue;
+      }
+      const uint16_t* up = sm.v.eu.upb;
+      const uint32_t v = u - 2 * UA;
       int lo = 0, hi = nbins - 1;  // last bin with up <= v
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;

@@ -1271,6 +1271,7 @@ struct Sorter {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
       const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 32 + 4 * nbins) +
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
+                                    r(4 * ResCfg<K>::B1MAX) +
                                     r(4 * (int64_t)NG * nbins) + 8 * 256);
       DevState& dsa = t_state.ds();
       if (dsa.has_last && dsa.last_stream != c.st)  // the arena of the last call is in use until its kernel ends
@@ -1301,11 +1302,12 @@ struct Sorter {
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
     {  // control block: statistics | unit counters | bucket totals, zeroed by the kernel
-      const size_t bytes = sizeof(DevStats) + 32 + 4 * (size_t)nbins;
+      const size_t bytes = sizeof(DevStats) + 32 + 4 * (size_t)nbins + 4 * (size_t)ResCfg<K>::B1MAX;
       unsigned char* cb = c.alloc<unsigned char>((int64_t)bytes);
       a.st = reinterpret_cast<DevStats*>(cb);
       a.unit_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
       a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 32);
+      a.pairc = a.tot + nbins;
       a.ctrl_words = (int)(bytes / 4);
     }
     DevState& ts = t_state.ds();

@@ -104,6 +104,28 @@ __device__ __forceinline__ void unit_warp_sort(K* ks, int len) {
   else unit_warp_net<K, UnitNet<K>::VTMAX>(ks, len);
 }
 
+// One warp merges the sorted runs A[0, na) and B[0, nb) (shared memory) into
+// dst[0, na + nb): each lane takes an equal slice of the output, finds its
+// start by merge path and merges serially (A wins ties).
+template <typename K>
+__device__ __forceinline__ void unit_warp_merge(const K* A, int na, const K* B, int nb, K* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int len = na + nb;
+  const int per = (len + 31) / 32;
+  const int d0 = lane * per, d1 = min(len, d0 + per);
+  if (d0 < d1) {
+    int i = merge_path_search<K>([&](int q) { return A[q]; }, na, [&](int q) { return B[q]; }, nb, d0);
+    int j = d0 - i;
+    for (int d = d0; d < d1; d++) {
+      const bool tA = j >= nb || (i < na && !(B[j] < A[i]));
+      dst[d] = tA ? A[i] : B[j];
+      i += tA;
+      j += !tA;
+    }
+  }
+  __syncwarp();
+}
+
 // One warp sorts ks[0, len) (len <= UnitNet<K>::PIECE, 16-byte aligned, slack
 // readable) and writes it to dst[0, len): one network, or two networks and a
 // merge-path merge (A = the first NET keys wins ties).
@@ -119,22 +141,7 @@ __device__ __forceinline__ void unit_warp_piece(K* ks, int len, K* __restrict__ 
   }
   unit_warp_net<K, UnitNet<K>::VTMAX>(ks, NET);
   unit_warp_net<K, UnitNet<K>::VTMAX>(ks + NET, len - NET);
-  const K* A = ks;
-  const K* B = ks + NET;
-  const int nb = len - NET;
-  const int per = (len + 31) / 32;
-  const int d0 = lane * per, d1 = min(len, d0 + per);
-  if (d0 < d1) {
-    int i = merge_path_search<K>([&](int q) { return A[q]; }, NET, [&](int q) { return B[q]; }, nb, d0);
-    int j = d0 - i;
-    for (int d = d0; d < d1; d++) {
-      const bool tA = j >= nb || (i < NET && !(B[j] < A[i]));
-      dst[d] = tA ? A[i] : B[j];
-      i += tA;
-      j += !tA;
-    }
-  }
-  __syncwarp();
+  unit_warp_merge<K>(ks, NET, ks + NET, len - NET, dst);
 }
 
 // CTA-wide merge sort of a[0, L) (any L <= CAP) into dst, b as scratch: runs of
