@@ -585,57 +585,79 @@ __global__ void __launch_bounds__(NT) k_plan(const SegDesc* __restrict__ segs, c
 // ---------------------------------------------------------------------------
 // K10: stable 3-way scatter of one chunk (H10).  The chunk is processed in
 // sub-tiles of NT*VTS keys in input order; within a sub-tile each key's rank
-// among equal-bucket keys comes from per-warp counters (match-any + popc),
-// so the scatter is stable.  Keys are staged in shared memory in bucket order
-// and written out contiguously per bucket.  Keys of equality buckets are not
+// among equal-bucket keys comes from per-warp counters (lanes with the same
+// bucket found by one ballot per id bit, popc of the lower lanes), so the
+// scatter is stable.  Keys are staged in shared memory in bucket order and
+// written out contiguously per bucket.  Keys of equality buckets are not
 // written (the finishing fill writes them; "spared"); their
 // payloads are.
-template <typename K, bool HAS_V, int NT, int VTS>
+//
+// NBMAX < kMaxBins: the COMPACT variant for levels whose splitters take few
+// distinct values (few-unique inputs, e.g. configs[3]: 100 values among 2047
+// splitters): bucket id b = 2i + e (i = a first-occurrence index of the
+// guide table, guide.cuh) is renumbered 2k + e over the md distinct splitters,
+// so the per-sub-tile bucket tables shrink from 2 B + 1 to 2 md + 2 entries
+// and shared memory from ~190 KB to ~60 KB (three CTAs per SM instead of one).
+// Each instance serves the segments of its size class and exits on the others.
+constexpr int kBinBits = 13;  // bucket ids 0 .. kMaxBins (invalid) < 2^13
+static_assert(kMaxBins < (1 << kBinBits), "");
+constexpr int bits_for(int v) { return v <= 1 ? 1 : 1 + bits_for(v >> 1); }  // bits of 0..v
+
+template <typename K, bool HAS_V, int NT, int VTS, int NBMAX>
 struct ScatterSmem {
   static constexpr int NW = NT / 32;
   static constexpr int ST = NT * VTS;
-  K spl[2 * kMaxBuckets];
+  static constexpr bool COMPACT = NBMAX < kMaxBins;
   K stk[ST];
   uint32_t stv[HAS_V ? ST : 1];
-  uint32_t cur[kMaxBins];
-  uint32_t lstart[kMaxBins];
-  uint32_t tot[kMaxBins];
+  uint32_t cur[NBMAX];
+  uint32_t lstart[NBMAX];
+  uint32_t tot[NBMAX];
   uint16_t stb[ST];
-  uint16_t wcnt[NW][kMaxBins + 1];
-  uint8_t eq[kMaxBuckets];
+  uint16_t wcnt[NW][NBMAX + 1];
+  uint16_t inv[COMPACT ? kMaxBuckets + 1 : 1];  // splitter index i -> distinct index k
   uint32_t red[NT / 32 + 1];
 };
 
-constexpr int kBinBits = 13;  // bucket ids 0 .. kMaxBins (invalid) < 2^13
-static_assert(kMaxBins < (1 << kBinBits), "");
+constexpr int kCompactBins = 512;  // compact variant: 2 md + 2 <= 512 bucket ids
 
-template <typename K, bool HAS_V, int NT, int VTS>
+template <typename K, bool HAS_V, int NT, int VTS, int NBMAX>
 __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
                                                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v,
                                                  const SegDesc* __restrict__ segs, const int* __restrict__ chunk_seg,
-                                                 int64_t chunk_size, const K* __restrict__ spl_all,
-                                                 const uint8_t* __restrict__ eq_all, const int* __restrict__ m_all,
+                                                 int64_t chunk_size, const GuideTab<K>* __restrict__ guides,
                                                  const uint32_t* __restrict__ mat, const uint16_t* __restrict__ bins_in,
                                                  const DevStats* __restrict__ gate) {
-  using SM = ScatterSmem<K, HAS_V, NT, VTS>;
+  using SM = ScatterSmem<K, HAS_V, NT, VTS, NBMAX>;
+  constexpr bool COMPACT = SM::COMPACT;
   // speculative launch: only on the partition route, and keys-only with every
   // key in an equality bucket needs no scatter at all
   if (gate && (gate->route != kRoutePartition || (!HAS_V && gate->noneq_total == 0))) return;
   constexpr int NW = SM::NW;
   constexpr int ST = SM::ST;
+  constexpr int BITS = COMPACT ? bits_for(NBMAX) : kBinBits;  // ids 0 .. NBMAX (invalid)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int c = blockIdx.x;
   const int s = chunk_seg[c];
+  const GuideTab<K>& gd = guides[s];
+  const int md = gd.md;
+  if (COMPACT != (2 * md + 2 <= kCompactBins)) return;  // the other instance's segment
   const SegDesc seg = segs[s];
   const int g = c - seg.chunk_base;
-  const int nb = seg.nbins;
-  const int m = m_all[s];
-  const int depth = tree_depth(m);
-  load_splitters_smem(spl_all + (int64_t)s * kMaxBuckets, eq_all + (int64_t)s * kMaxBuckets, m, sm.spl, sm.eq);
-  for (int b = tid; b < nb; b += NT)
-    sm.cur[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * seg.nchunks + g] - seg.len_prefix));
+  const int m = gd.m;
+  const int nb = COMPACT ? 2 * md + 2 : seg.nbins;
+  if (COMPACT) {
+    // occurring splitter indices are first occurrences (and m); any other index
+    // would need t_{i-1} < x <= t_i with t_{i-1} = t_i
+    for (int k = tid; k < md; k += NT) sm.inv[gd.first[k]] = (uint16_t)k;
+    if (tid == 0) sm.inv[m] = (uint16_t)md;
+  }
+  for (int b = tid; b < nb; b += NT) {
+    const int ob = COMPACT ? 2 * ((b >> 1) < md ? (int)gd.first[b >> 1] : m) + (b & 1) : b;
+    sm.cur[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)ob * seg.nchunks + g] - seg.len_prefix));
+  }
   __syncthreads();
   const int64_t c0 = seg.start + (int64_t)g * chunk_size;
   const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
@@ -645,33 +667,35 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     __syncwarp();
     K x[VTS];
     uint32_t v[VTS];
-    int bin[VTS];
-    int rk[VTS];
+    uint16_t bi[VTS];
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
-      int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
+      const int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
       x[i] = pos < c1 ? src_k[pos] : K(0);
       if (HAS_V) v[i] = pos < c1 ? src_v[pos] : 0u;
+      bi[i] = pos < c1 ? bins_in[pos] : (uint16_t)0;
     }
+    uint16_t rk[VTS];
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
-      int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
-      bool valid = pos < c1;
-      int b = !valid ? kMaxBins : (bins_in ? (int)bins_in[pos] : classify_key<K>(x[i], sm.spl, sm.eq, m, depth));
+      const int64_t pos = sub + (int64_t)w * 32 * VTS + i * 32 + lane;
+      const bool valid = pos < c1;
+      const int b0 = (int)bi[i];
+      const int b = !valid ? NBMAX : (COMPACT ? 2 * (int)sm.inv[b0 >> 1] + (b0 & 1) : b0);
       // lanes with the same bucket: one ballot per bit of the id (cheaper than
       // MATCH.ANY, which dominated this kernel's stalls)
       unsigned peers = 0xffffffffu;
 #pragma unroll
-      for (int bit = 0; bit < kBinBits; bit++) {
+      for (int bit = 0; bit < BITS; bit++) {
         const unsigned bal = __ballot_sync(0xffffffffu, (b >> bit) & 1);
         peers &= ((b >> bit) & 1) ? bal : ~bal;
       }
-      int base = sm.wcnt[w][b];
-      rk[i] = base + __popc(peers & lt);
+      const int base = sm.wcnt[w][b];
+      rk[i] = (uint16_t)(base + __popc(peers & lt));
       __syncwarp();
       if (lane == __ffs(peers) - 1) sm.wcnt[w][b] = (uint16_t)(base + __popc(peers));
       __syncwarp();
-      bin[i] = b;
+      bi[i] = (uint16_t)b;
     }
     __syncthreads();
     for (int b = tid; b < nb; b += NT) {
@@ -689,9 +713,9 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     smem_scan<NT>(sm.lstart, nb, 0u, [](uint32_t a, uint32_t b) { return a + b; }, true, false, sm.red);
 #pragma unroll
     for (int i = 0; i < VTS; i++) {
-      int b = bin[i];
-      if (b < kMaxBins) {
-        int lp = sm.lstart[b] + sm.wcnt[w][b] + rk[i];
+      const int b = bi[i];
+      if (b < NBMAX) {
+        const int lp = sm.lstart[b] + sm.wcnt[w][b] + rk[i];
         sm.stk[lp] = x[i];
         sm.stb[lp] = (uint16_t)b;
         if (HAS_V) sm.stv[lp] = v[i];
@@ -700,8 +724,8 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
     __syncthreads();
     const int cnt = (int)((c1 - sub) < ST ? (c1 - sub) : ST);
     for (int p = tid; p < cnt; p += NT) {
-      int b = sm.stb[p];
-      int64_t d = (int64_t)sm.cur[b] + (p - (int)sm.lstart[b]);
+      const int b = sm.stb[p];
+      const int64_t d = (int64_t)sm.cur[b] + (p - (int)sm.lstart[b]);
       if (!(b & 1)) dst_k[d] = sm.stk[p];
       if (HAS_V) dst_v[d] = sm.stv[p];
     }

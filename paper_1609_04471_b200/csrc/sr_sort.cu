@@ -804,14 +804,23 @@ struct Sorter {
                                                                  L.atomic ? nullptr : L.d_mat, gate);
       });
     }
-    using SM = ScatterSmem<K, HAS_V, kScatNT, scat_vt<K>()>;
-    size_t smem = sizeof(SM);
-    auto kern = k_scatter<K, HAS_V, kScatNT, scat_vt<K>()>;
+    // two instances, each serving the segments of its bucket-table size class
+    // (the compact one: few distinct splitters, guide.cuh md <= 255)
+    using SM = ScatterSmem<K, HAS_V, kScatNT, scat_vt<K>(), kMaxBins>;
+    using SMC = ScatterSmem<K, HAS_V, kScatNT, scat_vt<K>() / 4, kCompactBins>;
+    const size_t smem = sizeof(SM), smemc = sizeof(SMC);
+    auto kern = k_scatter<K, HAS_V, kScatNT, scat_vt<K>(), kMaxBins>;
+    auto kernc = k_scatter<K, HAS_V, kScatNT, scat_vt<K>() / 4, kCompactBins>;
     set_smem(kern, smem);
-    int64_t bytes = keys_in * (kw + vw) + noneq * kw + keys_in * vw + L.mat_entries * 4;
+    set_smem(kernc, smemc);
+    int64_t bytes = keys_in * (kw + vw) + noneq * kw + keys_in * vw + L.mat_entries * 4 + keys_in * 2;
+    c.launch("scatter", 0, [&] {  // (same name: the profile sums both instances' time)
+      kernc<<<(unsigned)L.total_chunks, kScatNT, smemc, c.st>>>(sk, sv, dk, dv, L.d_segs, L.d_chunk_seg, L.chunk_size,
+                                                                L.d_guide, L.d_mat, L.d_bins, gate);
+    });
     return c.launch("scatter", bytes, [&] {
       kern<<<(unsigned)L.total_chunks, kScatNT, smem, c.st>>>(sk, sv, dk, dv, L.d_segs, L.d_chunk_seg, L.chunk_size,
-                                                              L.d_spl, L.d_eq, L.d_m, L.d_mat, L.d_bins, gate);
+                                                              L.d_guide, L.d_mat, L.d_bins, gate);
     });
   }
 
