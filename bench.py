@@ -62,6 +62,10 @@ WORKLOADS = {
     # double" and "random 16-list" classes at the Table 1 size
     "c2d": (2_000_000, np.float64, ["funiform", "fbits"], 1),
     "c2l16": (2_000_000, ("rec", 16), ["lrandom", "lprefix"], 1),
+    # report-only: the paper's Table 1 "nearly sorted" class is 256-distance
+    # (PAPER.md:36, :84); configs[1](c) uses k-exchange instead
+    "c2k": (2_000_000, np.int32, ["distance256"], 1),
+    "c3k": (16_777_216, np.int32, ["distance256"], 2),
 }
 
 
@@ -110,6 +114,8 @@ def make_input_dev(sr, order, n, dtype, config, instance, dev):
         sr.generate(t, "random", gen.seed_for(config, gen.ORDERS["random"], instance))
     elif order == "nearly1000":
         sr.generate(t, "swaps", gen.seed_for(config, 2, instance), n // 1000)
+    elif order == "distance256":
+        sr.generate(t, "distance", gen.seed_for(config, gen.ORDERS[order], instance), 256)
     else:
         return None
     return t

@@ -66,8 +66,11 @@ enum {
   SR_ROUTE_MERGE = 3,     /* natural runs + merge levels (§3, Appendix A) */
   SR_ROUTE_PARTITION = 4, /* splitter partition with equality buckets (§4, Appendix B) */
   SR_ROUTE_TILE = 5,      /* n <= one CTA tile: tile sort only (PAPER.md:155 alpha cutoff) */
-  SR_ROUTE_OUTLIER = 6    /* keys only, few descents (k-exchange): descent endpoints extracted,
+  SR_ROUTE_OUTLIER = 6,   /* keys only, few descents (k-exchange): descent endpoints extracted,
                              sorted, merged with the sorted remainder */
+  SR_ROUTE_DISTANCE = 7   /* keys only, bounded displacement (k-distance): proven by the
+                             presortedness scan (every key < 512 positions from its place); sorted
+                             windows of 1024 keys, then merged windows offset by 512 */
 };
 
 /* ------------------------------------------------------------------ inputs */
@@ -187,6 +190,7 @@ enum {
                               maximum: 16384 keys for int32, 8192 for int64); larger buckets are left for
                               host-driven partition levels (tests lower it) */
   SR_OPT_OUTLIER_ROUTE = 5, /* 0: never choose the outlier route automatically */
+  SR_OPT_DISTANCE_ROUTE = 7, /* 0: never choose the k-distance route automatically */
   SR_OPT_WS_LIMIT = 6,    /* fault injection: device workspace bytes one call may take (0 = no limit); a
                              larger reservation fails with SR_ERR_OUT_OF_MEMORY as a real one would */
   SR_OPT_TUNE = 16        /* SR_OPT_TUNE + i, i < 8: tuning knobs of the large keys-only path (A/B runs):

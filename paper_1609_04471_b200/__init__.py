@@ -17,10 +17,11 @@ from . import build as _build
 SR_INT32, SR_INT64, SR_FLOAT32, SR_FLOAT64 = 0, 1, 2, 3  # include/sr_sort.h
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "size out of range", 4: "misaligned pointer",
           5: "out of device memory", 6: "CUDA error", 7: "internal error"}
-ROUTES = {0: "none", 1: "sorted", 2: "reversed", 3: "merge", 4: "partition", 5: "tile", 6: "outlier"}
+ROUTES = {0: "none", 1: "sorted", 2: "reversed", 3: "merge", 4: "partition", 5: "tile", 6: "outlier", 7: "distance"}
 ROUTE_MERGE, ROUTE_PARTITION, ROUTE_OUTLIER = 3, 4, 6
 OPT_FORCE_ROUTE, OPT_PROFILE, OPT_MERGE_ROUTE, OPT_RESIDENT, OPT_RESIDENT_CAP, OPT_OUTLIER_ROUTE, OPT_WS_LIMIT = (
     0, 1, 2, 3, 4, 5, 6)
+OPT_DISTANCE_ROUTE = 7
 OPT_TUNE = 16  # + 0 fused second level, + 1 level-1 buckets (n >= 2^26), + 2 fused mean sub-bucket
 
 EXPORTS = [

@@ -17,10 +17,14 @@ constexpr int kWarp = 32;
 template <typename K> struct KeyTraits;
 template <> struct KeyTraits<int32_t> {
   static __host__ __device__ __forceinline__ int32_t max_key() { return INT32_MAX; }
+  static __host__ __device__ __forceinline__ int32_t min_key() { return INT32_MIN; }
+  using AtomicT = int;
   static constexpr int kPadEvery = 32;   // one pad element per 128 B of smem
 };
 template <> struct KeyTraits<int64_t> {
   static __host__ __device__ __forceinline__ int64_t max_key() { return INT64_MAX; }
+  static __host__ __device__ __forceinline__ int64_t min_key() { return INT64_MIN; }
+  using AtomicT = long long;
   static constexpr int kPadEvery = 16;
 };
 

@@ -29,13 +29,13 @@ void presort_scan_t(Ctx& c, const K* keys, int64_t n, int strict, int tile, sr_p
   c.launch("presort_scan", n * sizeof(K), [&] {
     if (strict)
       k_presort_scan<K, true, false, 256><<<(unsigned)G, 256, 0, c.st>>>(keys, n, tile, d_sums, nullptr, nullptr,
-                                                                         nullptr, nullptr, 0, (int)G, nullptr, nullptr);
+                                                                         nullptr, nullptr, 0, (int)G, nullptr, nullptr, nullptr);
     else
       k_presort_scan<K, false, false, 256><<<(unsigned)G, 256, 0, c.st>>>(keys, n, tile, d_sums, nullptr, nullptr,
-                                                                          nullptr, nullptr, 0, (int)G, nullptr, nullptr);
+                                                                          nullptr, nullptr, 0, (int)G, nullptr, nullptr, nullptr);
   });
   c.launch("presort_resolve", G * 32, [&] {
-    k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(keys, n, d_sums, (int)G, tile, d_asc, d_desc, d_st, 0, 1);
+    k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(keys, n, d_sums, (int)G, tile, d_asc, d_desc, d_st, 0, 1, nullptr);
   });
   DevStats hs = *reinterpret_cast<DevStats*>(c.readback(d_st, sizeof(DevStats)));
   hs_out->n = hs.n;

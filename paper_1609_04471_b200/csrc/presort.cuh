@@ -235,10 +235,16 @@ struct ScanAcc {
 // flags become bit masks; counts are popcounts and first / last positions
 // come from ffs / clz once per vector.  Requires keys 16-byte aligned and
 // t0 a multiple of V; keys beyond n are never read.
+// With smn / smx (shared, one entry per kDSub-key subtile of [t0, t1), set to
+// +inf / -inf by the caller; t0 a multiple of kDSub) the pass also records
+// every subtile's min and max for the k-distance test (tile_mm_finish): a
+// warp's 32 vectors of a round lie in one subtile, so one warp reduction and
+// one shared atomic per round and warp.
 template <typename K, bool STRICT, int NT, int R>
 __device__ __forceinline__ void scan_range_vec(const K* __restrict__ keys, int64_t n, int64_t t0, int64_t t1,
-                                               ScanAcc& acc) {
+                                               ScanAcc& acc, K* smn = nullptr, K* smx = nullptr) {
   constexpr int V = 16 / (int)sizeof(K);
+  static_assert(kDSub % (32 * V) == 0, "a warp's round lies in one subtile");
   const int tid = threadIdx.x & (NT - 1), lane = threadIdx.x & 31;
   for (int64_t vb = t0 / V; vb * V < t1; vb += (int64_t)NT * R) {
     K x[R][V], hp[R], hn0[R], hn1[R];
@@ -284,6 +290,19 @@ __device__ __forceinline__ void scan_range_vec(const K* __restrict__ keys, int64
       dm &= valid;
       am &= valid;
       sm &= dm;
+      if (smn) {  // subtile min / max over the keys of [t0, t1)
+        K mn = KeyTraits<K>::max_key(), mx = KeyTraits<K>::min_key();
+#pragma unroll
+        for (int j = 0; j < V; j++)
+          if (i0 + j < t1 && i0 + j < n) { mn = min(mn, x[r][j]); mx = max(mx, x[r][j]); }
+        mn = warp_reduce_min(mn);
+        mx = warp_reduce_max(mx);
+        if (lane == 0 && i0 < t1) {
+          const int q = (int)((i0 - t0) / kDSub);
+          atomicMin(reinterpret_cast<typename KeyTraits<K>::AtomicT*>(smn + q), (typename KeyTraits<K>::AtomicT)mn);
+          atomicMax(reinterpret_cast<typename KeyTraits<K>::AtomicT*>(smx + q), (typename KeyTraits<K>::AtomicT)mx);
+        }
+      }
       acc.cd += __popc(dm);
       acc.ca += __popc(am);
       acc.cv += __popc(sm);
@@ -299,6 +318,37 @@ __device__ __forceinline__ void scan_range_vec(const K* __restrict__ keys, int64
   }
 }
 
+// k-distance test of one tile (all threads of the block; smn / smx filled by
+// scan_range_vec): ok = max(subtile q) <= min(subtile q + 2) for every q with
+// both subtiles inside [t0, t1) -- with such pairs on every tile boundary too
+// (checked by the resolve), every key lies less than 2 kDSub positions from its
+// place in the sorted output (PAPER.md:84 k-distance, k < 2 kDSub): the keys of
+// subtiles <= q-2 are <= x and those of subtiles >= q+2 are >= x for every x in
+// subtile q.  valid = 0 (no subtile statistics) makes the tile fail.
+template <typename K>
+__device__ __forceinline__ void tile_mm_init(K* smn, K* smx, int nsub) {
+  for (int q = threadIdx.x; q < nsub; q += blockDim.x) {
+    smn[q] = KeyTraits<K>::max_key();
+    smx[q] = KeyTraits<K>::min_key();
+  }
+}
+template <typename K>
+__device__ __forceinline__ void tile_mm_finish(const K* smn, const K* smx, int nsub, int valid, TileMM* out) {
+  int bad = !valid;
+  for (int q = threadIdx.x; q + 2 < nsub; q += blockDim.x) bad |= smx[q] > smn[q + 2];
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    TileMM t;
+    t.mn0 = (int64_t)smn[0];
+    t.mn1 = nsub > 1 ? (int64_t)smn[1] : INT64_MAX;
+    t.mx0 = nsub > 1 ? (int64_t)smx[nsub - 2] : INT64_MIN;
+    t.mx1 = (int64_t)smx[nsub - 1];
+    t.ok = !bad;
+    t.nsub = nsub;
+    *out = t;
+  }
+}
+
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
 // break rule: a_i <= a_{i+1} (pairs: only strictly descending runs may be
 // reversed, "the reversely sorted subsequence cannot contain equal
@@ -310,8 +360,10 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
                                                       TileSummary* __restrict__ sums, const K* __restrict__ spl,
                                                       const uint8_t* __restrict__ eqf, const int* __restrict__ mcount,
                                                       uint32_t* __restrict__ mat, int nbins, int G,
-                                                      uint32_t* __restrict__ tot, uint16_t* __restrict__ bins_out) {
+                                                      uint32_t* __restrict__ tot, uint16_t* __restrict__ bins_out,
+                                                      TileMM* __restrict__ mm) {
   constexpr int U = 8;
+  __shared__ K s_mn[65536 / kDSub], s_mx[65536 / kDSub];  // tile <= 65536 keys
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ClassifySmem<K>& csm = *reinterpret_cast<ClassifySmem<K>*>(smem_raw);  // FUSE only (dynamic)
   K* s_spl = csm.tree;
@@ -331,9 +383,16 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   }
   int cd = 0, ca = 0, cv = 0;
   int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
-  if (!FUSE && (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0) {
+  const int nsub = (int)((t1 - t0 + kDSub - 1) / kDSub);
+  const bool vec = !FUSE && (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0;
+  if (mm) {
+    tile_mm_init<K>(s_mn, s_mx, nsub);
+    __syncthreads();
+  }
+  if (vec) {
     ScanAcc acc;
-    scan_range_vec<K, STRICT, NT, (sizeof(K) == 4 ? 2 : 4)>(keys, n, t0, t1, acc);
+    scan_range_vec<K, STRICT, NT, (sizeof(K) == 4 ? 2 : 4)>(keys, n, t0, t1, acc, mm ? s_mn : nullptr,
+                                                            mm ? s_mx : nullptr);
     cd = acc.cd; ca = acc.ca; cv = acc.cv; fd = acc.fd; ld = acc.ld; fa = acc.fa; la = acc.la;
   } else
   for (int64_t base = t0; base < t1; base += NT * U) {
@@ -369,6 +428,10 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
       }
     }
   }
+  if (mm) {
+    __syncthreads();
+    tile_mm_finish<K>(s_mn, s_mx, nsub, vec ? 1 : 0, mm + blockIdx.x);
+  }
   cd = block_reduce_sum<NT>(cd, s_red);
   ca = block_reduce_sum<NT>(ca, s_red);
   fd = block_reduce_min<NT>(fd, s_red);
@@ -395,7 +458,7 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
 // Device-side route (H3 first stage) from the resolved statistics;
 // kRouteUndecided hands the merge-vs-partition cost comparison to the host planner.
 __device__ __forceinline__ int64_t resolve_route(int64_t n, int64_t D, int64_t A, int64_t V, int64_t covA, int64_t covD,
-                                                 int force, int merge_ok) {
+                                                 int force, int merge_ok, int dist_ok = 0) {
   if (D == 0) return kRouteSorted;
   if (A == 0 && force == 0) return kRouteReversed;
   if (force == kRouteMerge) return kRouteMerge;
@@ -406,8 +469,23 @@ __device__ __forceinline__ int64_t resolve_route(int64_t n, int64_t D, int64_t A
   if ((merge_ok & kAllowOutlier) && A > 0 && kViolRatio * V <= D &&
       ((merge_ok & kOutlierStrict) ? kOutlierRatioStrict : kOutlierRatio) * D <= n)
     return kRouteOutlier;
+  // bounded displacement (k-distance): two passes of window sorts
+  if (dist_ok && (merge_ok & kAllowDistance)) return kRouteDistance;
   if ((merge_ok & kAllowMerge) && 2 * (covA + covD) >= n) return kRouteUndecided;
   return kRoutePartition;
+}
+
+// The k-distance test over all tiles: every tile passed its own test and the
+// subtile pairs that straddle a tile boundary (the last two subtiles of tile
+// t against the first two of tile t+1) are ordered too.  mm == nullptr: no.
+__device__ __forceinline__ int tile_mm_pair_ok(const TileMM* __restrict__ mm, int t, int G) {
+  const int64_t* q = reinterpret_cast<const int64_t*>(mm + t);
+  if (!__ldcg(reinterpret_cast<const int*>(q + 4))) return 0;  // ok
+  if (t + 1 >= G) return 1;
+  const int64_t mx0 = __ldcg(q + 2), mx1 = __ldcg(q + 3);
+  const int64_t* r = reinterpret_cast<const int64_t*>(mm + t + 1);
+  const int64_t mn0 = __ldcg(r + 0), mn1 = __ldcg(r + 1);
+  return mx0 <= mn0 && mx1 <= mn1;
 }
 
 // K2: resolve tile summaries into D, the long runs of both directions and
@@ -422,7 +500,8 @@ template <typename K, int NT, bool WRITE = true>
 __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ keys, int64_t n,
                                                       const TileSummary* __restrict__ sums, int G, int64_t lmin,
                                                       RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
-                                                      DevStats* __restrict__ st, int force, int merge_ok) {
+                                                      DevStats* __restrict__ st, int force, int merge_ok,
+                                                      const TileMM* __restrict__ mm = nullptr) {
   __shared__ int32_t s_incl[2][NT];
   __shared__ int64_t s_red64[NT / 32 + 1];
   __shared__ int32_t s_red[NT / 32 + 1];
@@ -483,6 +562,10 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
   V = block_reduce_sum<NT>(V, s_red64);
   covA = block_reduce_sum<NT>(covA, s_red64);
   covD = block_reduce_sum<NT>(covD, s_red64);
+  int dok = mm != nullptr;
+  if (mm)
+    for (int t = tid; t < G; t += NT) dok &= tile_mm_pair_ok(mm, t, G);
+  dok = __syncthreads_and(dok);
   if (tid == 0) {
     // final runs after the last break
     int64_t lastLen = n - 1 - (int64_t)carryD;
@@ -507,8 +590,9 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
       ndsc++;
       covD += lastLenD;
     }
-    const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok);
+    const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok, dok);
     if (WRITE) {
+      st->dist_ok = dok;
       st->n = n;
       st->descents = D;
       st->asc_breaks = A;
@@ -535,7 +619,8 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
 template <typename K, bool WRITE>
 __device__ int64_t presort_resolve_warp(const K* __restrict__ keys, int64_t n, const TileSummary* ts, int G,
                                         int64_t lmin, RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
-                                        DevStats* __restrict__ st, int force, int merge_ok) {
+                                        DevStats* __restrict__ st, int force, int merge_ok,
+                                        const TileMM* __restrict__ mm = nullptr) {
   const int lane = threadIdx.x & 31;
   const int TPL = (G + 31) / 32;
   const int t0 = lane * TPL < G ? lane * TPL : G, t1 = t0 + TPL < G ? t0 + TPL : G;
@@ -631,8 +716,13 @@ __device__ int64_t presort_resolve_warp(const K* __restrict__ keys, int64_t n, c
     ndsc++;
     covD += lastLenD;
   }
-  const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok);
+  int dok = mm != nullptr;
+  if (mm)
+    for (int t = t0; t < t1; t++) dok &= tile_mm_pair_ok(mm, t, G);
+  dok = __all_sync(0xffffffffu, dok);
+  const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok, dok);
   if (WRITE && lane == 0) {
+    st->dist_ok = dok;
     st->n = n;
     st->descents = D;
     st->asc_breaks = A;
@@ -649,8 +739,9 @@ template <typename K, int NT>
 __global__ void __launch_bounds__(NT) k_presort_resolve(const K* __restrict__ keys, int64_t n,
                                                          const TileSummary* __restrict__ sums, int G, int64_t lmin,
                                                          RunDesc* __restrict__ asc, RunDesc* __restrict__ desc,
-                                                         DevStats* __restrict__ st, int force, int merge_ok) {
-  presort_resolve_block<K, NT>(keys, n, sums, G, lmin, asc, desc, st, force, merge_ok);
+                                                         DevStats* __restrict__ st, int force, int merge_ok,
+                                                         const TileMM* __restrict__ mm) {
+  presort_resolve_block<K, NT>(keys, n, sums, G, lmin, asc, desc, st, force, merge_ok, mm);
 }
 
 // K3: in-place reversal of ranges [start, start+len) (H2; PAPER.md:93 and

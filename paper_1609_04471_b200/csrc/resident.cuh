@@ -96,6 +96,7 @@ struct ResArgs {
   int64_t n;
   int tile, G;              // presort tiles (K1's tiling)
   TileSummary* sums;
+  TileMM* mm;               // per tile: the k-distance test (presort.cuh tile_mm_finish)
   RunDesc* asc;
   RunDesc* desc;
   DevStats* st;             // route, statistics; n_ovf counts the host list
@@ -295,9 +296,17 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
     int cd = 0, ca = 0, cv = 0;
     int fd = INT32_MAX, ld = -1, fa = INT32_MAX, la = -1;
-    if ((reinterpret_cast<uintptr_t>(a.keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0) {
+    // subtile minima / maxima for the k-distance test (scratch: the route
+    // step's sample area, unused by the scanning CTAs until then)
+    K* mmn = sm.u.sp.q;
+    K* mmx = sm.u.sp.q + kResGrp / kDSub;
+    const int nsub = (int)((t1 - t0 + kDSub - 1) / kDSub);
+    const bool vec = (reinterpret_cast<uintptr_t>(a.keys) & 15) == 0 && t0 % (16 / (int)sizeof(K)) == 0;
+    tile_mm_init<K>(mmn, mmx, nsub);
+    __syncthreads();
+    if (vec) {
       ScanAcc acc;
-      scan_range_vec<K, false, NT, (sizeof(K) == 4 ? 4 : 8)>(a.keys, n, t0, t1, acc);
+      scan_range_vec<K, false, NT, (sizeof(K) == 4 ? 4 : 8)>(a.keys, n, t0, t1, acc, mmn, mmx);
       cd = acc.cd; ca = acc.ca; cv = acc.cv; fd = acc.fd; ld = acc.ld; fa = acc.fa; la = acc.la;
     } else
     for (int64_t base = t0; base < t1; base += NT * UA) {
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       ts.ndesc = cd; ts.nab = ca; ts.fdesc = fd; ts.ldesc = ld; ts.fab = fa; ts.lab = la; ts.nviol = cv; ts.pad1 = 0;
       a.sums[t] = ts;
     }
+    tile_mm_finish<K>(mmn, mmx, nsub, vec ? 1 : 0, a.mm + t);  // (its barrier orders the next tile's init)
     __syncthreads();
   }
   SR_RES_STAMP(0);
@@ -394,9 +404,9 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
     if (tid == 0) s_route = __ldcg(reinterpret_cast<const long long*>(&a.st->route));
   } else if (w == 0) {  // H1 resolve by one warp (CTA 0 also writes the statistics and run lists)
     const int64_t r = c == 0 ? presort_resolve_warp<K, true>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
-                                                             a.force, a.merge_ok)
+                                                             a.force, a.merge_ok, a.mm)
                              : presort_resolve_warp<K, false>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
-                                                              a.force, a.merge_ok);
+                                                              a.force, a.merge_ok, a.mm);
     if (lane == 0) {
       s_route = r;
       if (c == 0) {  // the route is in a.st: tell the samplers

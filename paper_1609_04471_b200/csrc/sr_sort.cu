@@ -24,6 +24,7 @@
 
 #include "../../include/sr_sort.h"
 #include "bucket_sort.cuh"
+#include "distance.cuh"
 #include "fkeys.cuh"
 #include "generate.cuh"
 #include "measures.cuh"
@@ -44,6 +45,7 @@ int g_profile = 0;
 int g_merge_route = 1;
 int g_resident = 1;
 int g_outlier = 1;
+int g_distance = 1;
 int g_res_cap = 16384;
 int64_t g_ws_limit = 0;  // SR_OPT_WS_LIMIT (fault injection), 0 = none
 // SR_OPT_TUNE + i: tuning knobs of the large keys-only path (A/B measurements)
@@ -520,7 +522,27 @@ struct Sorter {
 
   // routes the device resolve may choose, and the forced route (outlier: keys only)
   int route_ok() const {
-    return (g_merge_route ? kAllowMerge : 0) | ((!HAS_V && g_outlier && !nested) ? kAllowOutlier : 0);
+    return (g_merge_route ? kAllowMerge : 0) | ((!HAS_V && g_outlier && !nested) ? kAllowOutlier : 0) |
+           ((!HAS_V && g_distance) ? kAllowDistance : 0);
+  }
+
+  // k-distance route (distance.cuh): window sorts, then window merges
+  void run_distance(const DevStats* gate = nullptr) {
+    if (!gate) c.plan.route = SR_ROUTE_DISTANCE;
+    constexpr int PIECE = UnitNet<K>::PIECE;
+    const size_t smem = sizeof(K) * PIECE * kDistWarps;
+    set_smem(k_window_sort<K>, smem);
+    set_smem(k_window_merge<K>, smem);
+    const int64_t nwin = ceil_div<int64_t>(n, 2 * kDT);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(nwin, kDistWarps), 148 * 16));
+    K* kk = keys;
+    const int64_t nn = n;
+    c.launch("window_sort", gate ? 0 : 2 * n * kw, [&] {
+      k_window_sort<K><<<grid, 32 * kDistWarps, smem, c.st>>>(kk, nn, gate);
+    });
+    c.launch("window_merge", gate ? 0 : 2 * n * kw, [&] {
+      k_window_merge<K><<<grid, 32 * kDistWarps, smem, c.st>>>(kk, nn, gate);
+    });
   }
   int forced() const {
     if (g_force_route == SR_ROUTE_OUTLIER && (HAS_V || nested)) return 0;
@@ -1280,7 +1302,7 @@ struct Sorter {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
       const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 32 + 4 * nbins) +
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
-                                    r(4 * ResCfg<K>::B1MAX) +
+                                    r(4 * ResCfg<K>::B1MAX) + r(G * (int64_t)sizeof(TileMM)) +
                                     r(4 * (int64_t)NG * nbins) + 8 * 256);
       DevState& dsa = t_state.ds();
       if (dsa.has_last && dsa.last_stream != c.st)  // the arena of the last call is in use until its kernel ends
@@ -1308,6 +1330,7 @@ struct Sorter {
     a.tile = (int)tile;
     a.G = (int)G;
     a.sums = c.alloc<TileSummary>(G);
+    a.mm = c.alloc<TileMM>(G);
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
     {  // control block: statistics | unit counters | bucket totals, zeroed by the kernel
@@ -1436,6 +1459,9 @@ struct Sorter {
         c.plan.route = SR_ROUTE_REVERSED;
         c.plan.desc_runs_reversed = 1;
         c.replan(h, 3 * n * kw);
+        return;
+      case kRouteDistance:
+        run_distance();
         return;
       case kRoutePartition: {
         c.plan.route = SR_ROUTE_PARTITION;
@@ -1630,7 +1656,7 @@ struct Sorter {
                   r(kMaxBuckets * kw) + r(kMaxBuckets) + r(4) + (HAS_V ? r(bins * G * 4) : 0) +
                   r(sizeof(DevStats) + 256 + 8 * ceil_div<int64_t>(bins * G, kScanNT * kScanIPT) + 4 * bins) +
                   r(4 * bins) + r(24 * (bins + n / kFillChunk + 2)) + r(24 * bins) + r(16 * bins) + r(2 * n) +
-                  r(kMaxSample * (kw + 4)) + 8 * 256;
+                  r(kMaxSample * (kw + 4)) + r(G * (int64_t)sizeof(TileMM)) + 8 * 256;
       c.reserve((size_t)b);
     }
     // Large n: the level-1 histogram rides on the presortedness read (one HBM
@@ -1645,6 +1671,7 @@ struct Sorter {
       if (fused) level_splitters(L1);
     }
     TileSummary* d_sums = c.alloc<TileSummary>(G);
+    TileMM* d_mm = HAS_V ? nullptr : c.alloc<TileMM>(G);
     RunDesc* d_asc = c.alloc<RunDesc>(G + 1);
     RunDesc* d_desc = c.alloc<RunDesc>(G + 1);
     DevStats* d_pst = part ? L1.d_st : c.alloc<DevStats>(1);
@@ -1660,22 +1687,23 @@ struct Sorter {
       if (fused) {
         if (HAS_V)
           k_presort_scan<K, true, true, kScanNT1><<<(unsigned)G, kScanNT1, csmem, c.st>>>(
-              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins);
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins, nullptr);
         else
           k_presort_scan<K, false, true, kScanNT1><<<(unsigned)G, kScanNT1, csmem, c.st>>>(
-              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins);
+              kk, n, (int)T, d_sums, L1.d_spl, L1.d_eq, L1.d_m, L1.d_mat, nbins1, (int)G, L1.d_tot, L1.d_bins, d_mm);
       } else {
         if (HAS_V)
           k_presort_scan<K, true, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr);
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr, nullptr);
         else
           k_presort_scan<K, false, false, kScanNT1><<<(unsigned)G, kScanNT1, 0, c.st>>>(
-              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr);
+              kk, n, (int)T, d_sums, nullptr, nullptr, nullptr, nullptr, 0, (int)G, nullptr, nullptr, d_mm);
       }
     });
     const int merge_ok = route_ok();
     c.launch("presort_resolve", G * (int64_t)sizeof(TileSummary), [&] {
-      k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst, force, merge_ok);
+      k_presort_resolve<K, 1024><<<1, 1024, 0, c.st>>>(kk, n, d_sums, (int)G, T, d_asc, d_desc, d_pst, force, merge_ok,
+                                                       d_mm);
     });
     // speculative route kernels
     int h_rev = -1, h_tile = -1, h_scat = -1, h_fin = -1, h_count = -1;
@@ -1728,6 +1756,9 @@ struct Sorter {
         return;
       case kRouteTile:
         c.plan.route = SR_ROUTE_TILE;
+        return;
+      case kRouteDistance:
+        run_distance();
         return;
       default:
         break;
@@ -2177,6 +2208,9 @@ int32_t sr_set_option(int32_t key, int64_t value) {
       return SR_OK;
     case SR_OPT_OUTLIER_ROUTE:
       g_outlier = value ? 1 : 0;
+      return SR_OK;
+    case SR_OPT_DISTANCE_ROUTE:
+      g_distance = value ? 1 : 0;
       return SR_OK;
     case SR_OPT_WS_LIMIT:
       if (value < 0) return SR_ERR_INVALID_ARGUMENT;

@@ -15,6 +15,17 @@ struct TileSummary {
   int32_t pad1;
 };
 
+// Bounded-displacement summary of one presort tile (the k-distance route,
+// PAPER.md:84): the tile is cut into subtiles of kDSub keys; ok = 1 when
+// max(subtile q) <= min(subtile q+2) for every q with both inside the tile;
+// mn0/mn1 are the mins of its first two subtiles, mx0/mx1 the maxes of its
+// last two (keys as int64; +inf / -inf where the tile has one subtile).
+constexpr int kDSub = 256;
+struct TileMM {
+  int64_t mn0, mn1, mx0, mx1;
+  int32_t ok, nsub;
+};
+
 // A long natural run [start, start+len) and its end keys as stored in the
 // input (before any reversal).  dir: 0 ascending, 1 descending.
 struct RunDesc {
@@ -39,6 +50,7 @@ struct DevStats {
   int64_t error;        // device-detected inconsistency (must stay 0)
   int64_t route;        // device-side route decision (kRoute*)
   int64_t big_keys;     // keys in large finishing items
+  int64_t dist_ok;      // bounded displacement < 2 kDSub (k-distance route possible)
 };
 
 // One segment of a partition level (H7-H10).
@@ -69,9 +81,9 @@ struct OvfSeg {
 
 // route codes (equal to the SR_ROUTE_* values of include/sr_sort.h)
 constexpr int64_t kRouteSorted = 1, kRouteReversed = 2, kRouteMerge = 3, kRoutePartition = 4, kRouteTile = 5,
-                  kRouteOutlier = 6, kRouteUndecided = 8;
+                  kRouteOutlier = 6, kRouteDistance = 7, kRouteUndecided = 8;
 // route_ok bits of the device resolve: merge route allowed, outlier route allowed
-constexpr int kAllowMerge = 1, kAllowOutlier = 2, kOutlierStrict = 4;
+constexpr int kAllowMerge = 1, kAllowOutlier = 2, kOutlierStrict = 4, kAllowDistance = 8;
 constexpr int64_t kOutlierRatioStrict = 512;  // with kOutlierStrict (the one-launch resident range)
 constexpr int64_t kOutlierRatio = 32;  // outlier route when descents <= n / kOutlierRatio ...
 constexpr int64_t kViolRatio = 16;     // ... and at most 1/16 of them have out-of-order neighbours
