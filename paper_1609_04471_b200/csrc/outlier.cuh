@@ -29,9 +29,9 @@ struct OutTile {  // keys per CTA: the tile state (OutSmem) fits the 48 KB stati
 
 // Shared state of one tile: the keys with a one-key halo on each side, the
 // kept keys in order (and where they came from), and per-(u, warp) counts.
-template <typename K, int NT>
+template <typename K, int NT, int TT = OutTile<K>::T>
 struct OutSmem {
-  static constexpr int T = OutTile<K>::T, VT = OutTile<K>::VT, NW = NT / 32;
+  static constexpr int T = TT, VT = TT / NT, NW = NT / 32;
   K s[T + 2];
   K sk[T];
   uint16_t si[T];
@@ -46,11 +46,12 @@ struct OutSmem {
 // between consecutive kept keys, repeated until the kept keys are sorted (at
 // most 4 times).  On return bal[u] holds the kept ballot of element u*NT+tid
 // (striped), gcnt the exclusive kept counts of the (u, warp) groups and
-// gcnt[VT*NW] the tile's kept total.
-template <typename K, int NT>
-__device__ __forceinline__ void out_tile_flags(const K* __restrict__ src, int64_t n, int64_t t0, int len,
-                                               OutSmem<K, NT>& sm, unsigned (&bal)[OutTile<K>::VT]) {
-  constexpr int VT = OutTile<K>::VT, NW = NT / 32;
+// gcnt[VT*NW] the tile's kept total.  Returns true when the kept keys were
+// found sorted (false: the iteration cap was hit first).
+template <typename K, int NT, int TT = OutTile<K>::T>
+__device__ __forceinline__ bool out_tile_flags(const K* __restrict__ src, int64_t n, int64_t t0, int len,
+                                               OutSmem<K, NT, TT>& sm, unsigned (&bal)[TT / NT]) {
+  constexpr int VT = TT / NT, NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   {
     K v[VT];
@@ -103,7 +104,7 @@ __device__ __forceinline__ void out_tile_flags(const K* __restrict__ src, int64_
       if (lane == 0) { sm.gcnt[VT * NW] = carry; sm.flag = 0; }
     }
     __syncthreads();
-    if (iter == 4) break;
+    if (iter == 4) return false;
     const int tot = sm.gcnt[VT * NW];
 #pragma unroll
     for (int u = 0; u < VT; u++) {
@@ -118,7 +119,7 @@ __device__ __forceinline__ void out_tile_flags(const K* __restrict__ src, int64_
     int any = 0;
     for (int j = tid; j + 1 < tot; j += NT)
       if (sm.sk[j] > sm.sk[j + 1]) { sm.rm[sm.si[j]] = 1; sm.rm[sm.si[j + 1]] = 1; any = 1; }
-    if (__syncthreads_or(any) == 0) break;  // the kept keys are sorted
+    if (__syncthreads_or(any) == 0) return true;  // the kept keys are sorted
 #pragma unroll
     for (int u = 0; u < VT; u++) {
       const int i = u * NT + tid;

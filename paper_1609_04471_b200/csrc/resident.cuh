@@ -49,6 +49,7 @@
 #include "bitonic.cuh"
 #include "common.cuh"
 #include "guide.cuh"
+#include "outlier.cuh"
 #include "partition.cuh"
 #include "presort.cuh"
 #include "types.cuh"
@@ -87,6 +88,29 @@ template <> struct ResCfg<int64_t> {
 };
 constexpr int64_t kResMaxN = ResCfg<int32_t>::MAXN;  // largest resident n over the key types
 
+// In-kernel outlier route (nearly sorted inputs, k-exchange PAPER.md:85; the
+// multi-kernel rounds of outlier.cuh in one launch):
+//   OA  tiles of TO keys: the endpoints of every descent are outliers (then,
+//       inside the tile, until the kept keys are sorted); kept keys in order
+//       then the outliers are written to ws[t0, t1)
+//   --  kept keys R (the tiles' kept prefixes, in order) must be sorted across
+//       tiles; splitter j = R[(j+1) OL - 1]; every outlier goes to bucket
+//       #{splitters < x} (at most OCAP per bucket)
+//   OD  bucket j = R[j OL, (j+1) OL) merged with its sorted outliers in one
+//       warp's shared staging area, then copied to keys[j OL + outliers of the
+//       buckets before j, ...) (R wins ties).  A tile boundary out of order or a full bucket leaves the
+//       keys untouched and hands the sort to the host's outlier route.
+template <typename K>
+struct ResOut {
+  static constexpr int TO = sizeof(K) == 4 ? 8192 : 4096;  // OA tile
+  static constexpr int OL = ResCfg<K>::WCAP / 4;           // kept keys per bucket
+  static constexpr int OCAP = ResCfg<K>::WCAP / 4;         // outliers per bucket (one warp network)
+  static_assert(OL + OCAP + OL + OCAP <= ResCfg<K>::WCAP, "R, O and the merged bucket fit one warp's staging");
+  static constexpr int OBMAX = 2 * ResCfg<K>::B1MAX;       // buckets (their starts live in ResSmem::start)
+  static constexpr int MAXG = (int)(ResCfg<K>::MAXN / TO);
+  static constexpr int64_t MAXN = (int64_t)OL * OBMAX;     // n this route accepts
+};
+
 struct ResDone;
 
 template <typename K>
@@ -120,6 +144,12 @@ struct ResArgs {
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
   ResDone* done;            // host-mapped completion record (CTA 0 writes it once the outcome is known)
   uint32_t seq;             // this call's completion sequence number
+  // in-kernel outlier route (ResOut): out_res = 1 when this launch runs it
+  int out_res, GO;          // GO tiles of ResOut::TO keys
+  uint32_t* okc;            // GO: kept keys per tile
+  K* ofl;                   // 2 GO: first / last kept key per tile
+  uint32_t* ocnt;           // OBMAX bucket counts, [OBMAX] unsorted tile, [OBMAX + 1] full bucket (control block)
+  K* obuf;                  // buckets x OCAP: the outliers of each bucket
 };
 
 // Host-mapped completion record: the statistics the planner needs and whether
@@ -181,6 +211,7 @@ struct ResSmem {
   static constexpr int S1MAX = ResCfg<K>::O1 * B1MAX;
   static constexpr int WCAP = ResCfg<K>::WCAP;
   static constexpr int GPC = ResCfg<K>::GPC;
+  static_assert(ResOut<K>::OBMAX <= NB1, "outlier bucket starts live in start[]");
   struct alignas(16) CT {          // C: tile-local counting sorts of this CTA's groups
     uint32_t cnt[NB1];             // current group's bucket counts; in D its piece offsets (goff)
     uint32_t lst[GPC][NB1 + 1];    // per held group: bucket starts inside stk, lst[nbins] = group length
@@ -202,12 +233,15 @@ struct ResSmem {
   union alignas(16) {
     GuideTab<K, 2048, B1MAX> guide1;  // C: level-1 classification table (guide.cuh)
     EU eu;                         // E
+    uint32_t okoff[ResOut<K>::MAXG + 1];  // outlier route: kept-key offsets of the tiles
   } v;
   union alignas(16) {
     K samp1[S1MAX];                // A: the sampler's piece of the sample + BitonicSort scratch
     SP sp;
     CT ct;
     E e;  // (UnitSmem: aligned x / y buffers)
+    OutSmem<K, kResNT, ResOut<K>::TO> ot;  // outlier route OA
+    K ospl[ResOut<K>::OBMAX];      // outlier route: bucket splitters
   } u;
   int32_t red[kResNT / 32 + 1];
   int64_t red64[kResNT / 32 + 1];
@@ -249,6 +283,259 @@ static_assert(sizeof(ResSmem<int32_t>) <= 227 * 1024 && sizeof(ResSmem<int64_t>)
               "one CTA per SM: the shared-memory layout must fit the 227 KB opt-in limit");
 static_assert(offsetof(ResSmem<int32_t>, u) % 16 == 0 && offsetof(ResSmem<int64_t>, u) % 16 == 0,
               "vectorised sort buffers need 16-byte alignment");
+
+// outlier-route sub-steps of CTA 0 (SR_TIMING diagnostics)
+#define SR_RES_OSUB(kk)                                                                             \
+  do {                                                                                              \
+    if (a.tstamp && c == 0 && tid == 0) a.tstamp[8 + 8 * (size_t)gridDim.x + 40 + (kk)] = res_now(); \
+  } while (0)
+
+// Coalesced copy of cnt keys from global (L2) to a warp's shared staging area.
+template <typename K>
+__device__ __forceinline__ void res_warp_copy(K* __restrict__ dst, const K* __restrict__ src, int cnt) {
+  const int lane = threadIdx.x & 31;
+  constexpr int UL = 16;
+  for (int i0 = 0; i0 < cnt; i0 += 32 * UL) {
+    K v[UL];
+#pragma unroll
+    for (int u = 0; u < UL; u++) {
+      const int i = i0 + u * 32 + lane;
+      v[u] = i < cnt ? __ldcg(src + i) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < UL; u++) {
+      const int i = i0 + u * 32 + lane;
+      if (i < cnt) dst[i] = v[u];
+    }
+  }
+}
+
+// ks[0, len) (len <= 64) sorted in place by one warp: each lane ranks its
+// (up to two) keys against all of them (ties by position) and stores them at
+// their ranks.
+template <typename K>
+__device__ __forceinline__ void res_warp_rank_sort(K* ks, int len) {
+  const int lane = threadIdx.x & 31;
+  const K x0 = lane < len ? ks[lane] : K(0);
+  const K x1 = lane + 32 < len ? ks[lane + 32] : K(0);
+  int r0 = 0, r1 = 0;
+  for (int k = 0; k < len; k++) {
+    const K y = ks[k];
+    r0 += (y < x0) || (y == x0 && k < lane);
+    r1 += (y < x1) || (y == x1 && k < lane + 32);
+  }
+  __syncwarp();
+  if (lane < len) ks[r0] = x0;
+  if (lane + 32 < len) ks[r1] = x1;
+  __syncwarp();
+}
+
+// The in-kernel outlier route (ResOut above).  Called by every CTA after the
+// route step chose kRouteOutlier; CTA 0 publishes the outcome.
+template <typename K, typename SM>
+__device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using RO = ResOut<K>;
+  constexpr int NT = kResNT, TO = RO::TO, OL = RO::OL, OCAP = RO::OCAP, OBMAX = RO::OBMAX;
+  constexpr int VT = TO / NT, NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int P = gridDim.x, c = blockIdx.x;
+  const int64_t n = a.n;
+  const int GO = a.GO;
+  auto add = [](uint32_t x, uint32_t y) { return x + y; };
+  // ---- OA: outliers of every tile; ws[t0, t1) = kept keys in order, then the outliers
+  {
+    OutSmem<K, NT, TO>& os = sm.u.ot;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int t = c; t < GO; t += P) {
+      const int64_t t0 = (int64_t)t * TO;
+      const int len = (int)(n - t0 < TO ? n - t0 : TO);
+      unsigned bal[VT];
+      if (t == c) SR_RES_OSUB(0);
+      const bool sorted = out_tile_flags<K, NT, TO>(a.keys, n, t0, len, os, bal);
+      if (t == c) SR_RES_OSUB(1);
+      const int tot = os.gcnt[VT * NW];
+#pragma unroll
+      for (int u = 0; u < VT; u++) {
+        const int i = u * NT + tid;
+        if (i < len) {
+          const int kr = os.gcnt[u * NW + w] + __popc(bal[u] & lt);  // kept before element i
+          if ((bal[u] >> lane) & 1u) os.sk[kr] = os.s[1 + i];
+          else os.sk[tot + (i - kr)] = os.s[1 + i];
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < len; i += NT) a.ws[t0 + i] = os.sk[i];
+      if (tid == 0) {
+        a.okc[t] = (uint32_t)tot;
+        if (tot > 0) {
+          a.ofl[2 * t] = os.sk[0];
+          a.ofl[2 * t + 1] = os.sk[tot - 1];
+        }
+        if (!sorted) atomicOr(a.ocnt + OBMAX, 1u);
+      }
+      __syncthreads();
+      if (t == c) SR_RES_OSUB(2);
+    }
+  }
+  if (a.tstamp && tid == 0) a.tstamp[8 + (size_t)c * 8 + 4] = res_now();
+  grid.sync();
+  // ---- tile offsets of the kept keys R, the cross-tile order check, splitters, outlier buckets
+  uint32_t* koff = sm.v.okoff;
+  for (int t = tid; t < GO; t += NT) koff[t] = __ldcg(a.okc + t);
+  if (tid == 0) koff[GO] = 0u;
+  __syncthreads();
+  smem_scan<NT>(koff, GO + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  SR_RES_OSUB(3);
+  const uint32_t r = koff[GO];
+  const int nbo = (int)((r + OL - 1) / OL);
+  int bad = (r == 0 || nbo > OBMAX) ? 1 : 0;
+  if (tid == 0 && __ldcg(a.ocnt + OBMAX)) bad = 1;
+  for (int t = tid; t < GO && !bad; t += NT) {
+    if (koff[t + 1] == koff[t]) continue;
+    int u = t + 1;
+    while (u < GO && koff[u + 1] == koff[u]) u++;
+    if (u < GO && __ldcg(a.ofl + 2 * t + 1) > __ldcg(a.ofl + 2 * u)) bad = 1;
+  }
+  if (__syncthreads_or(bad)) {  // not a few-outlier input: the host's rounds take over (keys untouched)
+    if (c == 0 && tid == 0) res_publish(a, 0);
+    return;
+  }
+  SR_RES_OSUB(4);
+  auto tile_of = [&](uint32_t g) {  // tile holding R[g]: the last t with koff[t] <= g
+    int lo = 0, hi = GO - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (koff[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  K* ospl = sm.u.ospl;
+  {  // (every thread's gathers issued together)
+    constexpr int SPT = (RO::OBMAX + NT - 1) / NT;
+    K v[SPT];
+#pragma unroll
+    for (int q = 0; q < SPT; q++) {
+      const int j = q * NT + tid;
+      if (j < nbo - 1) {
+        const uint32_t g = (uint32_t)(j + 1) * OL - 1u;
+        const int t = tile_of(g);
+        v[q] = __ldcg(a.ws + (int64_t)t * TO + (g - koff[t]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < SPT; q++)
+      if (q * NT + tid < nbo - 1) ospl[q * NT + tid] = v[q];
+  }
+  __syncthreads();
+  SR_RES_OSUB(5);
+  {  // this CTA's outliers (its tiles t = c + k P hold them at ws[t0 + kept, t1)), two per thread in flight
+    int total = 0;
+    for (int t = c; t < GO; t += P) total += (int)(min((int64_t)TO, n - (int64_t)t * TO) - (koff[t + 1] - koff[t]));
+    auto at = [&](int f) {  // flat index -> position in ws
+      for (int t = c;; t += P) {
+        const int64_t t0 = (int64_t)t * TO;
+        const int kc = (int)(koff[t + 1] - koff[t]);
+        const int oc_t = (int)(min((int64_t)TO, n - t0) - kc);
+        if (f < oc_t) return t0 + kc + f;
+        f -= oc_t;
+      }
+    };
+    for (int f0 = tid; f0 < total; f0 += 2 * NT) {
+      K x[2];
+      int lo[2] = {0, 0}, hi[2];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int f = f0 + q * NT;
+        x[q] = f < total ? a.ws[at(f)] : K(0);  // (written by this CTA)
+        hi[q] = f < total ? nbo - 1 : 0;  // bucket = #{splitters < x}
+      }
+      while (lo[0] < hi[0] || lo[1] < hi[1]) {
+#pragma unroll
+        for (int q = 0; q < 2; q++)
+          if (lo[q] < hi[q]) {
+            const int mid = (lo[q] + hi[q]) >> 1;
+            if (ospl[mid] < x[q]) lo[q] = mid + 1; else hi[q] = mid;
+          }
+      }
+      uint32_t slot[2];
+#pragma unroll
+      for (int q = 0; q < 2; q++) slot[q] = f0 + q * NT < total ? atomicAdd(a.ocnt + lo[q], 1u) : 0u;
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+        if (f0 + q * NT < total) {
+          if (slot[q] < (uint32_t)OCAP) a.obuf[(int64_t)lo[q] * OCAP + slot[q]] = x[q];
+          else atomicOr(a.ocnt + OBMAX + 1, 1u);
+        }
+    }
+  }
+  __syncthreads();
+  SR_RES_OSUB(6);
+  if (a.tstamp && tid == 0) a.tstamp[8 + (size_t)c * 8 + 5] = res_now();
+  grid.sync();
+  // ---- OD: bucket starts; each bucket merged by one warp into its final range
+  if (a.tstamp && c == 0 && tid == 0) a.tstamp[2] = res_now();
+  if (__ldcg(a.ocnt + OBMAX + 1)) {  // a bucket overflowed: the host's rounds take over (keys untouched)
+    if (c == 0 && tid == 0) res_publish(a, 0);
+    return;
+  }
+  uint32_t* obase = sm.start;
+  for (int j = tid; j < nbo; j += NT) obase[j] = __ldcg(a.ocnt + j);
+  if (tid == 0) obase[nbo] = 0u;
+  __syncthreads();
+  smem_scan<NT>(obase, nbo + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  if (c == 0 && tid == 0) {
+    a.st->n_items = nbo;
+    a.st->noneq_total = (long long)(n - r);  // (the outliers)
+    res_publish(a, 1);
+  }
+  K* stage = sm.u.e.x + w * SM::WCAP;
+  SR_RES_OSUB(7);
+  for (;;) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(a.unit_counter + 2, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= (uint32_t)nbo) break;
+    const int j = (int)u;
+    const bool first = a.tstamp && u == 0 && lane == 0;  // SR_TIMING: the first unit's steps
+    if (first) a.tstamp[8 + 8 * (size_t)P + 50] = res_now();
+    const uint32_t g0 = (uint32_t)j * OL;
+    const int len = (int)min((uint32_t)OL, r - g0);
+    const int oc = (int)(obase[j + 1] - obase[j]);
+    int t = tile_of(g0);
+    for (int done = 0; done < len; t++) {  // R[g0, g0 + len) from the tiles' kept prefixes
+      const uint32_t off = g0 + (uint32_t)done - koff[t];
+      const int take = min((int)(koff[t + 1] - koff[t] - off), len - done);
+      if (take > 0) res_warp_copy<K>(stage + done, a.ws + (int64_t)t * TO + off, take);
+      done += take > 0 ? take : 0;
+    }
+    res_warp_copy<K>(stage + OL, a.obuf + (int64_t)j * OCAP, oc);
+    __syncwarp();
+    if (first) a.tstamp[8 + 8 * (size_t)P + 51] = res_now();
+    // bucket j = R[g0, g0 + len) merged with its sorted outliers O[0, oc) (R
+    // wins ties) into the staging area's last half, then copied
+    // out coalesced
+    K* dst = a.keys + g0 + obase[j];
+    K* O = stage + OL;
+    K* out = stage + OL + OCAP;
+    if (oc > 1) {
+      if (oc <= 64) res_warp_rank_sort<K>(O, oc);
+      else unit_warp_sort<K>(O, oc);
+    }
+    if (first) a.tstamp[8 + 8 * (size_t)P + 52] = res_now();
+    const K* src = stage;
+    if (oc > 0) {
+      unit_warp_merge<K>(stage, len, O, oc, out);
+      src = out;
+    }
+    for (int i = lane; i < len + oc; i += 32) dst[i] = src[i];
+    __syncwarp();
+    if (first) a.tstamp[8 + 8 * (size_t)P + 53] = res_now();
+  }
+  if (a.tstamp && c == 0 && tid == 0) a.tstamp[3] = res_now();
+  if (a.tstamp && tid == 0) a.tstamp[8 + (size_t)c * 8 + 6] = res_now();
+}
 
 template <typename K>
 __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a) {
@@ -414,7 +701,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         atomicAdd(a.arrive, 1u);
         // every route but the partition is decided here: sorted / reversed finish
         // in this launch, merge / outlier / undecided continue on the host
-        if (r != kRoutePartition) res_publish(a, (r == kRouteSorted || r == kRouteReversed) ? 1 : 0);
+        if (r != kRoutePartition && !(r == kRouteOutlier && a.out_res))
+          res_publish(a, (r == kRouteSorted || r == kRouteReversed) ? 1 : 0);
       }
     }
   }
@@ -440,6 +728,10 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
         if (p < half) { a.keys[p] = y[u]; a.keys[n - 1 - p] = x[u]; }
       }
     }
+    return;
+  }
+  if (route == kRouteOutlier && a.out_res) {
+    res_outlier<K, SM>(a, sm);
     return;
   }
   if (route != kRoutePartition) return;  // MERGE / undecided: the host planner continues

@@ -1298,12 +1298,18 @@ struct Sorter {
     const int nbins = 2 * B1 + 1;
     const int64_t n_ovf = B1 + 1;
     if (NG > slots || G > kResMaxG) fail(SR_ERR_INTERNAL, "resident tile count");
+    // in-kernel outlier route (resident.cuh ResOut): keys only, n within its bucket range
+    using RO = ResOut<K>;
+    const bool out_res = (route_ok() & kAllowOutlier) && n <= RO::MAXN;
+    const int64_t GO = ceil_div<int64_t>(n, RO::TO);
+    const int64_t obk = ceil_div<int64_t>(n, RO::OL);  // most buckets it can use
     {
       auto r = [](int64_t b) { return (b + 255) & ~int64_t(255); };
       const size_t bytes = (size_t)(r(n * kw) + r(G * 32) + 2 * r((G + 1) * 32) + r(sizeof(DevStats) + 32 + 4 * nbins) +
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
                                     r(4 * ResCfg<K>::B1MAX) + r(G * (int64_t)sizeof(TileMM)) +
-                                    r(4 * (int64_t)NG * nbins) + 8 * 256);
+                                    r(4 * (int64_t)NG * nbins) + r(4 * (RO::OBMAX + 2)) +
+                                    (out_res ? r(4 * GO) + r(2 * GO * kw) + r(obk * RO::OCAP * kw) : 0) + 12 * 256);
       DevState& dsa = t_state.ds();
       if (dsa.has_last && dsa.last_stream != c.st)  // the arena of the last call is in use until its kernel ends
         check_cuda(cudaStreamWaitEvent(c.st, dsa.last_ev, 0), "cudaStreamWaitEvent");
@@ -1334,12 +1340,14 @@ struct Sorter {
     a.asc = c.alloc<RunDesc>(G + 1);
     a.desc = c.alloc<RunDesc>(G + 1);
     {  // control block: statistics | unit counters | bucket totals, zeroed by the kernel
-      const size_t bytes = sizeof(DevStats) + 32 + 4 * (size_t)nbins + 4 * (size_t)ResCfg<K>::B1MAX;
+      const size_t bytes =
+          sizeof(DevStats) + 32 + 4 * (size_t)nbins + 4 * (size_t)ResCfg<K>::B1MAX + 4 * (size_t)(RO::OBMAX + 2);
       unsigned char* cb = c.alloc<unsigned char>((int64_t)bytes);
       a.st = reinterpret_cast<DevStats*>(cb);
       a.unit_counter = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats));
       a.tot = reinterpret_cast<uint32_t*>(cb + sizeof(DevStats) + 32);
       a.pairc = a.tot + nbins;
+      a.ocnt = a.pairc + ResCfg<K>::B1MAX;
       a.ctrl_words = (int)(bytes / 4);
     }
     DevState& ts = t_state.ds();
@@ -1370,9 +1378,15 @@ struct Sorter {
     a.ovf = c.alloc<OvfSeg>(n_ovf);
     a.lmin = T;
     a.force = forced();
-    // the one-launch partition beats the host-driven outlier rounds at this size
-    // unless the outliers are very few
-    a.merge_ok = route_ok() | kOutlierStrict;
+    // the outlier route runs in this launch when it can; otherwise the one-launch
+    // partition beats the host-driven outlier rounds at this size unless the
+    // outliers are very few
+    a.merge_ok = route_ok() | (out_res ? 0 : kOutlierStrict);
+    a.out_res = out_res ? 1 : 0;
+    a.GO = (int)GO;
+    a.okc = out_res ? c.alloc<uint32_t>(GO) : nullptr;
+    a.ofl = out_res ? c.alloc<K>(2 * GO) : nullptr;
+    a.obuf = out_res ? c.alloc<K>(obk * RO::OCAP) : nullptr;
     a.capb = std::min(CAPB, g_res_cap);
     static const bool stamps = getenv("SR_TIMING") != nullptr;
     a.tstamp = stamps ? c.alloc<unsigned long long>(8 * P + 64) : nullptr;
@@ -1411,6 +1425,15 @@ struct Sorter {
         if (q[0] && q[2])
           fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
                   (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
+      }
+      {
+        const unsigned long long* q = t + 8 + 8 * P + 40;
+        if (q[0] && q[2])
+          fprintf(stderr, "[sr_resident] outlier CTA0 us: OA flags %.1f split+write %.1f | koff %.1f check %.1f splitters %.1f classify %.1f | OD start %.1f; warp0 unit: load %.1f sort %.1f merge %.1f\n",
+                  (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, q[3] ? (q[3] - t[8 + 4]) * 1e-3 : 0.0,
+                  q[4] ? (q[4] - q[3]) * 1e-3 : 0.0, q[5] ? (q[5] - q[4]) * 1e-3 : 0.0, q[6] ? (q[6] - q[5]) * 1e-3 : 0.0,
+                  q[7] ? (q[7] - t[0]) * 1e-3 : 0.0, q[11] ? (q[11] - q[10]) * 1e-3 : 0.0,
+                  q[12] ? (q[12] - q[11]) * 1e-3 : 0.0, q[13] && q[12] ? (q[13] - q[12]) * 1e-3 : 0.0);
       }
       {
         const unsigned long long* q = t + 8 + 8 * P + 24;
@@ -1479,6 +1502,12 @@ struct Sorter {
       }
       default:
         break;
+    }
+    if (hs.route == kRouteOutlier && in_kernel) {  // the launch ran the outlier route
+      c.plan.route = SR_ROUTE_OUTLIER;
+      // scan (read), tiles read + kept / outliers written, buckets read + written
+      c.replan(h, 5 * n * kw);
+      return;
     }
     c.replan(h, n * kw);
     if (hs.route == kRouteOutlier) {
