@@ -94,7 +94,8 @@ constexpr int64_t kResMaxN = ResCfg<int32_t>::MAXN;  // largest resident n over 
 //       inside the tile, until the kept keys are sorted); kept keys in order
 //       then the outliers are written to ws[t0, t1)
 //   --  kept keys R (the tiles' kept prefixes, in order) must be sorted across
-//       tiles; splitter j = R[(j+1) OL - 1]; every outlier goes to bucket
+//       tiles: a boundary out of order loses both endpoints until it is in
+//       order; splitter j = R[(j+1) OL - 1]; every outlier goes to bucket
 //       #{splitters < x} (at most OCAP per bucket)
 //   OD  bucket j = R[j OL, (j+1) OL) merged with its sorted outliers in one
 //       warp's shared staging area, then copied to keys[j OL + outliers of the
@@ -233,7 +234,10 @@ struct ResSmem {
   union alignas(16) {
     GuideTab<K, 2048, B1MAX> guide1;  // C: level-1 classification table (guide.cuh)
     EU eu;                         // E
-    uint32_t okoff[ResOut<K>::MAXG + 1];  // outlier route: kept-key offsets of the tiles
+    struct {                       // outlier route: per tile, kept keys [ks, ke) and their offset in R
+      uint32_t koff[ResOut<K>::MAXG + 1];
+      uint16_t ks[ResOut<K>::MAXG], ke[ResOut<K>::MAXG];
+    } ot;
   } v;
   union alignas(16) {
     K samp1[S1MAX];                // A: the sampler's piece of the sample + BitonicSort scratch
@@ -381,24 +385,50 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   }
   if (a.tstamp && tid == 0) a.tstamp[8 + (size_t)c * 8 + 4] = res_now();
   grid.sync();
-  // ---- tile offsets of the kept keys R, the cross-tile order check, splitters, outlier buckets
-  uint32_t* koff = sm.v.okoff;
-  for (int t = tid; t < GO; t += NT) koff[t] = __ldcg(a.okc + t);
-  if (tid == 0) koff[GO] = 0u;
-  __syncthreads();
-  smem_scan<NT>(koff, GO + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
-  SR_RES_OSUB(3);
-  const uint32_t r = koff[GO];
-  const int nbo = (int)((r + OL - 1) / OL);
-  int bad = (r == 0 || nbo > OBMAX) ? 1 : 0;
-  if (tid == 0 && __ldcg(a.ocnt + OBMAX)) bad = 1;
-  for (int t = tid; t < GO && !bad; t += NT) {
-    if (koff[t + 1] == koff[t]) continue;
-    int u = t + 1;
-    while (u < GO && koff[u + 1] == koff[u]) u++;
-    if (u < GO && __ldcg(a.ofl + 2 * t + 1) > __ldcg(a.ofl + 2 * u)) bad = 1;
+  // ---- tile boundaries, tile offsets of the kept keys R, splitters, outlier buckets
+  // A boundary whose kept keys are out of order (a descent between the last
+  // kept key of tile t and the first of t+1) loses both endpoints until it is
+  // in order, as inside the tiles: tile t keeps ws[t0 + oks[t], t0 + oke[t]).
+  // (Every CTA resolves every boundary itself, so no further grid barrier.)
+  uint32_t* koff = sm.v.ot.koff;
+  uint16_t* oks = sm.v.ot.ks;
+  uint16_t* oke = sm.v.ot.ke;
+  int bad = 0;
+  if (tid == 0 && __ldcg(a.ocnt + OBMAX)) bad = 1;  // a tile's kept keys were not sorted
+  for (int t = tid; t < GO; t += NT) {
+    const int kc = (int)__ldcg(a.okc + t);
+    if (kc == 0) bad = 1;
+    if (t == 0) oks[0] = 0;
+    if (t == GO - 1) oke[t] = (uint16_t)kc;
+    if (t + 1 < GO && kc > 0) {
+      const int kn = (int)__ldcg(a.okc + t + 1);
+      const K* wt = a.ws + (int64_t)t * TO;
+      const K* wu = wt + TO;
+      int ia = kc - 1, ib = 0;
+      K x = __ldcg(a.ofl + 2 * t + 1), y = __ldcg(a.ofl + 2 * t + 2);
+      while (x > y) {
+        ia--;
+        ib++;
+        if (ia < 0 || ib >= kn || ib > 64) { bad = 1; break; }
+        x = __ldcg(wt + ia);
+        y = __ldcg(wu + ib);
+      }
+      oke[t] = (uint16_t)(ia + 1);
+      oks[t + 1] = (uint16_t)ib;
+    }
   }
-  if (__syncthreads_or(bad)) {  // not a few-outlier input: the host's rounds take over (keys untouched)
+  bad = __syncthreads_or(bad);
+  for (int t = tid; t < GO && !bad; t += NT) {
+    if (oks[t] >= oke[t]) bad = 1;
+    koff[t] = (uint32_t)(oke[t] - oks[t]);
+  }
+  if (tid == 0) koff[GO] = 0u;
+  bad = __syncthreads_or(bad);
+  if (!bad) smem_scan<NT>(koff, GO + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  SR_RES_OSUB(3);
+  const uint32_t r = bad ? 0u : koff[GO];
+  const int nbo = (int)((r + OL - 1) / OL);
+  if (__syncthreads_or(bad || r == 0 || nbo > OBMAX)) {  // not a few-outlier input: the host's rounds take over (keys untouched)
     if (c == 0 && tid == 0) res_publish(a, 0);
     return;
   }
@@ -421,7 +451,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
       if (j < nbo - 1) {
         const uint32_t g = (uint32_t)(j + 1) * OL - 1u;
         const int t = tile_of(g);
-        v[q] = __ldcg(a.ws + (int64_t)t * TO + (g - koff[t]));
+        v[q] = __ldcg(a.ws + (int64_t)t * TO + oks[t] + (g - koff[t]));
       }
     }
 #pragma unroll
@@ -433,12 +463,12 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   {  // this CTA's outliers (its tiles t = c + k P hold them at ws[t0 + kept, t1)), two per thread in flight
     int total = 0;
     for (int t = c; t < GO; t += P) total += (int)(min((int64_t)TO, n - (int64_t)t * TO) - (koff[t + 1] - koff[t]));
-    auto at = [&](int f) {  // flat index -> position in ws
+    auto at = [&](int f) {  // flat index -> position in ws (a tile's outliers: [0, oks) and [oke, len))
       for (int t = c;; t += P) {
         const int64_t t0 = (int64_t)t * TO;
-        const int kc = (int)(koff[t + 1] - koff[t]);
-        const int oc_t = (int)(min((int64_t)TO, n - t0) - kc);
-        if (f < oc_t) return t0 + kc + f;
+        const int ks = oks[t], ke = oke[t];
+        const int oc_t = (int)(min((int64_t)TO, n - t0) - (ke - ks));
+        if (f < oc_t) return t0 + (f < ks ? f : ke + (f - ks));
         f -= oc_t;
       }
     };
@@ -507,7 +537,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
     for (int done = 0; done < len; t++) {  // R[g0, g0 + len) from the tiles' kept prefixes
       const uint32_t off = g0 + (uint32_t)done - koff[t];
       const int take = min((int)(koff[t + 1] - koff[t] - off), len - done);
-      if (take > 0) res_warp_copy<K>(stage + done, a.ws + (int64_t)t * TO + off, take);
+      if (take > 0) res_warp_copy<K>(stage + done, a.ws + (int64_t)t * TO + oks[t] + off, take);
       done += take > 0 ? take : 0;
     }
     res_warp_copy<K>(stage + OL, a.obuf + (int64_t)j * OCAP, oc);

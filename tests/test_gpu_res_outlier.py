@@ -140,3 +140,28 @@ def test_res_outlier_disabled():
     sr.set_option(sr.OPT_OUTLIER_ROUTE, 0)
     p = check(gen.make("nearly", 2_000_000, np.int32, config=1))
     assert p["route_name"] != "outlier"
+
+
+def test_res_outlier_c2_instances_stay_in_kernel():
+    """The bench's C2 nearly instances: clusters of exchanges that straddle a
+    tile boundary are resolved by trimming the boundary (no host hand-off)."""
+    n = 2_000_000
+    in_kernel = 0
+    for inst in range(20):
+        p = check(gen.make("nearly", n, np.int32, config=1, instance=inst))
+        assert p["route_name"] == "outlier", p
+        in_kernel += p["launches"] == 1
+    assert in_kernel == 20, in_kernel
+
+
+def test_res_outlier_boundary_trim():
+    """Exchanges chained through both sides of every outlier tile boundary."""
+    n = 1_200_000
+    a = np.arange(n, dtype=np.int32)
+    for t in range(TO32, n - 64, TO32):
+        a[t - 2], a[t + 1] = a[t + 1], a[t - 2]
+        a[t - 1], a[t + 3] = a[t + 3], a[t - 1]
+        a[t - 5], a[t] = a[t], a[t - 5]
+    sr.set_option(sr.OPT_FORCE_ROUTE, sr.ROUTE_OUTLIER)  # (auto: the k-distance route takes it)
+    p = check(a)
+    assert p["route_name"] == "outlier" and p["launches"] == 1, p
