@@ -197,7 +197,8 @@ enum {
                              +0 fused second level (k_bucket_sort) 1/0 (default 0: measured slower, DESIGN.md
                              §6.3); +1 level-1 buckets for n >= 2^26 (power of two <= 2048, default 512); +2 mean sub-bucket of
                              the fused level (16..4096, default 256); +3 cap on the level-1 buckets at
-                             any n (power of two, 0 = none; tests reach the fused level at small n) */
+                             any n (power of two, 0 = none; tests reach the fused level at small n); +5 keys-only
+                             scatter by two 512-thread CTAs per SM (1, default) or one 1024-thread CTA (0) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

@@ -110,6 +110,28 @@ __device__ __forceinline__ T warp_reduce_max(T v) {
   for (int o = 16; o > 0; o >>= 1) { T u = __shfl_xor_sync(0xffffffffu, v, o); v = u > v ? u : v; }
   return v;
 }
+// 32- and 64-bit signed keys: the warp reduction instruction (redux.sync), a
+// 64-bit key as its high word, then the low words of the lanes that hold it.
+template <>
+__device__ __forceinline__ int32_t warp_reduce_min<int32_t>(int32_t v) {
+  return __reduce_min_sync(0xffffffffu, v);
+}
+template <>
+__device__ __forceinline__ int32_t warp_reduce_max<int32_t>(int32_t v) {
+  return __reduce_max_sync(0xffffffffu, v);
+}
+template <>
+__device__ __forceinline__ int64_t warp_reduce_min<int64_t>(int64_t v) {
+  const int32_t hi = __reduce_min_sync(0xffffffffu, (int32_t)(v >> 32));
+  const unsigned lo = __reduce_min_sync(0xffffffffu, (int32_t)(v >> 32) == hi ? (unsigned)v : 0xffffffffu);
+  return (int64_t)(((uint64_t)(uint32_t)hi << 32) | lo);
+}
+template <>
+__device__ __forceinline__ int64_t warp_reduce_max<int64_t>(int64_t v) {
+  const int32_t hi = __reduce_max_sync(0xffffffffu, (int32_t)(v >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (int32_t)(v >> 32) == hi ? (unsigned)v : 0u);
+  return (int64_t)(((uint64_t)(uint32_t)hi << 32) | lo);
+}
 
 // Block-wide exclusive sum. `scratch` needs NT/32 + 1 entries. Returns the
 // exclusive prefix; *total receives the block sum. Contains __syncthreads().

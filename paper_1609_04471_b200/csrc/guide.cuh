@@ -53,7 +53,7 @@ __device__ __forceinline__ uint64_t guide_u(K x) {  // order-preserving unsigned
 // counts (a = #{ud_k < start(c)} = #{k : cell(k) < c} because ud is sorted).
 // Returns with g complete and visible to the block.
 template <typename K, int NT, typename G>
-__device__ void guide_build(const K* spl, const uint8_t* eqf, int m, G& g, int* red) {
+__device__ __noinline__ void guide_build(const K* spl, const uint8_t* eqf, int m, G& g, int* red) {
   constexpr int kGCells = G::kCells;
   constexpr int PER = (G::kBMax + NT - 1) / NT;
   constexpr int CPT = kGCells / NT;

@@ -87,6 +87,14 @@ __device__ void smem_scan(T* a, int L, T identity, Op op, bool exclusive, bool r
   __syncthreads();
 }
 
+// Exclusive sum of a shared uint32 array in place (one out-of-line copy: the
+// resident kernel calls it from several phases, and every inlined copy is
+// instruction-cache footprint fetched cold after an L2 flush).
+template <int NT>
+__device__ __noinline__ void smem_exclusive_sum_u32(uint32_t* a, int L, uint32_t* scratch) {
+  smem_scan<NT>(a, L, 0u, [](uint32_t x, uint32_t y) { return x + y; }, true, false, scratch);
+}
+
 // ---------------------------------------------------------------------------
 // K7: splitters for every segment of a level, in two kernels.
 //
@@ -835,6 +843,114 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
     const int tot = (int)sm.total;
     for (int p = tid; p < tot; p += NT) {
       int b = sm.stb[p];
+      dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
+    }
+    __syncthreads();
+  }
+}
+
+// K10k2 (keys only, bucket ids from the count pass): the same per-sub-tile
+// counting sort as k_scatter_keys with NT = 512 threads, 8K-key sub-tiles and
+// tables sized for NBC bins, so that two CTAs share an SM and one's loads
+// overlap the other's stores (k_scatter_keys: one 1024-thread CTA per SM whose
+// phases are serialised by its barriers).
+template <typename K, int NT, int VTS, int NBC>
+struct ScatterKeys2Smem {
+  static constexpr int ST = NT * VTS;
+  K stk[ST];
+  uint32_t cnt[NBC];
+  uint32_t base[NBC];
+  uint32_t run[NBC];
+  uint16_t lstart[NBC];
+  uint16_t stb[ST];
+  uint32_t red[NT / 32 + 1];
+  uint32_t total;
+};
+
+template <typename K, int NT, int VTS, int NBC>
+__global__ void __launch_bounds__(NT, 2) k_scatter_keys2(const K* __restrict__ src, K* __restrict__ dst,
+                                                          const SegDesc* __restrict__ segs,
+                                                          const int* __restrict__ chunk_seg, int64_t chunk_size,
+                                                          uint32_t* __restrict__ cursor,
+                                                          const uint16_t* __restrict__ bins_in,
+                                                          const uint32_t* __restrict__ mat,
+                                                          const DevStats* __restrict__ gate) {
+  if (gate && (gate->route != kRoutePartition || gate->noneq_total == 0)) return;
+  using SM = ScatterKeys2Smem<K, NT, VTS, NBC>;
+  constexpr int ST = SM::ST;
+  static_assert(ST <= 65535, "16-bit local offsets");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x;
+  const int s = chunk_seg[c];
+  const SegDesc seg = segs[s];
+  const int g = c - seg.chunk_base;
+  const int nb = seg.nbins;
+  uint32_t* cur = mat ? nullptr : cursor + seg.mat_base;
+  if (mat)
+    for (int b = tid; b < nb; b += NT)
+      sm.run[b] = (uint32_t)(seg.start + ((int64_t)mat[seg.mat_base + (int64_t)b * seg.nchunks + g] - seg.len_prefix));
+  const int64_t c0 = seg.start + (int64_t)g * chunk_size;
+  const int64_t c1 = (c0 + chunk_size < seg.start + seg.len) ? c0 + chunk_size : seg.start + seg.len;
+  for (int64_t sub = c0; sub < c1; sub += ST) {
+    for (int b = tid; b < nb; b += NT) sm.cnt[b] = 0;
+    __syncthreads();
+    K x[VTS];
+    int bin[VTS];
+    uint32_t rk[VTS];
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      const int64_t p = sub + i * NT + tid;
+      x[i] = p < c1 ? src[p] : K(0);
+      bin[i] = p < c1 ? (int)bins_in[p] : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      if (bin[i] & 1) bin[i] = -1;  // (also the positions past c1) equality buckets are filled later
+      else rk[i] = atomicAdd(&sm.cnt[bin[i]], 1u);
+    }
+    __syncthreads();
+    {  // local starts (exclusive scan of cnt) and this chunk's slices of the buckets
+      constexpr int BPT = (NBC + NT - 1) / NT;
+      uint32_t v[BPT], sum = 0;
+#pragma unroll
+      for (int r = 0; r < BPT; r++) {
+        const int b = tid * BPT + r;
+        v[r] = b < nb ? sm.cnt[b] : 0u;
+        sum += v[r];
+      }
+      uint32_t tot;
+      uint32_t pre = block_exclusive_sum<NT>(sum, sm.red, &tot);
+#pragma unroll
+      for (int r = 0; r < BPT; r++) {
+        const int b = tid * BPT + r;
+        if (b < nb) {
+          sm.lstart[b] = (uint16_t)pre;
+          if (mat) {
+            sm.base[b] = sm.run[b];
+            sm.run[b] += v[r];
+          } else if (v[r]) {
+            sm.base[b] = atomicAdd(&cur[b], v[r]);
+          }
+        }
+        pre += v[r];
+      }
+      if (tid == 0) sm.total = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < VTS; i++) {
+      if (bin[i] >= 0) {
+        const uint32_t lp = sm.lstart[bin[i]] + rk[i];
+        sm.stk[lp] = x[i];
+        sm.stb[lp] = (uint16_t)bin[i];
+      }
+    }
+    __syncthreads();
+    const int tot = (int)sm.total;
+    for (int p = tid; p < tot; p += NT) {
+      const int b = sm.stb[p];
       dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
     }
     __syncthreads();

@@ -292,9 +292,14 @@ __device__ __forceinline__ void scan_range_vec(const K* __restrict__ keys, int64
       sm &= dm;
       if (smn) {  // subtile min / max over the keys of [t0, t1)
         K mn = KeyTraits<K>::max_key(), mx = KeyTraits<K>::min_key();
+        if (i0 + V <= t1 && i0 + V <= n) {  // (every vector but the last of a range)
 #pragma unroll
-        for (int j = 0; j < V; j++)
-          if (i0 + j < t1 && i0 + j < n) { mn = min(mn, x[r][j]); mx = max(mx, x[r][j]); }
+          for (int j = 0; j < V; j++) { mn = min(mn, x[r][j]); mx = max(mx, x[r][j]); }
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; j++)
+            if (i0 + j < t1 && i0 + j < n) { mn = min(mn, x[r][j]); mx = max(mx, x[r][j]); }
+        }
         mn = warp_reduce_min(mn);
         mx = warp_reduce_max(mx);
         if (lane == 0 && i0 < t1) {

@@ -347,7 +347,6 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   const int P = gridDim.x, c = blockIdx.x;
   const int64_t n = a.n;
   const int GO = a.GO;
-  auto add = [](uint32_t x, uint32_t y) { return x + y; };
   // ---- OA: outliers of every tile; ws[t0, t1) = kept keys in order, then the outliers
   {
     OutSmem<K, NT, TO>& os = sm.u.ot;
@@ -424,7 +423,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   }
   if (tid == 0) koff[GO] = 0u;
   bad = __syncthreads_or(bad);
-  if (!bad) smem_scan<NT>(koff, GO + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  if (!bad) smem_exclusive_sum_u32<NT>(koff, GO + 1, reinterpret_cast<uint32_t*>(sm.red));
   SR_RES_OSUB(3);
   const uint32_t r = bad ? 0u : koff[GO];
   const int nbo = (int)((r + OL - 1) / OL);
@@ -514,7 +513,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   for (int j = tid; j < nbo; j += NT) obase[j] = __ldcg(a.ocnt + j);
   if (tid == 0) obase[nbo] = 0u;
   __syncthreads();
-  smem_scan<NT>(obase, nbo + 1, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  smem_exclusive_sum_u32<NT>(obase, nbo + 1, reinterpret_cast<uint32_t*>(sm.red));
   if (c == 0 && tid == 0) {
     a.st->n_items = nbo;
     a.st->noneq_total = (long long)(n - r);  // (the outliers)
@@ -567,8 +566,85 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
   if (a.tstamp && tid == 0) a.tstamp[8 + (size_t)c * 8 + 6] = res_now();
 }
 
+// Phase C for one held group (tile [t0, t1) of src, slot k): 3-way bucket ids
+// from the guide table, a counting sort of the group by bucket in shared
+// memory, and the group's piece offset inside every bucket (one atomicAdd on
+// the bucket total).
+template <typename K, typename SM>
+__device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __restrict__ src, int64_t t0, int64_t t1,
+                                       int k, int nbins, uint32_t* __restrict__ tot, uint32_t* __restrict__ goff_row) {
+  constexpr int NT = kResNT;
+  constexpr int U = kResGrp / NT;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = blockIdx.x;
+  typename SM::CT& ct = sm.u.ct;
+  SR_RES_SUB(0);
+  for (int b = tid; b < nbins; b += NT) ct.cnt[b] = 0;
+  K x[U];
+  int bin[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t i = t0 + u * NT + tid;
+    x[u] = i < t1 ? src[i] : K(0);
+  }
+  guide_classify<K, U>(x, bin, sm.v.guide1);
+  SR_RES_SUB(1);
+  __syncthreads();
+  uint32_t rk[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t i = t0 + u * NT + tid;
+    const bool valid = i < t1;
+    rk[u] = 0;
+    if (__any_sync(0xffffffffu, valid && (bin[u] & 1))) {
+      // equality ids: warp-aggregated increments, ranks from the peer mask
+      const unsigned peers = __match_any_sync(0xffffffffu, valid ? bin[u] : -1);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (valid && lane == leader) base = atomicAdd(&ct.cnt[bin[u]], (uint32_t)__popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      rk[u] = base + __popc(peers & lanemask_lt());
+    } else if (valid) {
+      rk[u] = atomicAdd(&ct.cnt[bin[u]], 1u);
+    }
+    if (!valid) bin[u] = -1;
+  }
+  SR_RES_SUB(2);
+  __syncthreads();
+  uint32_t* lst = ct.lst[k];
+  {  // unrolled: all of a thread's atomics in flight together
+    constexpr int BI = (SM::NB1 + NT - 1) / NT;
+    uint32_t go[BI];
+#pragma unroll
+    for (int r = 0; r < BI; r++) {
+      const int b = r * NT + tid;
+      const uint32_t cb = b < nbins ? ct.cnt[b] : 0u;
+      if (b < nbins) lst[b] = cb;
+      // this group's piece of bucket b starts at offset goff inside the bucket
+      // (pieces of different groups in arbitrary order: the bucket is sorted later)
+      go[r] = cb ? atomicAdd(&tot[b], cb) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < BI; r++)
+      if (r * NT + tid < nbins) goff_row[r * NT + tid] = go[r];
+  }
+  if (tid == 0) lst[nbins] = (uint32_t)(t1 - t0);
+  SR_RES_SUB(3);
+  __syncthreads();
+  smem_exclusive_sum_u32<NT>(lst, nbins, reinterpret_cast<uint32_t*>(sm.red));
+  SR_RES_SUB(4);
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (bin[u] >= 0) {
+      ct.stk[k][lst[bin[u]] + rk[u]] = x[u];
+      ct.stb[k][lst[bin[u]] + rk[u]] = (uint16_t)bin[u];
+    }
+  __syncthreads();
+  SR_RES_SUB(5);
+}
+
 template <typename K>
-__global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a) {
+__global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid_constant__ ResArgs<K> a) {
   namespace cg = cooperative_groups;
   using SM = ResSmem<K>;
   constexpr int NT = kResNT;
@@ -579,7 +655,6 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   const int P = gridDim.x, c = blockIdx.x;
   const int64_t n = a.n;
   const int nbins = 2 * a.B1 + 1;
-  auto add = [](uint32_t x, uint32_t y) { return x + y; };
 
   // ================= A: H1 tile scan; level-1 sample ranked by every CTA =================
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[0] = res_now();
@@ -858,75 +933,11 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
   SR_RES_STAMP(3);
   const int ngm = (c < PS && a.NG > c) ? (a.NG - 1 - c) / PS + 1 : 0;  // groups of this CTA: t = c + k PS, k < ngm <= GPC
   {
-    typename SM::CT& ct = sm.u.ct;
-    constexpr int U = kResGrp / NT;
     for (int k = 0; k < ngm; k++) {
       const int t = c + k * PS;
       const int64_t t0 = (int64_t)t * a.tile;
       const int64_t t1 = t0 + a.tile < n ? t0 + a.tile : n;
-      SR_RES_SUB(0);
-      for (int b = tid; b < nbins; b += NT) ct.cnt[b] = 0;
-      K x[U];
-      int bin[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t i = t0 + u * NT + tid;
-        x[u] = i < t1 ? a.keys[i] : K(0);
-      }
-      guide_classify<K, U>(x, bin, sm.v.guide1);
-      SR_RES_SUB(1);
-      __syncthreads();
-      uint32_t rk[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t i = t0 + u * NT + tid;
-        const bool valid = i < t1;
-        rk[u] = 0;
-        if (__any_sync(0xffffffffu, valid && (bin[u] & 1))) {
-          // equality ids: warp-aggregated increments, ranks from the peer mask
-          const unsigned peers = __match_any_sync(0xffffffffu, valid ? bin[u] : -1);
-          const int leader = __ffs(peers) - 1;
-          uint32_t base = 0;
-          if (valid && lane == leader) base = atomicAdd(&ct.cnt[bin[u]], (uint32_t)__popc(peers));
-          base = __shfl_sync(0xffffffffu, base, leader);
-          rk[u] = base + __popc(peers & lanemask_lt());
-        } else if (valid) {
-          rk[u] = atomicAdd(&ct.cnt[bin[u]], 1u);
-        }
-        if (!valid) bin[u] = -1;
-      }
-      SR_RES_SUB(2);
-      __syncthreads();
-      uint32_t* lst = ct.lst[k];
-      {  // unrolled: all of a thread's atomics in flight together
-        constexpr int BI = (SM::NB1 + NT - 1) / NT;
-        uint32_t go[BI];
-#pragma unroll
-        for (int r = 0; r < BI; r++) {
-          const int b = r * NT + tid;
-          const uint32_t cb = b < nbins ? ct.cnt[b] : 0u;
-          if (b < nbins) lst[b] = cb;
-          // this group's piece of bucket b starts at offset goff inside the bucket
-          // (pieces of different groups in arbitrary order: the bucket is sorted later)
-          go[r] = cb ? atomicAdd(&a.tot[b], cb) : 0u;
-        }
-#pragma unroll
-        for (int r = 0; r < BI; r++)
-          if (r * NT + tid < nbins) a.goff[(size_t)t * nbins + r * NT + tid] = go[r];
-      }
-      if (tid == 0) lst[nbins] = (uint32_t)(t1 - t0);
-      SR_RES_SUB(3);
-      __syncthreads();
-      smem_scan<NT>(lst, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
-      SR_RES_SUB(4);
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        if (bin[u] >= 0) {
-          ct.stk[k][lst[bin[u]] + rk[u]] = x[u];
-          ct.stb[k][lst[bin[u]] + rk[u]] = (uint16_t)bin[u];
-        }
-      __syncthreads();
-      SR_RES_SUB(5);
+      res_group<K, SM>(a, sm, a.keys, t0, t1, k, nbins, a.tot, a.goff + (size_t)t * nbins);
     }
   }
   SR_RES_STAMP(4);
@@ -944,7 +955,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(ResArgs<K> a
       if (r * NT + tid < nbins) start[r * NT + tid] = v[r];
   }
   __syncthreads();
-  smem_scan<NT>(start, nbins, 0u, add, true, false, reinterpret_cast<uint32_t*>(sm.red));
+  smem_exclusive_sum_u32<NT>(start, nbins, reinterpret_cast<uint32_t*>(sm.red));
   if (tid == 0) start[nbins] = (uint32_t)n;
   __syncthreads();
   if (c == 0) {  // statistics; every bucket size is known: publish the outcome early

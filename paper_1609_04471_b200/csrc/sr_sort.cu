@@ -52,7 +52,7 @@ int64_t g_ws_limit = 0;  // SR_OPT_WS_LIMIT (fault injection), 0 = none
 //   [0] fused level 2 (k_bucket_sort) on/off   [1] level-1 buckets for n >= kBigLevel1
 //   [2] mean sub-bucket the fused level aims for   [3] cap on the level-1 buckets at any n (0 = none; tests)
 //   [4] k_bucket_sort phase skips (timing experiments only; the output is then NOT sorted): 1 finishing, 2 scatter
-int64_t g_tune[8] = {0, 512, 256, 0, 0, 0, 0, 0};
+int64_t g_tune[8] = {0, 512, 256, 0, 0, 1, 0, 0};
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -815,6 +815,22 @@ struct Sorter {
     for (auto& s : L.segs) keys_in += s.len;
     const int64_t noneq = hs ? hs->noneq_total : keys_in;
     const DevStats* gate = hs ? nullptr : L.d_st;
+    if (!HAS_V && g_tune[5] && L.d_bins) {  // (A/B: two 512-thread CTAs per SM)
+      constexpr int VT2 = sizeof(K) == 4 ? 16 : 8;
+      const bool small = L.total_bins <= 1025 * (int64_t)L.segs.size() && [&] {
+        for (auto& sd : L.segs) if (sd.nbins > 1025) return false;
+        return true;
+      }();
+      auto launch2 = [&](auto kern, size_t smem) {
+        set_smem(kern, smem);
+        return c.launch("scatter", keys_in * kw + noneq * kw, [&] {
+          kern<<<(unsigned)L.total_chunks, 512, smem, c.st>>>(sk, dk, L.d_segs, L.d_chunk_seg, L.chunk_size, L.d_cursor,
+                                                               L.d_bins, L.atomic ? nullptr : L.d_mat, gate);
+        });
+      };
+      if (small) return launch2(k_scatter_keys2<K, 512, VT2, 1025>, sizeof(ScatterKeys2Smem<K, 512, VT2, 1025>));
+      return launch2(k_scatter_keys2<K, 512, VT2, kMaxBins>, sizeof(ScatterKeys2Smem<K, 512, VT2, kMaxBins>));
+    }
     if (!HAS_V) {
       using SM = ScatterKeysSmem<K, kScatKNT, scat_kvt<K>()>;
       size_t smem = sizeof(SM);

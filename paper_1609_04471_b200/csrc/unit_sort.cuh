@@ -113,7 +113,7 @@ __device__ __forceinline__ void unit_warp_sort(K* ks, int len) {
 // touches 4x (int32) / 2x (int64) fewer sectors than one key per lane would
 // (lane-strided slices are uncoalesced by construction).
 template <typename K>
-__device__ __forceinline__ void unit_warp_merge(const K* A, int na, const K* B, int nb, K* __restrict__ dst) {
+__device__ __noinline__ void unit_warp_merge(const K* A, int na, const K* B, int nb, K* __restrict__ dst) {
   constexpr int V = 16 / (int)sizeof(K);
   using Vec = typename std::conditional<sizeof(K) == 4, int4, longlong2>::type;
   const int lane = threadIdx.x & 31;
@@ -221,7 +221,7 @@ __device__ __noinline__ void unit_cta_merge_sort(K* a, K* b, int L, K* __restric
 #define SR_UNIT_MARK(k)
 #endif
 template <typename K, int CAP, int NT>
-__device__ void unit_sort(K* __restrict__ dst, int L, UnitSmem<K, CAP, NT>& e) {
+__device__ __noinline__ void unit_sort(K* __restrict__ dst, int L, UnitSmem<K, CAP, NT>& e) {
   using U = UnitSmem<K, CAP, NT>;
   constexpr int SB = U::SB, NB = U::NB, O2 = U::O2, S2 = U::S2, NW = U::NW;
   constexpr int DEPTH = 5;
