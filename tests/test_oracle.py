@@ -496,6 +496,16 @@ def test_measures_brute_force_small():
             assert m["max_dis"] == int(d.max()) and m["misplaced"] == int((d != 0).sum())
 
 
+def test_mono_exhaustive_three_letters():
+    """Mono against the dynamic program over all cut points on EVERY sequence
+    of length <= 9 over 3 letters (the definition)."""
+    import itertools
+    for n in range(1, 10):
+        for t in itertools.product((0, 1, 2), repeat=n):
+            a = np.array(t, np.int32)
+            assert oracle.measures(a)["mono"] == _mono_dp(list(t)), t
+
+
 @pytest.mark.parametrize("k", [1, 8, 256])
 def test_measures_generated_classes(k):
     n = 20000
