@@ -11,17 +11,18 @@
 // splitter partition into <= 2048 buckets followed by per-warp (or, for big
 // buckets, per-CTA) sorts of the buckets.
 //   A  H1 scan of every tile (vectorised, presort.cuh scan_range_vec); CTA 0
-//      zeroes the control block.  The last four CTAs (one tile each) gather
-//      and sort one quarter each of the level-1 sample (S1 = O1 B1 jittered
-//      positions, R8).
+//      zeroes the control block.  The last four CTAs (no tile) gather and
+//      sort one quarter each of the level-1 sample (S1 = O1 B1 jittered
+//      positions, R8), merge the quarters pairwise, select the
+//      splitters (R14) and build the guide table (sampler 0) -- speculatively,
+//      before the route is known, so the splitters are ready when it is.
 //   -- grid sync --
 //   C  warp 0 resolves the tile summaries into the device route (K2's logic;
-//      CTA 0 also writes the statistics and run lists) while the other warps
-//      merge the sample quarters pairwise.  SORTED exits;
+//      CTA 0 also writes the statistics and run lists).  SORTED exits;
 //      REVERSED reverses in place; MERGE / undecided
 //      return to the host planner.  PARTITION: splitter j = element O1 (j+1)
 //      of the merged halves (merge-path selection, R14) with its gamma flag
-//      (count > gamma = 2 in the sample) -> Eytzinger tree; each
+//      (count > gamma = 2 in the sample) -> guide table; each
 //      held tile is classified (3-way ids) and counting-
 //      sorted by bucket in shared memory; its piece offset inside every bucket
 //      comes from one atomicAdd on the bucket total.
@@ -142,6 +143,9 @@ struct ResArgs {
   uint32_t* pairc;          // B1MAX: halves done per class-A warp unit (zeroed with the control block)
   uint32_t* arrive;         // persistent arrival counter of the route step (never reset)
   uint32_t arrive_base;     // its value before this launch (every launch adds gridDim.x + 1)
+  uint32_t* scount;         // persistent sampler-step counter (never reset; every launch adds 3 kResSamplers)
+  uint32_t scount_base;     // its value before this launch
+  GuideTab<K, 2048, ResCfg<K>::B1MAX>* guide;  // level-1 classification table (built by sampler 0)
   int ctrl_words;           // 32-bit words of the control block st | unit_counter | tot (zeroed in phase A)
   ResDone* done;            // host-mapped completion record (CTA 0 writes it once the outcome is known)
   uint32_t seq;             // this call's completion sequence number
@@ -287,6 +291,43 @@ static_assert(sizeof(ResSmem<int32_t>) <= 227 * 1024 && sizeof(ResSmem<int64_t>)
               "one CTA per SM: the shared-memory layout must fit the 227 KB opt-in limit");
 static_assert(offsetof(ResSmem<int32_t>, u) % 16 == 0 && offsetof(ResSmem<int64_t>, u) % 16 == 0,
               "vectorised sort buffers need 16-byte alignment");
+
+// Block sort of x[0, L) (L a power of two, 128 <= L <= 4 NT; x and y hold L
+// keys each): every warp sorts 128-key chunks with its register network, then
+// log2(L / 128) merge-path rounds (4 outputs per thread, one barrier each)
+// ping-pong between x and y.  Returns the buffer holding the sorted keys.
+// (Used for the samplers' quarters: the block bitonic network with a barrier
+// per cross-warp stage took 5.5 us for 2048 keys.)
+template <typename K, int NT>
+__device__ __forceinline__ K* res_block_sort(K* x, K* y, int L) {
+  const int tid = threadIdx.x, w = tid >> 5;
+  for (int c0 = w * 128; c0 < L; c0 += NT * 4) WarpBitonic<K, 4>::sort(x + c0, 128);
+  __syncthreads();
+  K* src = x;
+  K* dst = y;
+  for (int W = 128; W < L; W *= 2) {
+    for (int o0 = tid * 4; o0 < L; o0 += NT * 4) {
+      const int p0 = (o0 / (2 * W)) * (2 * W);
+      const K* A = src + p0;
+      const K* B = A + W;
+      const int diag = o0 - p0;
+      int i = merge_path_search<K>([&](int q) { return A[q]; }, W, [&](int q) { return B[q]; }, W, diag);
+      int j = diag - i;
+#pragma unroll
+      for (int d = 0; d < 4; d++) {
+        const bool tA = j >= W || (i < W && !(B[j] < A[i]));
+        dst[o0 + d] = tA ? A[i] : B[j];
+        i += tA;
+        j += !tA;
+      }
+    }
+    __syncthreads();
+    K* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src;
+}
 
 // outlier-route sub-steps of CTA 0 (SR_TIMING diagnostics)
 #define SR_RES_OSUB(kk)                                                                             \
@@ -769,8 +810,118 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       if (q < QS) e.x[q] = sx[r];
     }
     __syncthreads();
-    BitonicSort<K, NT, SG>::sort(e.x, QS);  // register / shuffle bitonic network, QS <= NT SG keys
-    for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = e.x[q];
+    SR_RES_CSUB(5);
+    const K* sq = QS >= 128 ? res_block_sort<K, NT>(e.x, e.y, QS) : e.x;
+    if (QS < 128) BitonicSort<K, NT, SG>::sort(e.x, QS);
+    SR_RES_CSUB(6);
+    for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = sq[q];
+  }
+  if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
+    static_assert(kResSamplers == 4, "four sorted sample pieces");
+    // speculatively, before the route is known (the splitters are ready when it
+    // is; wasted only on the sorted / reversed / outlier routes, which the
+    // other CTAs finish without the samplers).  Sampler steps are counted on a
+    // persistent counter that every launch advances by 3 kResSamplers.
+    const int m1 = a.B1 - 1;
+    typename SM::SP& sp = sm.u.sp;
+    // (every sampler takes every step, so the counter advances by the same
+    // amount in every launch; once CTA 0 has published a route other than
+    // PARTITION the remaining work is skipped)
+    __shared__ int s_skip;
+    if (tid == 0) s_skip = 0;
+    auto step = [&](uint32_t target) {  // publish this CTA's writes, wait for the other samplers'
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(a.scount, 1u);
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.scount) : "memory");
+        } while ((uint32_t)(v - a.scount_base) < target);
+        uint32_t arr;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(arr) : "l"(a.arrive) : "memory");
+        if ((uint32_t)(arr - a.arrive_base) >= (uint32_t)P + 1u &&
+            __ldcg(reinterpret_cast<const long long*>(&a.st->route)) != kRoutePartition)
+          s_skip = 1;
+      }
+      __syncthreads();
+      return s_skip != 0;
+    };
+    const bool skip1 = step(kResSamplers);
+    SR_RES_CSUB(0);
+    if (!skip1) {  // half h = quarter / 2 of the pairwise merges (pieces 2h, 2h+1), this sampler's
+       // part of it: merged positions [part R, (part + 1) R), written to mrg[h 2R + ...]
+      const int R = QS, h = quarter >> 1, part = quarter & 1;
+      for (int i = tid; i < 2 * R; i += NT) sp.q[i] = __ldcg(a.samp + (int64_t)h * 2 * R + i);
+      __syncthreads();
+      SR_RES_CSUB(1);
+      const K* A = sp.q;
+      const K* B = sp.q + R;
+      const int per = (R + NT - 1) / NT, d0 = part * R + tid * per, d1 = min(d0 + per, (part + 1) * R);
+      if (d0 < d1) {
+        int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, d0);
+        int j = d0 - i;
+        for (int d = d0; d < d1; d++) {
+          const bool tA = j >= R || (i < R && !(B[j] < A[i]));
+          a.mrg[(int64_t)h * 2 * R + d] = tA ? A[i] : B[j];
+          i += tA;
+          j += !tA;
+        }
+      }
+    }
+    SR_RES_CSUB(4);
+    const bool skip2 = step(2 * kResSamplers);
+    SR_RES_CSUB(2);
+    // splitter j = element O1 (j+1) of the merged halves (DESIGN.md R9, R14),
+    // with its gamma flag (more than gamma = 2 of the elements r-2 .. r+2 equal
+    // to it, PAPER.md:168); this sampler's quarter of the j range, +inf padded
+    if (!skip2) {
+    for (int i = tid; i < S1; i += NT) sp.q[i] = __ldcg(a.mrg + i);
+    __syncthreads();
+    const K* A0 = sp.q;
+    const K* A1 = sp.q + H1;
+    constexpr int JQ = B1MAX / kResSamplers;
+    for (int j = quarter * JQ + tid; j < (quarter + 1) * JQ; j += NT) {
+      K t = KeyTraits<K>::max_key();
+      uint8_t f = 0;
+      if (j < m1) {
+        const int r = (j + 1) * ResCfg<K>::O1;
+        const int d0 = r - 2 > 0 ? r - 2 : 0;
+        int i0 = merge_path_search<K>([&](int i) { return A0[i]; }, H1, [&](int i) { return A1[i]; }, H1, d0);
+        int i1 = d0 - i0;
+        K win[5];  // merged elements d0 .. d0+4 (A0 wins ties)
+#pragma unroll
+        for (int q = 0; q < 5; q++) {
+          const bool take0 = i1 >= H1 || (i0 < H1 && !(A1[i1] < A0[i0]));
+          win[q] = (i0 >= H1 && i1 >= H1) ? KeyTraits<K>::max_key() : (take0 ? A0[i0] : A1[i1]);
+          i0 += take0;
+          i1 += !take0;
+        }
+        const int k = r - d0;
+        t = win[k];
+        const bool m1e = k >= 1 && win[k - 1] == t, m2e = k >= 2 && win[k - 2] == t;
+        const bool p1e = r + 1 < S1 && win[k + 1] == t, p2e = r + 2 < S1 && win[k + 2] == t;
+        f = ((m1e && m2e) || (m1e && p1e) || (p1e && p2e)) ? 1 : 0;  // count > gamma = 2 (PAPER.md:168)
+      }
+      a.spl[j] = t;
+      a.spf[j] = f;
+    }
+    }
+    SR_RES_CSUB(3);
+    const bool skip3 = step(3 * kResSamplers);
+    if (quarter == 0 && !skip3) {  // one guide table (guide.cuh) for every CTA: built once, loaded in phase C
+      K* s_spl = sm.u.ct.stk[0];
+      uint8_t* s_eq = reinterpret_cast<uint8_t*>(sm.u.ct.stb[0]);
+      for (int j = tid; j < m1; j += NT) {
+        s_spl[j] = __ldcg(a.spl + j);
+        s_eq[j] = __ldcg(a.spf + j);
+      }
+      __syncthreads();
+      guide_build<K, NT>(s_spl, s_eq, m1, sm.v.guide1, sm.red);
+      const int4* gs = reinterpret_cast<const int4*>(&sm.v.guide1);
+      int4* gd = reinterpret_cast<int4*>(a.guide);
+      for (int i = tid; i < (int)(sizeof(sm.v.guide1) / 16); i += NT) gd[i] = gs[i];
+    }
   }
   SR_RES_STAMP(1);
   // samplers take the route CTA 0 publishes (one more arrival) instead of
@@ -840,96 +991,11 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     return;
   }
   if (route != kRoutePartition) return;  // MERGE / undecided: the host planner continues
-  const int m1 = a.B1 - 1;
-  if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
-    static_assert(kResSamplers == 4, "four sorted sample pieces");
-    // (sampler steps are counted in unit_counter[3]: CTA 0 zeroed it before
-    // publishing the route these CTAs waited for)
-    auto step = [&](uint32_t target) {  // publish this CTA's writes, wait for the other samplers'
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        atomicAdd(a.unit_counter + 3, 1u);
-        uint32_t v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.unit_counter + 3) : "memory");
-        } while (v < target);
-      }
-      __syncthreads();
-    };
-    step(kResSamplers);
-    SR_RES_CSUB(0);
-    {  // half h = quarter / 2 of the pairwise merges (pieces 2h, 2h+1), this sampler's
-       // part of it: merged positions [part R, (part + 1) R), written to mrg[h 2R + ...]
-      const int R = QS, h = quarter >> 1, part = quarter & 1;
-      for (int i = tid; i < 2 * R; i += NT) sp.q[i] = __ldcg(a.samp + (int64_t)h * 2 * R + i);
-      __syncthreads();
-      SR_RES_CSUB(1);
-      const K* A = sp.q;
-      const K* B = sp.q + R;
-      const int per = (R + NT - 1) / NT, d0 = part * R + tid * per, d1 = min(d0 + per, (part + 1) * R);
-      if (d0 < d1) {
-        int i = merge_path_search<K>([&](int x) { return A[x]; }, R, [&](int x) { return B[x]; }, R, d0);
-        int j = d0 - i;
-        for (int d = d0; d < d1; d++) {
-          const bool tA = j >= R || (i < R && !(B[j] < A[i]));
-          a.mrg[(int64_t)h * 2 * R + d] = tA ? A[i] : B[j];
-          i += tA;
-          j += !tA;
-        }
-      }
-    }
-    SR_RES_CSUB(4);
-    step(2 * kResSamplers);
-    SR_RES_CSUB(2);
-    // splitter j = element O1 (j+1) of the merged halves (DESIGN.md R9, R14),
-    // with its gamma flag (more than gamma = 2 of the elements r-2 .. r+2 equal
-    // to it, PAPER.md:168); this sampler's quarter of the j range, +inf padded
-    for (int i = tid; i < S1; i += NT) sp.q[i] = __ldcg(a.mrg + i);
-    __syncthreads();
-    const K* A0 = sp.q;
-    const K* A1 = sp.q + H1;
-    constexpr int JQ = B1MAX / kResSamplers;
-    for (int j = quarter * JQ + tid; j < (quarter + 1) * JQ; j += NT) {
-      K t = KeyTraits<K>::max_key();
-      uint8_t f = 0;
-      if (j < m1) {
-        const int r = (j + 1) * ResCfg<K>::O1;
-        const int d0 = r - 2 > 0 ? r - 2 : 0;
-        int i0 = merge_path_search<K>([&](int i) { return A0[i]; }, H1, [&](int i) { return A1[i]; }, H1, d0);
-        int i1 = d0 - i0;
-        K win[5];  // merged elements d0 .. d0+4 (A0 wins ties)
-#pragma unroll
-        for (int q = 0; q < 5; q++) {
-          const bool take0 = i1 >= H1 || (i0 < H1 && !(A1[i1] < A0[i0]));
-          win[q] = (i0 >= H1 && i1 >= H1) ? KeyTraits<K>::max_key() : (take0 ? A0[i0] : A1[i1]);
-          i0 += take0;
-          i1 += !take0;
-        }
-        const int k = r - d0;
-        t = win[k];
-        const bool m1e = k >= 1 && win[k - 1] == t, m2e = k >= 2 && win[k - 2] == t;
-        const bool p1e = r + 1 < S1 && win[k + 1] == t, p2e = r + 2 < S1 && win[k + 2] == t;
-        f = ((m1e && m2e) || (m1e && p1e) || (p1e && p2e)) ? 1 : 0;  // count > gamma = 2 (PAPER.md:168)
-      }
-      a.spl[j] = t;
-      a.spf[j] = f;
-    }
-    SR_RES_CSUB(3);
-  }
   grid.sync();
 
   // ================= C: splitter tree; tile-local bucket grouping =================
-  {  // the splitters (staged in the union's phase-C buffers) -> this CTA's guide table
-    K* s_spl = sm.u.ct.stk[0];
-    uint8_t* s_eq = reinterpret_cast<uint8_t*>(sm.u.ct.stb[0]);
-    for (int j = tid; j < m1; j += NT) {
-      s_spl[j] = __ldcg(a.spl + j);
-      s_eq[j] = __ldcg(a.spf + j);
-    }
-    __syncthreads();
-    guide_build<K, NT>(s_spl, s_eq, m1, sm.v.guide1, sm.red);
-  }
+  guide_load(a.guide, sm.v.guide1);  // (built once by sampler 0)
+  __syncthreads();
   SR_RES_STAMP(3);
   const int ngm = (c < PS && a.NG > c) ? (a.NG - 1 - c) / PS + 1 : 0;  // groups of this CTA: t = c + k PS, k < ngm <= GPC
   {

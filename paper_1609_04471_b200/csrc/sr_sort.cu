@@ -73,6 +73,7 @@ struct DevState {
   uint32_t done_seq = 0;
   uint32_t* arrive = nullptr;  // resident route-step arrival counter (device, zeroed once, never reset)
   uint32_t arrive_base = 0;
+  uint32_t scount_base = 0;    // the sampler-step counter (arrive + 16) before the next launch
   // resident scratch kept between calls: calls from this thread on this device
   // are ordered on the device (same stream: stream order; another stream: it
   // waits for last_ev), so the next call reuses the arena without a
@@ -1328,7 +1329,8 @@ struct Sorter {
                                     2 * r(S1 * kw) + r(ResCfg<K>::B1MAX * kw) + r(ResCfg<K>::B1MAX) + r(16 * n_ovf) +
                                     r(4 * ResCfg<K>::B1MAX) + r(G * (int64_t)sizeof(TileMM)) +
                                     r(4 * (int64_t)NG * nbins) + r(4 * (RO::OBMAX + 2)) +
-                                    (out_res ? r(4 * GO) + r(2 * GO * kw) + r(obk * RO::OCAP * kw) : 0) + 12 * 256);
+                                    (out_res ? r(4 * GO) + r(2 * GO * kw) + r(obk * RO::OCAP * kw) : 0) +
+                                    r(sizeof(GuideTab<K, 2048, ResCfg<K>::B1MAX>)) + 13 * 256);
       DevState& dsa = t_state.ds();
       if (dsa.has_last && dsa.last_stream != c.st)  // the arena of the last call is in use until its kernel ends
         check_cuda(cudaStreamWaitEvent(c.st, dsa.last_ev, 0), "cudaStreamWaitEvent");
@@ -1381,11 +1383,16 @@ struct Sorter {
       check_cuda(cudaMalloc((void**)&ts.arrive, 256), "cudaMalloc(arrive)");
       check_cuda(cudaMemset(ts.arrive, 0, 256), "cudaMemset(arrive)");
       ts.arrive_base = 0;
+      ts.scount_base = 0;
     }
     if (!ts.last_ev) check_cuda(cudaEventCreateWithFlags(&ts.last_ev, cudaEventDisableTiming), "cudaEventCreate");
     if (!ts.launch_ev) check_cuda(cudaEventCreateWithFlags(&ts.launch_ev, cudaEventDisableTiming), "cudaEventCreate");
     a.arrive = ts.arrive;
     a.arrive_base = ts.arrive_base;
+    a.scount = ts.arrive + 16;
+    a.scount_base = ts.scount_base;
+    a.guide = reinterpret_cast<GuideTab<K, 2048, ResCfg<K>::B1MAX>*>(
+        c.alloc<unsigned char>((int64_t)sizeof(GuideTab<K, 2048, ResCfg<K>::B1MAX>)));
     a.S1 = S1;
     a.B1 = B1;
     a.samp = c.alloc<K>(S1);
@@ -1418,6 +1425,7 @@ struct Sorter {
       check_cuda(launch_coop((const void*)k_resident<K>, P, kResNT, args, smem, c.st), "resident launch");
     });
     ts.arrive_base += (uint32_t)P + 1u;  // every CTA arrives once, CTA 0 once more (route published)
+    ts.scount_base += 3u * kResSamplers;  // the samplers' three steps
     check_cuda(cudaEventRecord(ts.last_ev, c.st), "cudaEventRecord");
     ts.last_stream = c.st;
     ts.has_last = true;
@@ -1442,8 +1450,8 @@ struct Sorter {
       {
         const unsigned long long* q = t + 8 + 8 * P + 16;
         if (q[0] && q[2])
-          fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
-                  (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
+          fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: gathered %.1f quarter sorted %.1f pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
+                  (q[5] - t[0]) * 1e-3, (q[6] - t[0]) * 1e-3, (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
       }
       {
         const unsigned long long* q = t + 8 + 8 * P + 40;
