@@ -54,12 +54,15 @@ _lib = None
 
 
 def lib():
-    """Load (building in-tree if the sources are newer) libsr_sort.so."""
+    """Load (building in-tree if the sources are newer) libsr_sort.so, or with
+    SR_CHECKED_LIB=1 the checked build libsr_sort_checked.so (device-side index
+    checks, build.py --checked)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.needs_build():
-            _build.build()
+        checked = os.environ.get("SR_CHECKED_LIB", "0") not in ("", "0")
+        path = _build.LIB_CHECKED if checked else _build.LIB
+        if _build.needs_build(checked):
+            _build.build(checked=checked)
         if not os.path.exists(path):
             raise ImportError(f"libsr_sort.so missing at {path}; run paper_1609_04471_b200/build.py")
         L = ctypes.CDLL(path)

@@ -8,6 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsr_sort.so")
+LIB_CHECKED = os.path.join(HERE, "libsr_sort_checked.so")  # -DSR_CHECKED: device-side index checks (SR_CHECK)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "sr_sort.h")
 
 NVCC_FLAGS = [
@@ -20,25 +21,29 @@ def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [HEADER])
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(checked: bool = False) -> bool:
+    lib = LIB_CHECKED if checked else LIB
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    if force or needs_build(checked):
         nvcc = os.environ.get("NVCC", "nvcc")
         if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
             nvcc = "/usr/local/cuda/bin/nvcc"
-        cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "sr_sort.cu")]
+        cmd = [nvcc, *NVCC_FLAGS, *(["-DSR_CHECKED=1"] if checked else []), "-o", lib + ".tmp",
+               os.path.join(CSRC, "sr_sort.cu")]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    print(build(force=True, verbose=True, checked="--checked" in sys.argv))

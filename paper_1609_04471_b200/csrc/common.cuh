@@ -2,11 +2,31 @@
 //
 // Nothing here is shared with oracle/ (the two share no code).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "sr_sort is written for sm_100a (B200) only"
+#endif
+
+// Checked build (build.py --checked: -DSR_CHECKED, libsr_sort_checked.so):
+// SR_CHECK asserts an index or range on the device and traps with its source
+// line on a violation (the pool does not allow compute-sanitizer; the checked
+// library runs the GPU test suite instead).  No code in the normal build.
+#ifdef SR_CHECKED
+#define SR_CHECK(cond)                                                              \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("[sr checked] %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                     \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define SR_CHECK(cond) \
+  do {                 \
+  } while (0)
 #endif
 
 namespace sr {

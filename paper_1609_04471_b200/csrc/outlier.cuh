@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(NT) k_outlier_split(const K* __restrict__ src,
   const uint32_t kbase = cnt[blockIdx.x];
   const uint32_t r = cnt[G];
   const int64_t obase = (int64_t)r + (t0 - kbase);
+  SR_CHECK((int64_t)kbase + tot <= r && obase + (len - tot) <= n);
   for (int i = tid; i < tot; i += NT) dst[kbase + i] = sm.sk[i];
   for (int i = tid; i < len - tot; i += NT) dst[obase + i] = sm.sk[tot + i];
   int b = 0;

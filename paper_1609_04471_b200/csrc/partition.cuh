@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K* __restrict__ src_k, con
       const int b = bi[i];
       if (b < NBMAX) {
         const int lp = sm.lstart[b] + sm.wcnt[w][b] + rk[i];
+        SR_CHECK(lp < (uint32_t)ST);
         sm.stk[lp] = x[i];
         sm.stb[lp] = (uint16_t)b;
         if (HAS_V) sm.stv[lp] = v[i];
@@ -835,6 +836,7 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
     for (int i = 0; i < VTS; i++) {
       if (bin[i] >= 0) {
         uint32_t lp = sm.lstart[bin[i]] + rk[i];
+        SR_CHECK(lp < (uint32_t)ST);
         sm.stk[lp] = x[i];
         sm.stb[lp] = (uint16_t)bin[i];
       }
@@ -843,6 +845,8 @@ __global__ void __launch_bounds__(NT) k_scatter_keys(const K* __restrict__ src, 
     const int tot = (int)sm.total;
     for (int p = tid; p < tot; p += NT) {
       int b = sm.stb[p];
+      SR_CHECK((int64_t)sm.base[b] + (p - (int)sm.lstart[b]) >= seg.start &&
+               (int64_t)sm.base[b] + (p - (int)sm.lstart[b]) < seg.start + seg.len);
       dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
     }
     __syncthreads();
@@ -943,6 +947,7 @@ __global__ void __launch_bounds__(NT, 2) k_scatter_keys2(const K* __restrict__ s
     for (int i = 0; i < VTS; i++) {
       if (bin[i] >= 0) {
         const uint32_t lp = sm.lstart[bin[i]] + rk[i];
+        SR_CHECK(lp < (uint32_t)ST);
         sm.stk[lp] = x[i];
         sm.stb[lp] = (uint16_t)bin[i];
       }
@@ -951,6 +956,8 @@ __global__ void __launch_bounds__(NT, 2) k_scatter_keys2(const K* __restrict__ s
     const int tot = (int)sm.total;
     for (int p = tid; p < tot; p += NT) {
       const int b = sm.stb[p];
+      SR_CHECK((int64_t)sm.base[b] + (p - (int)sm.lstart[b]) >= seg.start &&
+               (int64_t)sm.base[b] + (p - (int)sm.lstart[b]) < seg.start + seg.len);
       dst[(int64_t)sm.base[b] + (p - (int)sm.lstart[b])] = sm.stk[p];
     }
     __syncthreads();

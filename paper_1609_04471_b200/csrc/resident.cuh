@@ -410,6 +410,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
         }
       }
       __syncthreads();
+      SR_CHECK(t0 + len <= n);
       for (int i = tid; i < len; i += NT) a.ws[t0 + i] = os.sk[i];
       if (tid == 0) {
         a.okc[t] = (uint32_t)tot;
@@ -586,6 +587,7 @@ __device__ __forceinline__ void res_outlier(const ResArgs<K>& a, SM& sm) {
     // bucket j = R[g0, g0 + len) merged with its sorted outliers O[0, oc) (R
     // wins ties) into the staging area's last half, then copied
     // out coalesced
+    SR_CHECK((int64_t)g0 + obase[j] + len + oc <= n && oc <= OCAP && len <= OL);
     K* dst = a.keys + g0 + obase[j];
     K* O = stage + OL;
     K* out = stage + OL + OCAP;
@@ -677,6 +679,7 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
 #pragma unroll
   for (int u = 0; u < U; u++)
     if (bin[u] >= 0) {
+      SR_CHECK(bin[u] < nbins && lst[bin[u]] + rk[u] < (uint32_t)kResGrp);
       ct.stk[k][lst[bin[u]] + rk[u]] = x[u];
       ct.stb[k][lst[bin[u]] + rk[u]] = (uint16_t)bin[u];
     }
@@ -1066,6 +1069,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
         const int i = u * NT + tid;
         if (i < len) {
           const int b = ct.stb[k][i];
+          SR_CHECK(b < nbins && (int64_t)ct.cnt[b] + i - lst[b] < n);
           if (!(b & 1)) a.ws[ct.cnt[b] + (uint32_t)i - lst[b]] = ct.stk[k][i];
         }
       }
@@ -1181,6 +1185,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       }
       unsigned long long* prof = (a.tstamp && c == 0) ? a.tstamp + 8 + 8 * (size_t)P : nullptr;
       if (prof && tid == 0) { prof[5] += res_now() - tg0; prof[7] += 1; }
+      SR_CHECK((int64_t)s + len <= n && len <= SM::CAPB);
       unit_sort<K, SM::CAPB, NT>(a.keys + s, len, e);
       if (a.tstamp && tid == 0) {  // SR_TIMING: longest CTA unit, count
         unsigned long long* q = a.tstamp + 8 + 8 * (size_t)P + 24;
@@ -1213,6 +1218,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
         }
         const int s = (int)start[lo], len = (int)(start[lo + 1] - start[lo]);
         const int h0 = h ? NET : 0, hl = h ? len - NET : NET;
+        SR_CHECK((int64_t)s + len <= n && len <= WCAP && h0 + hl <= len);
         K* hw = a.ws + s + h0;
         for (int i = lane; i < hl; i += 32) stage[i] = __ldcg(hw + i);
         __syncwarp();
@@ -1255,6 +1261,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
         const K key = __ldcg(a.spl + (b - 1) / 2);
         const int f0 = (int)(v - up[b]) * kResWarpFill;
         const int f1 = f0 + kResWarpFill < len ? f0 + kResWarpFill : len;
+        SR_CHECK((int64_t)s + f1 <= n);
         for (int i = f0 + lane; i < f1; i += 32) a.keys[s + i] = key;
         continue;
       }
@@ -1278,6 +1285,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       int unsorted = 0;  // is_sorted
       for (int i = lane; i + 1 < len; i += 32) unsorted |= stage[i + 1] < stage[i];
       if (__any_sync(0xffffffffu, unsorted)) {
+        SR_CHECK((int64_t)s + len <= n && len <= WCAP);
         unit_warp_piece<K>(stage, len, a.keys + s);  // <= WCAP keys: one network, or two and a merge
       } else {
         for (int i = lane; i < len; i += 32) a.keys[s + i] = stage[i];

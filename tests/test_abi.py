@@ -36,6 +36,19 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(L, f)
 
 
+def test_checked_library_exports_and_checks():
+    """The checked build (-DSR_CHECKED: device-side SR_CHECK index asserts, the
+    stand-in for compute-sanitizer on this pool) exports the same symbols and
+    contains the trap the normal build does not."""
+    path = srbuild.build(checked=True)
+    out = subprocess.check_output(["nm", "-D", "--defined-only", path], text=True)
+    syms = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for f in _header_functions():
+        assert f in syms, f
+    traps = lambda p: subprocess.check_output(["cuobjdump", "-sass", p], text=True).count("BPT.TRAP")
+    assert traps(path) > traps(srbuild.build())
+
+
 def test_sass_is_sm100a():
     path = srbuild.build()
     out = subprocess.check_output(["cuobjdump", "--list-elf", path], text=True)
