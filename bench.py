@@ -62,6 +62,7 @@ WORKLOADS = {
     # double" and "random 16-list" classes at the Table 1 size
     "c2d": (2_000_000, np.float64, ["funiform", "fbits"], 1),
     "c2l16": (2_000_000, ("rec", 16), ["lrandom", "lprefix"], 1),
+    "c2l256": (200_000, ("rec", 256), ["lrandom", "lprefix"], 1),  # the paper's 256-int lists (1024 B)
     # report-only: the paper's Table 1 "nearly sorted" class is 256-distance
     # (PAPER.md:36, :84); configs[1](c) uses k-exchange instead
     "c2k": (2_000_000, np.int32, ["distance256"], 1),

@@ -2011,33 +2011,78 @@ void sort_records_impl(int32_t* recs, int64_t n, int words, cudaStream_t st) {
   uint32_t* flag = c.alloc<uint32_t>(n);
   const int64_t tiles = ceil_div<int64_t>(n, kScanNT * kScanIPT);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n, 256)));
-  c.launch("rec_init", n * (int64_t)words * 4 + n * 12, [&] {
-    k_rec_init<<<grid, 256, 0, c.st>>>(recs, n, words, kA, idx);
-  });
-  int launches = 0;
-  int rounds = 0;
-  for (int w = std::min(words, 2);; w++) {
+  // word ranges (one readback): field widths of the packed keys
+  std::vector<int32_t> mm0(2 * (size_t)words);
+  for (int j = 0; j < words; j++) {
+    mm0[2 * j] = INT32_MAX;
+    mm0[2 * j + 1] = INT32_MIN;
+  }
+  int32_t* d_mm = c.alloc<int32_t>(2 * (int64_t)words);
+  c.upload(d_mm, mm0);
+  {
+    const int bs = words <= 256 ? (256 / words) * words : words;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div<int64_t>(n * words, bs)));
+    c.launch("rec_minmax", n * (int64_t)words * 4, [&] { k_rec_minmax<<<g, bs, 0, c.st>>>(recs, n, words, d_mm); });
+  }
+  const int32_t* hmm = reinterpret_cast<const int32_t*>(c.readback(d_mm, 8 * (size_t)words));
+  std::vector<int> wl, wb;
+  std::vector<int32_t> wmin;
+  for (int j = 0; j < words; j++) {
+    const uint32_t range = (uint32_t)hmm[2 * j + 1] - (uint32_t)hmm[2 * j];
+    if (range == 0) continue;  // constant word: never decides
+    wl.push_back(j);
+    wmin.push_back(hmm[2 * j]);
+    wb.push_back(32 - __builtin_clz(range));
+  }
+  int launches = 0, rounds = 0;
+  size_t pos = 0;
+  int seg_bits = 0;
+  uint32_t* ex = nullptr;  // rounds >= 1: exclusive scan of the boundary flags
+  while (pos < wl.size()) {
+    RecRound rr{};
+    rr.seg_bits = seg_bits;
+    int used = seg_bits;
+    while (pos < wl.size() && rr.nw < 64 && used + wb[pos] <= 64) {
+      rr.wl[rr.nw] = wl[pos];
+      rr.wmin[rr.nw] = wmin[pos];
+      rr.wbits[rr.nw] = wb[pos];
+      used += wb[pos];
+      rr.nw++;
+      pos++;
+    }
+    rr.shift = 64 - used;
+    int64_t* kin = kA;
+    int64_t* kout = ex ? kB : kA;
+    c.launch("rec_key", n * (4 * (int64_t)rr.nw + 12), [&] {
+      k_rec_key<<<grid, 256, 0, c.st>>>(recs, n, words, rr, ex, kin, kout, idx);
+    });
+    if (ex) std::swap(kA, kB);
     {  // stable pair sort of (key, idx) on the integer path
       Ctx sc(st);
       Sorter<int64_t, true>(sc, kA, idx, n).run();
       launches += sc.plan.launches;
     }
     rounds++;
-    if (w >= words) break;
-    // control: scan status (zeroed) + the tie flag
+    if (pos >= wl.size()) break;
+    // control: tie flag + boundary count | scan status (zeroed)
     unsigned char* ctrl = c.alloc<unsigned char>(256 + 8 * tiles);
     c.memset0(ctrl, 256 + 8 * tiles);
-    uint32_t* any_tie = reinterpret_cast<uint32_t*>(ctrl);
+    uint32_t* ctl = reinterpret_cast<uint32_t*>(ctrl);
     int* tile_counter = reinterpret_cast<int*>(ctrl + 128);
     unsigned long long* status = reinterpret_cast<unsigned long long*>(ctrl + 256);
-    c.launch("rec_flags", n * 12, [&] { k_rec_flags<<<grid, 256, 0, c.st>>>(kA, n, flag, any_tie); });
-    const uint32_t tie = *reinterpret_cast<const uint32_t*>(c.readback(any_tie, 4));
-    if (!tie) break;  // every record is already in place
+    c.launch("rec_flags", n * 12, [&] { k_rec_flags<<<grid, 256, 0, c.st>>>(kA, n, flag, ctl); });
+    const uint32_t* h = reinterpret_cast<const uint32_t*>(c.readback(ctl, 8));
+    if (!h[0]) break;  // every record is already in place
+    seg_bits = h[1] ? 32 - __builtin_clz(h[1]) : 0;  // segment ids 0 .. boundaries
     c.launch("scan", n * 8, [&] {
       k_scan_u32<kScanNT, kScanIPT><<<(unsigned)tiles, kScanNT, 0, c.st>>>(flag, n, status, tile_counter, nullptr);
     });
-    c.launch("rec_next", n * 28, [&] { k_rec_next<<<grid, 256, 0, c.st>>>(recs, n, words, w, flag, kA, kB, idx); });
-    std::swap(kA, kB);
+    ex = flag;
+  }
+  if (rounds == 0) {  // every word constant: all records equal, input order kept
+    c.plan.levels = 0;
+    c.plan.route = SR_ROUTE_SORTED;
+    return;
   }
   int32_t* out = c.alloc<int32_t>(n * (int64_t)words);
   c.launch("rec_gather", 2 * n * (int64_t)words * 4, [&] {
