@@ -23,9 +23,10 @@
 //      return to the host planner.  PARTITION: splitter j = element O1 (j+1)
 //      of the merged halves (merge-path selection, R14) with its gamma flag
 //      (count > gamma = 2 in the sample) -> guide table; each
-//      held tile is classified (3-way ids) and counting-
-//      sorted by bucket in shared memory; its piece offset inside every bucket
-//      comes from one atomicAdd on the bucket total.
+//      held tile is classified (3-way ids) and its range
+//      keys counting-sorted by bucket in shared memory (equality keys are only
+//      counted); its piece offset inside every bucket comes from one atomicAdd
+//      on the bucket total.
 //   -- grid sync --
 //   D  bucket starts (exclusive scan of the totals, every CTA); every held
 //      key goes to start[b] + offset + rank in the workspace, so each bucket
@@ -662,7 +663,9 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
     for (int r = 0; r < BI; r++) {
       const int b = r * NT + tid;
       const uint32_t cb = b < nbins ? ct.cnt[b] : 0u;
-      if (b < nbins) lst[b] = cb;
+      // only range keys are placed (equality keys are never moved: their
+      // buckets are filled in phase E)
+      if (b < nbins) lst[b] = (b & 1) ? 0u : cb;
       // this group's piece of bucket b starts at offset goff inside the bucket
       // (pieces of different groups in arbitrary order: the bucket is sorted later)
       go[r] = cb ? atomicAdd(&tot[b], cb) : 0u;
@@ -671,14 +674,14 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
     for (int r = 0; r < BI; r++)
       if (r * NT + tid < nbins) goff_row[r * NT + tid] = go[r];
   }
-  if (tid == 0) lst[nbins] = (uint32_t)(t1 - t0);
   SR_RES_SUB(3);
   __syncthreads();
   smem_exclusive_sum_u32<NT>(lst, nbins, reinterpret_cast<uint32_t*>(sm.red));
+  if (tid == 0) lst[nbins] = lst[nbins - 1] + ct.cnt[nbins - 1];  // placed (range) keys; bin nbins-1 is a range bin
   SR_RES_SUB(4);
 #pragma unroll
   for (int u = 0; u < U; u++)
-    if (bin[u] >= 0) {
+    if (bin[u] >= 0 && !(bin[u] & 1)) {
       SR_CHECK(bin[u] < nbins && lst[bin[u]] + rk[u] < (uint32_t)kResGrp);
       ct.stk[k][lst[bin[u]] + rk[u]] = x[u];
       ct.stb[k][lst[bin[u]] + rk[u]] = (uint16_t)bin[u];
