@@ -198,7 +198,8 @@ enum {
                              §6.3); +1 level-1 buckets for n >= 2^26 (power of two <= 2048, default 512); +2 mean sub-bucket of
                              the fused level (16..4096, default 256); +3 cap on the level-1 buckets at
                              any n (power of two, 0 = none; tests reach the fused level at small n); +5 keys-only
-                             scatter by two 512-thread CTAs per SM (1, default) or one 1024-thread CTA (0); +6 mean bucket
+                             scatter by two 512-thread CTAs per SM (1), by them only where the level's bin tables are
+                             small and one 1024-thread CTA elsewhere (2, default), or one 1024-thread CTA (0); +6 mean bucket
                              of levels >= 2 (power of two; 0 = default: 512 int32 / 256 int64) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */

@@ -52,7 +52,7 @@ int64_t g_ws_limit = 0;  // SR_OPT_WS_LIMIT (fault injection), 0 = none
 //   [0] fused level 2 (k_bucket_sort) on/off   [1] level-1 buckets for n >= kBigLevel1
 //   [2] mean sub-bucket the fused level aims for   [3] cap on the level-1 buckets at any n (0 = none; tests)
 //   [4] k_bucket_sort phase skips (timing experiments only; the output is then NOT sorted): 1 finishing, 2 scatter
-int64_t g_tune[8] = {0, 512, 256, 0, 0, 1, 0, 0};
+int64_t g_tune[8] = {0, 512, 256, 0, 0, 2, 0, 0};
 #ifndef SR_WARP_VT64
 #define SR_WARP_VT64 1
 #endif
@@ -819,12 +819,14 @@ struct Sorter {
     for (auto& s : L.segs) keys_in += s.len;
     const int64_t noneq = hs ? hs->noneq_total : keys_in;
     const DevStats* gate = hs ? nullptr : L.d_st;
-    if (!HAS_V && g_tune[5] && L.d_bins) {  // (A/B: two 512-thread CTAs per SM)
+    const bool small = L.total_bins <= 1025 * (int64_t)L.segs.size() && [&] {
+      for (auto& sd : L.segs) if (sd.nbins > 1025) return false;
+      return true;
+    }();
+    // (A/B: 1 = two 512-thread CTAs per SM at every level, 2 = only where the
+    // bin tables are small, 0 = one 1024-thread CTA per SM)
+    if (!HAS_V && L.d_bins && (g_tune[5] == 1 || (g_tune[5] == 2 && small))) {
       constexpr int VT2 = sizeof(K) == 4 ? 16 : 8;
-      const bool small = L.total_bins <= 1025 * (int64_t)L.segs.size() && [&] {
-        for (auto& sd : L.segs) if (sd.nbins > 1025) return false;
-        return true;
-      }();
       auto launch2 = [&](auto kern, size_t smem) {
         set_smem(kern, smem);
         return c.launch("scatter", keys_in * kw + noneq * kw, [&] {

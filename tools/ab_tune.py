@@ -15,7 +15,7 @@ sr.generate(src, order, seed=12345, param=int(os.environ.get("GEN_PARAM", "0")))
 work = torch.empty_like(src)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 ref = None
-DEF = {0: 0, 1: 512, 2: 256, 3: 0, 4: 0, 5: 1, 6: 0, 7: 0}
+DEF = {0: 0, 1: 512, 2: 256, 3: 0, 4: 0, 5: 2, 6: 0, 7: 0}
 for st in settings:
     kv = dict(DEF)
     for p in filter(None, st.split(",")):
