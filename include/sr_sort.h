@@ -200,7 +200,10 @@ enum {
                              any n (power of two, 0 = none; tests reach the fused level at small n); +5 keys-only
                              scatter by two 512-thread CTAs per SM (1), by them only where the level's bin tables are
                              small and one 1024-thread CTA elsewhere (2, default), or one 1024-thread CTA (0); +6 mean bucket
-                             of levels >= 2 (power of two; 0 = default: 512 int32 / 256 int64) */
+                             of levels >= 2 (power of two; 0 = default: 512 int32 / 256 int64); +7 keys-only
+                             warp finishing below level 1: 0 (default) items <= 256 by the 8-key network and
+                             (256, 512] / (512, 1024] as two 8- / 16-key networks and a merge, 2 only the latter
+                             split, 1 the 16- and 32-key networks (no split) */
 };
 /* Process-global, not thread-safe.  SR_ERR_INVALID_ARGUMENT for unknown keys/values. */
 int32_t sr_set_option(int32_t key, int64_t value);

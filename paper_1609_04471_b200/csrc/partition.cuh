@@ -24,6 +24,7 @@
 #include "guide.cuh"
 #include "presort.cuh"
 #include "types.cuh"
+#include "unit_sort.cuh"
 
 namespace sr {
 
@@ -1021,6 +1022,57 @@ __global__ void __launch_bounds__(32 * WARPS) k_finish_warp(const Item* __restri
     }
     if (unsorted || from_ws) {
       __syncwarp();
+      for (int i = lane; i < len; i += 32) dk[i] = ks[i];
+    }
+    __syncwarp();
+  }
+}
+
+// K11w2 (keys only): items of (min_len, 64 VH] keys as two halves sorted by the
+// VH-key-per-lane network and one warp merge-path merge straight into the
+// caller's keys (A = the first half wins ties).  Against one
+// 2 VH network: fewer instructions per key and half the registers (the wide
+// network's 128 registers held the SM at 16 warps).
+template <typename K, int VH, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_finish_warp_split(const Item* __restrict__ items,
+                                                                   const int64_t* __restrict__ count_ptr,
+                                                                   K* __restrict__ keys, const K* __restrict__ ws_k,
+                                                                   const DevStats* __restrict__ gate, int64_t gate_route,
+                                                                   int min_len) {
+  if (gate && gate->route != gate_route) return;  // speculative launch on another route
+  constexpr int H = 32 * VH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  K* ks = reinterpret_cast<K*>(smem_raw) + w * 2 * H;
+  const int64_t count = *count_ptr;
+  for (int64_t it = (int64_t)blockIdx.x * WARPS + w; it < count; it += (int64_t)gridDim.x * WARPS) {
+    const Item item = items[it];
+    if ((item.kind & 0xf) == kItemFill) continue;  // (fills: the 16-key launch)
+    const int len = item.len;
+    if (len <= min_len || len > 2 * H) continue;
+    const bool from_ws = (item.kind >> 4) & 1;
+    const int64_t s = item.start;
+    K* dk = keys + s;
+    const K* sk = (from_ws ? ws_k : keys) + s;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {  // striped, coalesced loads, VH in flight per half
+      K x[VH];
+#pragma unroll
+      for (int r = 0; r < VH; r++) {
+        const int i = h * H + r * 32 + lane;
+        x[r] = i < len ? sk[i] : KeyTraits<K>::max_key();
+      }
+#pragma unroll
+      for (int r = 0; r < VH; r++) ks[h * H + r * 32 + lane] = x[r];
+    }
+    __syncwarp();
+    int unsorted = 0;
+    for (int i = lane; i + 1 < len; i += 32) unsorted |= ks[i + 1] < ks[i];
+    if (__any_sync(0xffffffffu, unsorted)) {
+      WarpBitonic<K, VH>::sort(ks, H);
+      WarpBitonic<K, VH>::sort(ks + H, len - H);
+      unit_warp_merge<K>(ks, H, ks + H, len - H, dk);
+    } else if (from_ws) {
       for (int i = lane; i < len; i += 32) dk[i] = ks[i];
     }
     __syncwarp();

@@ -656,6 +656,7 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
   SR_RES_SUB(2);
   __syncthreads();
   uint32_t* lst = ct.lst[k];
+  int ranged = 0;  // any range key in this group (else nothing is placed: no scan)
   {  // unrolled: all of a thread's atomics in flight together
     constexpr int BI = (SM::NB1 + NT - 1) / NT;
     uint32_t go[BI];
@@ -666,6 +667,7 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
       // only range keys are placed (equality keys are never moved: their
       // buckets are filled in phase E)
       if (b < nbins) lst[b] = (b & 1) ? 0u : cb;
+      ranged |= !(b & 1) && cb;
       // this group's piece of bucket b starts at offset goff inside the bucket
       // (pieces of different groups in arbitrary order: the bucket is sorted later)
       go[r] = cb ? atomicAdd(&tot[b], cb) : 0u;
@@ -675,9 +677,12 @@ __device__ __noinline__ void res_group(const ResArgs<K>& a, SM& sm, const K* __r
       if (r * NT + tid < nbins) goff_row[r * NT + tid] = go[r];
   }
   SR_RES_SUB(3);
-  __syncthreads();
-  smem_exclusive_sum_u32<NT>(lst, nbins, reinterpret_cast<uint32_t*>(sm.red));
-  if (tid == 0) lst[nbins] = lst[nbins - 1] + ct.cnt[nbins - 1];  // placed (range) keys; bin nbins-1 is a range bin
+  if (__syncthreads_or(ranged)) {
+    smem_exclusive_sum_u32<NT>(lst, nbins, reinterpret_cast<uint32_t*>(sm.red));
+    if (tid == 0) lst[nbins] = lst[nbins - 1] + ct.cnt[nbins - 1];  // placed (range) keys; bin nbins-1 is a range bin
+  } else if (tid == 0) {
+    lst[nbins] = 0;  // every key of the group is in an equality bucket (few-unique inputs)
+  }
   SR_RES_SUB(4);
 #pragma unroll
   for (int u = 0; u < U; u++)
@@ -1053,6 +1058,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     typename SM::CT& ct = sm.u.ct;
     for (int k = 0; k < ngm; k++) {
       const int t = c + k * PS;
+      if (ct.lst[k][nbins] == 0) continue;  // nothing placed (every key in an equality bucket)
       {
         constexpr int BI = (SM::NB1 + NT - 1) / NT;
         uint32_t go[BI];

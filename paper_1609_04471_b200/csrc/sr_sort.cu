@@ -890,12 +890,48 @@ struct Sorter {
   // keys only: two launches over the small item list, by size class -- items
   // <= 512 keys (and fills) with the 16-key-per-lane network, larger ones with
   // the widest network the level allows
+  // (min_len, 64 VH] keys: two VH-key-per-lane networks + a merge (k_finish_warp_split)
+  template <int VH>
+  void finish_split(Level& L, int64_t max_items, const DevStats* gate, int min_len) {
+    constexpr int W = kWarpItemsPerCta;
+    auto kern = k_finish_warp_split<K, VH, W>;
+    const size_t smem = sizeof(K) * 2 * 32 * VH * W;
+    set_smem(kern, smem);
+    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(max_items, W), gate ? 148 * 6 : 148 * 32);
+    K* kk = keys;
+    const K* wkk = wk;
+    const int64_t* cnt = &L.d_st->n_items;
+    c.launch("finish_small", 0, [&] {
+      kern<<<grid, 32 * W, smem, c.st>>>(L.d_items, cnt, kk, wkk, gate, kRoutePartition, min_len);
+    });
+  }
+  // keys only: launches over the small item list by size class.  Level 1
+  // (64 keys per lane allowed): items <= 512 keys (and fills) with the
+  // 16-key-per-lane network, larger ones with the 64-key network.  Deeper
+  // levels: items <= 256 (and fills) with the 8-key network, (256, 512] and
+  // (512, 1024] as two 8- / 16-key networks and a merge (SR_OPT_TUNE+7 = 1:
+  // 16- and 32-key networks instead, measured slower: C5a 7.67 -> 7.43 ms)
   int finish_small(Level& L, int64_t max_items, int64_t bytes, const DevStats* gate) {
     if (HAS_V) return finish<kFinSmallNT>(L.d_items, &L.d_st->n_items, 0, max_items, bytes, gate, kRoutePartition);
     if (max_items <= 0) return -1;
-    const int h = finish_warp<16>(L, max_items, bytes, gate, 0, 1, 148 * 64);
-    if (L.warp_vt == 64 && sizeof(K) == 4) finish_warp<64>(L, max_items, 0, gate, 512, 0, 148 * 16);
-    else finish_warp<32>(L, max_items, 0, gate, 512, 0, 148 * 16);
+    if (L.warp_vt == 64 && sizeof(K) == 4) {
+      const int h = finish_warp<16>(L, max_items, bytes, gate, 0, 1, 148 * 64);
+      finish_warp<64>(L, max_items, 0, gate, 512, 0, 148 * 16);
+      return h;
+    }
+    if (g_tune[7] == 1) {
+      const int h = finish_warp<16>(L, max_items, bytes, gate, 0, 1, 148 * 64);
+      finish_warp<32>(L, max_items, 0, gate, 512, 0, 148 * 16);
+      return h;
+    }
+    if (g_tune[7] == 2) {  // (the split for (512, 1024] only)
+      const int h = finish_warp<16>(L, max_items, bytes, gate, 0, 1, 148 * 64);
+      finish_split<16>(L, max_items, gate, 512);
+      return h;
+    }
+    const int h = finish_warp<8>(L, max_items, bytes, gate, 0, 1, 148 * 64);
+    finish_split<8>(L, max_items, gate, 256);
+    finish_split<16>(L, max_items, gate, 512);
     return h;
   }
 
