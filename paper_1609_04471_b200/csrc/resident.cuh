@@ -106,8 +106,8 @@ constexpr int64_t kResMaxN = ResCfg<int32_t>::MAXN;  // largest resident n over 
 template <typename K>
 struct ResOut {
   static constexpr int TO = sizeof(K) == 4 ? 8192 : 4096;  // OA tile
-  static constexpr int OL = ResCfg<K>::WCAP / 4;           // kept keys per bucket
-  static constexpr int OCAP = ResCfg<K>::WCAP / 4;         // outliers per bucket (one warp network)
+  static constexpr int OL = ResCfg<K>::WCAP * 3 / 8;       // kept keys per bucket
+  static constexpr int OCAP = ResCfg<K>::WCAP / 8;         // outliers per bucket (one warp network)
   static_assert(OL + OCAP + OL + OCAP <= ResCfg<K>::WCAP, "R, O and the merged bucket fit one warp's staging");
   static constexpr int OBMAX = 2 * ResCfg<K>::B1MAX;       // buckets (their starts live in ResSmem::start)
   static constexpr int MAXG = (int)(ResCfg<K>::MAXN / TO);

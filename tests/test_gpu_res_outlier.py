@@ -17,8 +17,8 @@ from workloads import gen
 pytestmark = pytest.mark.gpu
 
 TO32 = 8192  # ResOut<int32_t>::TO (outlier tile)
-OCAP32 = 512  # ResOut<int32_t>::OCAP (outliers per bucket)
-MAXN32, MAXN64 = 512 * 4096, 256 * 2048  # ResOut<K>::MAXN (the route's n range)
+OCAP32 = 256  # ResOut<int32_t>::OCAP (outliers per bucket)
+MAXN32, MAXN64 = 768 * 4096, 384 * 2048  # ResOut<K>::MAXN (the route's n range)
 
 
 @pytest.fixture(autouse=True)
