@@ -338,7 +338,7 @@ __device__ __forceinline__ void tile_mm_init(K* smn, K* smx, int nsub) {
   }
 }
 template <typename K>
-__device__ __forceinline__ void tile_mm_finish(const K* smn, const K* smx, int nsub, int valid, TileMM* out) {
+__device__ __forceinline__ int tile_mm_finish(const K* smn, const K* smx, int nsub, int valid, TileMM* out) {
   int bad = !valid;
   for (int q = threadIdx.x; q + 2 < nsub; q += blockDim.x) bad |= smx[q] > smn[q + 2];
   bad = __syncthreads_or(bad);
@@ -352,6 +352,7 @@ __device__ __forceinline__ void tile_mm_finish(const K* smn, const K* smx, int n
     t.nsub = nsub;
     *out = t;
   }
+  return !bad;  // (every thread)
 }
 
 // K1: one CTA per tile of `tile` keys.  STRICT selects the descending-run
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(NT) k_presort_scan(const K* __restrict__ keys,
   cv = block_reduce_sum<NT>(cv, s_red);
   if (tid == 0) {
     TileSummary s;
-    s.ndesc = cd; s.nab = ca; s.fdesc = fd; s.ldesc = ld; s.fab = fa; s.lab = la; s.nviol = cv; s.pad1 = 0;
+    s.ndesc = cd; s.nab = ca; s.fdesc = fd; s.ldesc = ld; s.fab = fa; s.lab = la; s.nviol = cv; s.tok = 0;
     sums[blockIdx.x] = s;
   }
   if (FUSE) {
@@ -520,7 +521,7 @@ __device__ __forceinline__ int64_t presort_resolve_block(const K* __restrict__ k
     if (t < G) {
       const int4* p = reinterpret_cast<const int4*>(sums + t);
       int4 a = __ldcg(p), b = __ldcg(p + 1);
-      s.ndesc = a.x; s.nab = a.y; s.fdesc = a.z; s.ldesc = a.w; s.fab = b.x; s.lab = b.y; s.nviol = b.z; s.pad1 = 0;
+      s.ndesc = a.x; s.nab = a.y; s.fdesc = a.z; s.ldesc = a.w; s.fab = b.x; s.lab = b.y; s.nviol = b.z; s.tok = 0;
     } else { s.ndesc = 0; s.nab = 0; s.fdesc = 0; s.ldesc = -1; s.fab = 0; s.lab = -1; s.nviol = 0; }
     D += s.ndesc;
     A += s.nab;
@@ -721,11 +722,22 @@ __device__ int64_t presort_resolve_warp(const K* __restrict__ keys, int64_t n, c
     ndsc++;
     covD += lastLenD;
   }
-  int dok = mm != nullptr;
-  if (mm)
-    for (int t = t0; t < t1; t++) dok &= tile_mm_pair_ok(mm, t, G);
-  dok = __all_sync(0xffffffffu, dok);
-  const int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok, dok);
+  // the k-distance test only where it can change the route (every route before
+  // it in resolve_route is independent of dist_ok); the tiles' own verdicts are
+  // in ts[t].tok, so the straddle pairs in global memory are read only when
+  // every tile passed
+  int64_t route = resolve_route(n, D, A, V, covA, covD, force, merge_ok, 0);
+  int dok = 0;
+  if (mm && (merge_ok & kAllowDistance) && (route == kRoutePartition || route == kRouteUndecided)) {
+    dok = 1;
+    for (int t = t0; t < t1; t++) dok &= ts[t].tok != 0;
+    dok = __all_sync(0xffffffffu, dok);
+    if (dok) {
+      for (int t = t0; t < t1; t++) dok &= tile_mm_pair_ok(mm, t, G);
+      dok = __all_sync(0xffffffffu, dok);
+    }
+    if (dok) route = resolve_route(n, D, A, V, covA, covD, force, merge_ok, dok);
+  }
   if (WRITE && lane == 0) {
     st->dist_ok = dok;
     st->n = n;

@@ -790,6 +790,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       sm.agg[w][6] = cv;
     }
     __syncthreads();
+    // (tile_mm_finish's barrier orders the agg writes above and the next tile's init)
+    const int tok = tile_mm_finish<K>(mmn, mmx, nsub, vec ? 1 : 0, a.mm + t);
     if (tid == 0) {
       for (int v = 1; v < kResWarps; v++) {
         cd += sm.agg[v][0]; ca += sm.agg[v][1];
@@ -797,10 +799,9 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
         cv += sm.agg[v][6];
       }
       TileSummary ts;
-      ts.ndesc = cd; ts.nab = ca; ts.fdesc = fd; ts.ldesc = ld; ts.fab = fa; ts.lab = la; ts.nviol = cv; ts.pad1 = 0;
+      ts.ndesc = cd; ts.nab = ca; ts.fdesc = fd; ts.ldesc = ld; ts.fab = fa; ts.lab = la; ts.nviol = cv; ts.tok = tok;
       a.sums[t] = ts;
     }
-    tile_mm_finish<K>(mmn, mmx, nsub, vec ? 1 : 0, a.mm + t);  // (its barrier orders the next tile's init)
     __syncthreads();
   }
   SR_RES_STAMP(0);
@@ -932,6 +933,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       const int4* gs = reinterpret_cast<const int4*>(&sm.v.guide1);
       int4* gd = reinterpret_cast<int4*>(a.guide);
       for (int i = tid; i < (int)(sizeof(sm.v.guide1) / 16); i += NT) gd[i] = gs[i];
+      SR_RES_CSUB(7);
     }
   }
   SR_RES_STAMP(1);
@@ -953,6 +955,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     for (int i = tid; i < 2 * a.G; i += NT) dst[i] = __ldcg(src + i);
   }
   __syncthreads();
+  if (a.tstamp && c == 0 && tid == 0) a.tstamp[8 + 8 * (size_t)P + 32] = res_now();
   __shared__ int64_t s_route;
   if (sampler) {
     if (tid == 0) s_route = __ldcg(reinterpret_cast<const long long*>(&a.st->route));
@@ -961,6 +964,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
                                                              a.force, a.merge_ok, a.mm)
                              : presort_resolve_warp<K, false>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
                                                               a.force, a.merge_ok, a.mm);
+    if (a.tstamp && c == 0 && lane == 0) a.tstamp[8 + 8 * (size_t)P + 33] = res_now();
     if (lane == 0) {
       s_route = r;
       if (c == 0) {  // the route is in a.st: tell the samplers

@@ -1486,10 +1486,16 @@ struct Sorter {
                   (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3, (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3);
       }
       {
+        if (t[8 + 8 * P + 33])
+          fprintf(stderr, "[sr_resident] route step of CTA 0, us since start: all arrived %.1f summaries loaded %.1f resolved %.1f\n",
+                  (t[1] - t[0]) * 1e-3, (t[8 + 8 * P + 32] - t[0]) * 1e-3, (t[8 + 8 * P + 33] - t[0]) * 1e-3);
+      }
+      {
         const unsigned long long* q = t + 8 + 8 * P + 16;
         if (q[0] && q[2])
-          fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: gathered %.1f quarter sorted %.1f pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f\n",
-                  (q[5] - t[0]) * 1e-3, (q[6] - t[0]) * 1e-3, (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3);
+          fprintf(stderr, "[sr_resident] C splitters (sampler 0) us since start: gathered %.1f quarter sorted %.1f pieces sorted %.1f loaded %.1f half merged %.1f merged %.1f selected %.1f guide %.1f\n",
+                  (q[5] - t[0]) * 1e-3, (q[6] - t[0]) * 1e-3, (q[0] - t[0]) * 1e-3, (q[1] - t[0]) * 1e-3, (q[4] - t[0]) * 1e-3, (q[2] - t[0]) * 1e-3, (q[3] - t[0]) * 1e-3,
+                  q[7] ? (q[7] - t[0]) * 1e-3 : 0.0);
       }
       {
         const unsigned long long* q = t + 8 + 8 * P + 40;

@@ -12,7 +12,7 @@ struct TileSummary {
   int32_t fdesc, ldesc;
   int32_t fab, lab;
   int32_t nviol;   // descents whose outer neighbours are out of order (outlier route choice)
-  int32_t pad1;
+  int32_t tok;     // resident path: the tile passed its own k-distance test (TileMM.ok); 0 elsewhere
 };
 
 // Bounded-displacement summary of one presort tile (the k-distance route,

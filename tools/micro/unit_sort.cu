@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(512, 1) k_units(const int* src, int* dst, int 
       const int s = u * L, len = min(L, n - s);
       for (int p = w * 256; p < len; p += 16 * 256) warp_copy_vec(src + s + p, e.x + p, min(256, len - p));
       __syncthreads();
-      res_bucket_sort2<int, 512>(dst + s, len, e);
+      unit_sort<int, 16384, 512>(dst + s, len, e);
       __syncthreads();
     }
   } else {
@@ -73,13 +73,8 @@ __global__ void __launch_bounds__(512, 1) k_units(const int* src, int* dst, int 
         warp_copy_vec(src + s, stage, len);
       }
       __syncwarp();
-      if (MODE != 3) res_warp_sort<int, 2048>(stage, len);
-      __syncwarp();
-      if (MODE == 1) {
-        for (int i = lane; i < len; i += 32) dst[s + i] = stage[i];
-      } else {
-        warp_copy_vec(stage, dst + s, len);
-      }
+      if (MODE != 3) unit_warp_piece<int>(stage, len, dst + s);  // sorted into dst
+      else warp_copy_vec(stage, dst + s, len);
       __syncwarp();
     }
   }
