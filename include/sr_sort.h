@@ -126,6 +126,25 @@ int32_t sr_sort_pairs(void *keys, void *vals, int64_t n, int32_t dtype, void *st
  */
 int32_t sr_sort_host(void *host_keys, void *host_vals, int64_t n, int32_t dtype, void *stream);
 
+/* A batch of `count` independent sorts with HOST buffers -- the paper's
+ * procedure sorts many instances of one size back to back (100 per input
+ * class).  Instance i is host_keys[i][0..n[i]) (and, when
+ * host_vals and host_vals[i] are not NULL, the 4-byte payloads host_vals[i]:
+ * a stable pair sort); each is sorted in place exactly as sr_sort_host would.
+ * The instances are pipelined over a ring of four device buffers and two copy
+ * streams of the library beside `stream`: the upload of instance i+1 and the
+ * download of instance i-1 overlap the sort of instance i (PCIe is full
+ * duplex; the copies use the copy engines, not the SMs).  Pinned host
+ * buffers are needed for the overlap (pageable ones are staged by the driver
+ * and serialise).  The call starts after earlier work on `stream` and
+ * synchronises it before returning; host buffers must not overlap.  Scratch: 4
+ * buffers of max(n) keys (+ payloads) from the device pool, beside each
+ * sort's own.  Errors as for sr_sort_host; on an error the batch stops,
+ * instances already downloaded are sorted, the others are unspecified (each
+ * still a permutation of its input or untouched). */
+int32_t sr_sort_host_batch(void *const *host_keys, void *const *host_vals, const int64_t *n, int32_t count,
+                           int32_t dtype, void *stream);
+
 /* Record keys (the paper's "random 16-/64-/256-list"
  * classes, Table 2): recs holds n records of
  * `words` (1..1024) consecutive signed int32 values (row-major, 4-byte

@@ -25,7 +25,7 @@ OPT_DISTANCE_ROUTE = 7
 OPT_TUNE = 16  # + 0 fused second level, + 1 level-1 buckets (n >= 2^26), + 2 fused mean sub-bucket
 
 EXPORTS = [
-    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",
+    "sr_sort_keys", "sr_sort_pairs", "sr_sort_host", "sr_sort_host_batch", "sr_sort_records", "sr_presortedness", "sr_last_plan", "sr_status_string", "sr_last_error",
     "sr_set_option", "sr_last_profile", "sr_presort_scan", "sr_reverse_range", "sr_tile_sort", "sr_merge_path",
     "sr_merge", "sr_splitters", "sr_partition_level", "sr_generate",
 ]
@@ -70,6 +70,7 @@ def lib():
         L.sr_sort_keys.argtypes = [vp, i64, i32, vp]
         L.sr_sort_pairs.argtypes = [vp, vp, i64, i32, vp]
         L.sr_sort_host.argtypes = [vp, vp, i64, i32, vp]
+        L.sr_sort_host_batch.argtypes = [vp, vp, vp, i32, i32, vp]
         L.sr_sort_records.argtypes = [vp, i64, i32, vp]
         L.sr_presortedness.argtypes = [vp, i64, i32, ctypes.POINTER(Measures), vp]
         L.sr_last_plan.argtypes = [ctypes.POINTER(Plan)]
@@ -195,6 +196,26 @@ def sort_host(keys: np.ndarray, vals: np.ndarray | None = None, stream: int = 0)
     assert keys.flags.c_contiguous and (vals is None or (vals.flags.c_contiguous and vals.itemsize == 4))
     vp = None if vals is None else vals.ctypes.data_as(ctypes.c_void_p)
     _check(lib().sr_sort_host(keys.ctypes.data_as(ctypes.c_void_p), vp, keys.size, code, ctypes.c_void_p(stream)))
+    return keys if vals is None else (keys, vals)
+
+
+def sort_host_batch(keys: list, vals: list | None = None, stream: int = 0):
+    """End-to-end sort of a batch of HOST numpy arrays of one dtype in place,
+    uploads and downloads overlapped with the sorts (sr_sort_host_batch)."""
+    codes = {np.dtype(np.int32): SR_INT32, np.dtype(np.int64): SR_INT64,
+             np.dtype(np.float32): SR_FLOAT32, np.dtype(np.float64): SR_FLOAT64}
+    count = len(keys)
+    if count == 0:
+        return keys
+    if keys[0].dtype not in codes or any(k.dtype != keys[0].dtype for k in keys):
+        raise TypeError("keys must all be int32, int64, float32 or float64 arrays of one dtype")
+    assert all(k.flags.c_contiguous for k in keys)
+    assert vals is None or (len(vals) == count and all(
+        v is None or (v.flags.c_contiguous and v.itemsize == 4 and v.size == k.size) for k, v in zip(keys, vals)))
+    kp = (ctypes.c_void_p * count)(*[k.ctypes.data for k in keys])
+    vp = None if vals is None else (ctypes.c_void_p * count)(*[None if v is None else v.ctypes.data for v in vals])
+    ns = (ctypes.c_int64 * count)(*[k.size for k in keys])
+    _check(lib().sr_sort_host_batch(kp, vp, ns, count, codes[keys[0].dtype], ctypes.c_void_p(stream)))
     return keys if vals is None else (keys, vals)
 
 

@@ -84,6 +84,8 @@ struct DevState {
   cudaStream_t last_stream = nullptr;
   bool has_last = false;
   cudaEvent_t launch_ev = nullptr;     // recorded before each resident launch (watchdog start)
+  // sr_sort_host_batch: the two copy streams (host->device, device->host) beside the caller's stream
+  cudaStream_t batch_h2d = nullptr, batch_d2h = nullptr;
   // the resident kernel as a cooperative node of an instantiated one-node CUDA
   // graph, its parameters replaced per call: cudaGraphExecKernelNodeSetParams +
   // cudaGraphLaunch take ~3.5 us less host time than cudaLaunchCooperativeKernel
@@ -109,6 +111,8 @@ struct DevState {
     has_last = false;
   }
   ~DevState() {
+    if (batch_h2d) cudaStreamDestroy(batch_h2d);
+    if (batch_d2h) cudaStreamDestroy(batch_d2h);
     for (auto& cg : coop) {
       if (cg.ge) cudaGraphExecDestroy(cg.ge);
       if (cg.g) cudaGraphDestroy(cg.g);
@@ -2222,6 +2226,109 @@ int32_t sr_sort_host(void* host_keys, void* host_vals, int64_t n, int32_t dtype,
   if (dv) cudaFreeAsync(dv, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (rc == SR_OK && e != cudaSuccess) {
+    t_state.err = cudaGetErrorString(e);
+    rc = SR_ERR_CUDA;
+  }
+  return rc;
+}
+
+int32_t sr_sort_host_batch(void* const* host_keys, void* const* host_vals, const int64_t* n, int32_t count,
+                           int32_t dtype, void* stream) {
+  t_state.err.clear();
+  if (count < 0 || (count > 0 && (!host_keys || !n))) return SR_ERR_INVALID_ARGUMENT;
+  if (!dtype_ok(dtype)) return SR_ERR_UNSUPPORTED_DTYPE;
+  int64_t nmax = 0;
+  for (int i = 0; i < count; ++i) {
+    if (n[i] < 0 || (n[i] >= 2 && !host_keys[i])) return SR_ERR_INVALID_ARGUMENT;
+    if (n[i] > INT32_MAX) return SR_ERR_SIZE;
+    nmax = std::max(nmax, n[i]);
+  }
+  if (nmax <= 1) return SR_OK;
+  const int64_t kw = key_bytes(dtype);
+  cudaStream_t st = (cudaStream_t)stream;
+  // ring of R device buffers: instance i lives in slot i % R from its upload to the end of its download
+  constexpr int kRing = 4;
+  const int R = std::min<int>(count, kRing);
+  void *dk[kRing] = {}, *dv[kRing] = {};
+  std::vector<cudaEvent_t> up(count, nullptr), sorted(count, nullptr), down(count, nullptr);
+  bool pairs = false;
+  for (int i = 0; host_vals && i < count; ++i) pairs = pairs || (host_vals[i] && n[i] >= 2);
+  int next_up = 0;  // instances [0, next_up) have their upload enqueued
+  cudaStream_t sh = nullptr, sd = nullptr;
+  int32_t rc = guarded([&] {
+    DevState& ds = t_state.ds();
+    if (!ds.batch_h2d) check_cuda(cudaStreamCreateWithFlags(&ds.batch_h2d, cudaStreamNonBlocking), "stream");
+    if (!ds.batch_d2h) check_cuda(cudaStreamCreateWithFlags(&ds.batch_d2h, cudaStreamNonBlocking), "stream");
+    sh = ds.batch_h2d;
+    sd = ds.batch_d2h;
+    for (int i = 0; i < count; ++i) {
+      check_cuda(cudaEventCreateWithFlags(&up[i], cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreateWithFlags(&sorted[i], cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreateWithFlags(&down[i], cudaEventDisableTiming), "event");
+    }
+    for (int r = 0; r < R; ++r) {
+      check_cuda(cudaMallocAsync(&dk[r], nmax * kw, st), "cudaMallocAsync");
+      if (pairs) check_cuda(cudaMallocAsync(&dv[r], nmax * 4, st), "cudaMallocAsync");
+    }
+    // the copy streams start after the buffers exist and after the caller's earlier work on `stream`
+    check_cuda(cudaEventRecord(sorted[0], st), "record");
+    check_cuda(cudaStreamWaitEvent(sh, sorted[0], 0), "wait");
+  });
+  auto upload_through = [&](int last) {  // enqueue the uploads of instances next_up .. last
+    for (; next_up <= last && next_up < count; ++next_up) {
+      const int j = next_up, r = j % R;
+      if (j >= R) check_cuda(cudaStreamWaitEvent(sh, down[j - R], 0), "wait");  // slot free again
+      if (n[j] >= 2) {
+        check_cuda(cudaMemcpyAsync(dk[r], host_keys[j], n[j] * kw, cudaMemcpyHostToDevice, sh), "h2d");
+        if (host_vals && host_vals[j])
+          check_cuda(cudaMemcpyAsync(dv[r], host_vals[j], n[j] * 4, cudaMemcpyHostToDevice, sh), "h2d");
+      }
+      check_cuda(cudaEventRecord(up[j], sh), "record");
+    }
+  };
+  for (int i = 0; rc == SR_OK && i < count; ++i) {
+    const int r = i % R;
+    // uploads run ahead of the sorts as far as the ring allows: the download of instance i - 1 is
+    // already enqueued, so slot (i + R - 1) % R has its release event
+    rc = guarded([&] {
+      upload_through(i + R - 1);
+      check_cuda(cudaStreamWaitEvent(st, up[i], 0), "wait");
+    });
+    if (rc != SR_OK) break;
+    const bool has_v = host_vals && host_vals[i];
+    if (n[i] >= 2) rc = has_v ? sr_sort_pairs(dk[r], dv[r], n[i], dtype, stream) : sr_sort_keys(dk[r], n[i], dtype, stream);
+    if (rc != SR_OK) break;
+    rc = guarded([&] {
+      check_cuda(cudaEventRecord(sorted[i], st), "record");
+      check_cuda(cudaStreamWaitEvent(sd, sorted[i], 0), "wait");
+      if (n[i] >= 2) {
+        check_cuda(cudaMemcpyAsync(host_keys[i], dk[r], n[i] * kw, cudaMemcpyDeviceToHost, sd), "d2h");
+        if (has_v) check_cuda(cudaMemcpyAsync(host_vals[i], dv[r], n[i] * 4, cudaMemcpyDeviceToHost, sd), "d2h");
+      }
+      check_cuda(cudaEventRecord(down[i], sd), "record");
+    });
+  }
+  // drain both copy streams into the caller's stream, release the ring, synchronise
+  const std::string err = t_state.err;
+  if (sh && sd) {
+    cudaEvent_t tail = up.empty() ? nullptr : up[0];
+    if (tail && cudaEventRecord(tail, sh) == cudaSuccess) cudaStreamWaitEvent(st, tail, 0);
+    tail = sorted.empty() ? nullptr : sorted[0];
+    if (tail && cudaEventRecord(tail, sd) == cudaSuccess) cudaStreamWaitEvent(st, tail, 0);
+  }
+  for (int r = 0; r < kRing; ++r) {
+    if (dk[r]) cudaFreeAsync(dk[r], st);
+    if (dv[r]) cudaFreeAsync(dv[r], st);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  for (int i = 0; i < count; ++i) {
+    if (up[i]) cudaEventDestroy(up[i]);
+    if (sorted[i]) cudaEventDestroy(sorted[i]);
+    if (down[i]) cudaEventDestroy(down[i]);
+  }
+  if (rc != SR_OK) {
+    t_state.err = err;
+  } else if (e != cudaSuccess) {
     t_state.err = cudaGetErrorString(e);
     rc = SR_ERR_CUDA;
   }

@@ -132,6 +132,59 @@ def test_host_api_roundtrip():
     assert np.array_equal(hk, oracle.sort_keys(k.astype(np.int64)))
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_batch_keys(pinned):
+    """sr_sort_host_batch: instances of mixed size and order (resident, tile,
+    multi-kernel, empty, single) pipelined over the ring of four buffers, more
+    instances than ring slots; each bit-exact with the oracle."""
+    specs = [("random", 2_000_000), ("reversed", 2_000_000), ("nearly", 2_000_000), ("few_unique", 2_000_000),
+             ("random", 0), ("sorted", 1), ("random", 5000), ("distance256", 300_007), ("random", 3_000_001),
+             ("runs1024", 100_003), ("random", 2)]
+    src = [gen.make(o, n, np.int32, config=13, instance=i) for i, (o, n) in enumerate(specs)]
+    if pinned:
+        hold = [torch.from_numpy(k.copy()).pin_memory() for k in src]
+        bufs = [h.numpy() for h in hold]
+    else:
+        bufs = [k.copy() for k in src]
+    stream = torch.cuda.Stream()
+    sr.sort_host_batch(bufs, stream=stream.cuda_stream)
+    for k, b, (o, n) in zip(src, bufs, specs):
+        assert np.array_equal(b, oracle.sort_keys(k)), (o, n)
+
+
+def test_host_batch_pairs_and_int64():
+    ns = [700_001, 8193, 1_500_000, 33, 2_000_000, 100]
+    ks = [gen.make("few100" if i % 2 else "random", n, np.int64, config=14, instance=i) for i, n in enumerate(ns)]
+    vs = [gen.index_payload(n) for n in ns]
+    hk, hv = [k.copy() for k in ks], [v.copy() for v in vs]
+    hv[3] = None  # a keys-only instance inside a pair batch
+    sr.sort_host_batch(hk, hv)
+    for i, (k, v) in enumerate(zip(ks, vs)):
+        if hv[i] is None:
+            assert np.array_equal(hk[i], oracle.sort_keys(k))
+        else:
+            ek, ev = oracle.sort_pairs(k, v)
+            assert np.array_equal(hk[i], ek) and np.array_equal(hv[i], ev), i
+
+
+def test_host_batch_errors():
+    k = gen.make("random", 1000, np.int32, config=15)
+    assert sr.sort_host_batch([]) == []
+    with pytest.raises(TypeError):
+        sr.sort_host_batch([k.copy(), k.astype(np.int64)])
+    import ctypes
+    L = sr.lib()
+    ns = (ctypes.c_int64 * 1)(-1)
+    kp = (ctypes.c_void_p * 1)(k.ctypes.data)
+    assert L.sr_sort_host_batch(kp, None, ns, 1, sr.SR_INT32, None) == 1   # SR_ERR_INVALID_ARGUMENT
+    ns[0] = 1000
+    assert L.sr_sort_host_batch(kp, None, ns, 1, 99, None) == 2            # SR_ERR_UNSUPPORTED_DTYPE
+    assert L.sr_sort_host_batch(None, None, ns, 1, sr.SR_INT32, None) == 1
+    assert L.sr_sort_host_batch(kp, None, ns, -1, sr.SR_INT32, None) == 1
+    kp[0] = None
+    assert L.sr_sort_host_batch(kp, None, ns, 1, sr.SR_INT32, None) == 1
+
+
 def test_streams_and_concurrency():
     """Work is enqueued on the caller's stream; two streams sort independently."""
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
