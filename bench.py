@@ -8,11 +8,17 @@ values).  One STEP = one sort of one instance of each of the four orders
 same line carries, under "c5a", configs[4]'s 256M-key int32 random sort (the
 metric's "n=2M/256M" second half), measured the same way in the same run.
 
-Timing: every sort is bracketed by CUDA events on the sort's stream.  Before
-each sort the input is restored from a pristine device copy and L2 is flushed
-by writing a 512 MiB buffer (both untimed, outside the events); the K timed
-steps are bracketed by barrier + synchronize on both sides and the max over
-ranks is taken.  e2e: the same metric through the host-buffer calls (HOST
+Timing: every sort is bracketed by CUDA events on the sort's stream.  No sort
+finds its input in L2.  The 2M-key workloads run configs[1]'s procedure --
+seeded instances of each order sorted back to back -- with one input buffer
+per sort of the run (steps + warmup, every order: 736 MB by default, >= 4 L2
+sizes or the flush below is used), all restored from pristine copies before
+the first sort, so every input comes from HBM while what the sorts share (the
+kernels' code, the scratch) stays cached; detail.l2_flushed times a few steps
+the other way: input restored and L2 flushed by a 512 MiB write before every
+sort (untimed), which also evicts the code.  The 1 GiB workloads (one instance
+per order) use the flush.  The K timed steps are bracketed by barrier +
+synchronize on both sides and the max over ranks is taken.  e2e: the same metric through the host-buffer calls (HOST
 pinned buffers; H2D copies, sorts, D2H copies and the stream sync inside the
 events): the step's instances as one sr_sort_host_batch call (uploads and
 downloads of neighbouring instances overlap the sorts), with the
@@ -136,7 +142,7 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled every ~2 ms during the timed region
+    """SM clock + throttle reasons sampled every ~0.5 ms during the timed region
     (NVML in-process; the timed region is far shorter than nvidia-smi's -lms
     floor).  Falls back to one nvidia-smi query if NVML is unavailable."""
 
@@ -180,7 +186,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def __exit__(self, *a):
         self.stop.set()
@@ -267,13 +273,37 @@ def unpin(old):
             pass
 
 
-def ref_config(wl):
+L2_BYTES = 126 * 1024 * 1024
+L2_TEXT = {
+    "flush": "flushed (512 MiB write) before every sort, outside the timed region",
+    "rotate": "inputs larger than L2: every sort of the run (steps + warmup, every order) has its own input "
+              "buffer, all restored from the pristine instances before the first sort, so at least 4x the L2 "
+              "size of other traffic lies between an input's last write and its sort (the input comes from HBM; "
+              "what the sorts share -- code, scratch -- stays cached, as between the paper's 100 instances per "
+              "order); the flushed variant is under detail.l2_flushed",
+}
+
+
+def l2_mode(wl, args):
+    """How the timed sorts are kept from finding their input in L2: "rotate"
+    (distinct input buffers, >= 4 L2 sizes in total; configs[1]'s "100 seeded
+    instances each of four input orders" back to back) when the run's inputs
+    are that large, else "flush" (a 512 MiB write before every sort; this also
+    evicts the kernels' code, which the next sort then fetches from HBM).  The
+    1 GiB workloads sort one instance per order: flush."""
+    n, dtype, orders, cfg = WORKLOADS[wl]
+    per = n * (elem_bytes(dtype) + (4 if wl in PAIRS else 0))
+    if args.l2 == "flush" or n >= 50_000_000:
+        return "flush"
+    return "rotate" if per * len(orders) * (args.steps + args.warmup) >= 4 * L2_BYTES else "flush"
+
+
+def ref_config(wl, args):
     """The workload description both arms print (the driver pairs the arms on
     metric + config)."""
     n, dtype, orders, cfg = WORKLOADS[wl]
     return {"workload": wl, "n": n, "dtype": dtype_label(dtype), "pairs": wl in PAIRS, "orders": orders,
-            "keys_per_step": n * len(orders),
-            "l2": "flushed (512 MiB write) before every sort, outside the timed region"}
+            "keys_per_step": n * len(orders), "l2": L2_TEXT[l2_mode(wl, args)]}
 
 
 def run_reference(args, wl):
@@ -304,7 +334,7 @@ def run_reference(args, wl):
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3),
             "unit": "Mkeys/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": dtype_label(dtype), "data": "synthetic", "config": ref_config(wl),
+            "dtype": dtype_label(dtype), "data": "synthetic", "config": ref_config(wl, args),
             "cpu_baseline": {"value": round(v, 3), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
                              "sample": f"first {m} keys of instance 0 of each order, single-threaded C mergesort"
                                        + (f" pinned to core {core}" if core is not None else "")},
@@ -399,24 +429,46 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
         vals_pristine = torch.from_numpy(gen.index_payload(n).view(np.int32)).to(dev)
         work_v = torch.empty(n, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    rotate = l2_mode(wl, args) == "rotate"
+    works, works_v = {}, {}
+    if rotate:  # one input buffer per sort of the run (see l2_mode)
+        for i in range(total):
+            for o in orders:
+                works[(o, i)] = torch.empty(shape, dtype=tdt, device=dev)
+                if pairs:
+                    works_v[(o, i)] = torch.empty(n, dtype=torch.int32, device=dev)
 
-    def one_sort(o, i, ev=None):
-        work.copy_(pristine[(o, i % ninst)])
-        if pairs:
-            work_v.copy_(vals_pristine)
-        flush.fill_(i)
+    def restore_all():  # in the order the sorts run
+        for i in range(total):
+            for o in orders:
+                works[(o, i)].copy_(pristine[(o, i % ninst)])
+                if pairs:
+                    works_v[(o, i)].copy_(vals_pristine)
+
+    def one_sort(o, i, ev=None, flushed=False):
+        """Sort instance i of order o; returns (plan, keys, vals) -- the buffers hold the output."""
+        if rotate and not flushed:
+            wk, wv = works[(o, i)], works_v.get((o, i))
+        else:
+            wk, wv = work, work_v if pairs else None
+            wk.copy_(pristine[(o, i % ninst)])
+            if pairs:
+                wv.copy_(vals_pristine)
+            flush.fill_(i)
         if ev:
             ev[0].record(stream)
         if rec:
-            sr.sort_records(work)
+            sr.sort_records(wk)
         elif pairs:
-            sr.sort_pairs(work, work_v)
+            sr.sort_pairs(wk, wv)
         else:
-            sr.sort_keys(work)
+            sr.sort_keys(wk)
         if ev:
             ev[1].record(stream)
-        return sr.last_plan()
+        return sr.last_plan(), wk, wv
 
+    if rotate:
+        restore_all()
     for w in range(warm):
         for o in orders:
             one_sort(o, w)
@@ -436,14 +488,17 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
         t_wall0 = time.perf_counter()
         for s in range(steps):
             for j, o in enumerate(orders):
-                plans.append((o, one_sort(o, warm + s, evs[s][j])))
+                plan, wk, wv = one_sort(o, warm + s, evs[s][j])
+                plans.append((o, plan))
                 if big:
                     if o not in first_big:
-                        first_big[o] = (work.clone(), work_v.clone() if pairs else None)
+                        first_big[o] = (wk.clone(), wv.clone() if pairs else None)
                     else:
-                        big_same &= torch.equal(first_big[o][0], work) and (not pairs or torch.equal(first_big[o][1], work_v))
+                        big_same &= torch.equal(first_big[o][0], wk) and (not pairs or torch.equal(first_big[o][1], wv))
+                elif rotate:
+                    kept[(o, warm + s)] = (wk, wv)  # (the sort's own buffer: nothing else writes it before the checks)
                 else:
-                    kept[(o, warm + s)] = (work.clone(), work_v.clone() if pairs else None)
+                    kept[(o, warm + s)] = (wk.clone(), wv.clone() if pairs else None)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     if ws > 1:
@@ -513,6 +568,26 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     if big and not big_same:
         check["failed"] += 1
     del kept, first_big, to_check
+
+    # ---- the flushed variant (rotate runs only): restore + 512 MiB write before every sort, which
+    # also evicts the kernels' code; a few steps, same events, for comparison
+    flushed = None
+    if rotate:
+        fsteps = min(steps, 5)
+        for o in orders:
+            one_sort(o, 0, flushed=True)
+        fev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in orders]
+               for _ in range(fsteps)]
+        for s in range(fsteps):
+            for j, o in enumerate(orders):
+                one_sort(o, warm + s, fev[s][j], flushed=True)
+        torch.cuda.synchronize()
+        fms = {o: statistics.mean(fev[s][j][0].elapsed_time(fev[s][j][1]) for s in range(fsteps))
+               for j, o in enumerate(orders)}
+        ftot = max_over_ranks(sum(fms.values()), dev)
+        flushed = {"value": round(n * len(orders) * ws / (ftot / 1e3) / 1e6, 2), "unit": "Mkeys/s", "steps": fsteps,
+                   "ms_per_step": round(ftot, 4), "per_order_ms_mean": {o: round(v, 4) for o, v in fms.items()},
+                   "l2": L2_TEXT["flush"]}
 
     # ---- e2e through the host API (pinned host buffers, copies inside the events)
     e2e = None
@@ -593,6 +668,8 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     # ---- per-kernel device times (profile pass over the same inputs, CUDA events on the sort stream)
     sr.set_option(sr.OPT_PROFILE, 1)
     kern = {}
+    if rotate:
+        restore_all()
     for s in range(steps):
         for o in orders:
             one_sort(o, warm + s)
@@ -618,14 +695,15 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
                                 "GBps": round(v["bytes"] / v["launches"] / (v["ms"] / v["launches"] / 1e3) / 1e9, 1),
                                 "launches_per_step": v["launches"] / steps} for k, v in kern.items()}}
     step_ms_mean = total_ms / steps
-    del pristine, work, flush
+    del pristine, work, flush, works, works_v
     torch.cuda.empty_cache()
     return {
         "value": round(value, 2), "ms_per_step": round(step_ms_mean, 4), "dtype": dtype_label(dtype) + (
             "+u32 payload" if pairs else ""),
         "detail": {"per_order_ms_mean": {o: round(statistics.mean(v), 4) for o, v in per_order_ms.items()},
                    "total_of_order_means_ms": round(sum(statistics.mean(v) for v in per_order_ms.values()), 4),
-                   "routes": route_of, "wall_s": round(t_wall, 3),
+                   "routes": route_of, "wall_s": round(t_wall, 3), "l2_mode": "rotate" if rotate else "flush",
+                   **({"l2_flushed": flushed} if flushed else {}),
                    "parallelism": f"independent instances per rank x{ws}"},
         "whole_step_hbm": {"bytes_planned_per_step": int(bytes_planned),
                            "GBps": round(bytes_planned / (step_ms_mean / 1e3) / 1e9, 1),
@@ -646,6 +724,9 @@ def main():
     ap.add_argument("--sub", default="c5a", help="second workload reported inside the same line ('none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--l2", default="rotate", choices=["rotate", "flush"],
+                    help="keep inputs out of L2 by rotating input buffers (when the run's inputs are >= 4 L2 "
+                         "sizes) or by a 512 MiB write before every sort (see l2_mode)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     wl = args.workload
@@ -672,7 +753,7 @@ def main():
     sub = None
     if args.sub and args.sub != "none" and args.sub != wl:
         sm = measure(args.sub, args, sr, dev, stream, rank, ws, oracle_leg)
-        sub = {"workload": args.sub, "config": ref_config(args.sub), "value": sm["value"], "unit": "Mkeys/s",
+        sub = {"workload": args.sub, "config": ref_config(args.sub, args), "value": sm["value"], "unit": "Mkeys/s",
                "ms_per_step": sm["ms_per_step"], "dtype": sm["dtype"], **{k: sm[k] for k in (
                    "detail", "whole_step_hbm", "roofline", "gpu_launches", "clocks", "e2e", "verified",
                    "cpu_baseline")}}
@@ -680,7 +761,7 @@ def main():
     line = {
         "metric": METRIC, "value": m["value"], "unit": "Mkeys/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": m["dtype"], "data": "synthetic", "config": ref_config(wl),
+        "vs_baseline": None, "dtype": m["dtype"], "data": "synthetic", "config": ref_config(wl, args),
         "detail": m["detail"], "whole_step_hbm": m["whole_step_hbm"], "roofline": m["roofline"],
         "gpu_launches": m["gpu_launches"], "clocks": m["clocks"], "verified": m["verified"],
     }
