@@ -986,6 +986,32 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     // and round would leave the reversal latency-bound)
     constexpr int UR = 8;
     const int64_t half = n / 2, stride = (int64_t)P * NT;
+    constexpr int V = 16 / (int)sizeof(K);
+    if ((reinterpret_cast<uintptr_t>(a.keys) & 15) == 0 && n % V == 0) {
+      // 16-byte vectors: vector p swaps with vector nv-1-p, both reversed inside
+      // (a quarter of the scalar loop's memory instructions)
+      constexpr int UV = 4;
+      const int64_t nv = n / V, halfv = nv / 2;
+      int4* kv = reinterpret_cast<int4*>(a.keys);
+      auto rev = [](int4 v) { return sizeof(K) == 4 ? make_int4(v.w, v.z, v.y, v.x) : make_int4(v.z, v.w, v.x, v.y); };
+      for (int64_t p0 = (int64_t)c * NT + tid; p0 < halfv; p0 += UV * stride) {
+        int4 x[UV], y[UV];
+#pragma unroll
+        for (int u = 0; u < UV; u++) {
+          const int64_t p = p0 + u * stride;
+          if (p < halfv) { x[u] = kv[p]; y[u] = kv[nv - 1 - p]; }
+        }
+#pragma unroll
+        for (int u = 0; u < UV; u++) {
+          const int64_t p = p0 + u * stride;
+          if (p < halfv) { kv[p] = rev(y[u]); kv[nv - 1 - p] = rev(x[u]); }
+        }
+      }
+      if ((nv & 1) && c == 0 && tid == 0) kv[halfv] = rev(kv[halfv]);  // the middle vector
+      __syncthreads();
+      SR_RES_STAMP(3);  // (SR_TIMING: printed as "C.tree" on this route)
+      return;
+    }
     for (int64_t p0 = (int64_t)c * NT + tid; p0 < half; p0 += UR * stride) {
       K x[UR], y[UR];
 #pragma unroll

@@ -63,6 +63,26 @@ def test_resident_c2_and_limits(order):
             assert p["launches"] > 1  # beyond the resident limit: multi-kernel path
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_resident_reversal_vector_and_scalar(dtype):
+    """REVERSED route in the one launch: 16-byte vector
+    swaps when the keys are 16-byte aligned and n is a whole number of vectors
+    (even and odd vector counts: the middle vector reverses in place), the
+    scalar loop otherwise (ragged n, or a base pointer off the 16-byte grid)."""
+    v = 16 // np.dtype(dtype).itemsize
+    for n in [8192 + v, 8192 + 2 * v, 8192 + 3 * v, 8193 + v, 100_000, 100_000 + v, 1_000_003, 2_000_000, 2_000_000 + v]:
+        for off in (0, 1):
+            k = gen.make("reversed", n, dtype, config=1)
+            buf = torch.empty(n + off, dtype=torch.int32 if dtype == np.int32 else torch.int64, device="cuda")
+            d = buf[off:]
+            d.copy_(torch.from_numpy(k))
+            sr.sort_keys(d)
+            torch.cuda.synchronize()
+            p = sr.last_plan()
+            assert p["route_name"] == "reversed" and p["launches"] == 1, (n, off, p)
+            assert np.array_equal(d.cpu().numpy(), oracle.sort_keys(k)), (n, off)
+
+
 @pytest.mark.parametrize("cap", [1, 37, 300, 1024, 2000])
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
 def test_resident_lowered_caps(cap, dtype):
