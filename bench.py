@@ -649,9 +649,11 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
                         if pairs:
                             hvals.copy_(hvals_src)
                         sr.sort_host(hb, hv, stream.cuda_stream)
-                        bad += 0 if torch.equal(hbo, hbuf) else 1
-                        hk_np = hbo.numpy().reshape(n, -1)[:, 0] if rec else hbo.numpy()
-                        bad += 0 if bool(np.all(hk_np[:-1] <= hk_np[1:])) else 1
+                        ibits = np.int32 if hbo.element_size() == 4 else np.int64  # (bit patterns: NaN keys)
+                        bad += 0 if np.array_equal(hbo.numpy().view(ibits), hbuf.numpy().view(ibits)) else 1
+                        if not hbo.is_floating_point():
+                            hk_np = hbo.numpy()
+                            bad += 0 if bool(np.all(hk_np[:-1] <= hk_np[1:])) else 1
                     for hvo in hvs or []:
                         bad += 0 if torch.equal(hvo, hvals) else 1
             bat_ms = max_over_ranks(bat_ms, dev)

@@ -138,6 +138,37 @@ def test_h7_splitters(order, nb, dtype):
     assert ge.tolist() == ee.tolist()
 
 
+@pytest.mark.parametrize("order", ["random", "few_unique", "all_equal", "organ_pipe", "nearly"])
+@pytest.mark.parametrize("nb", [64, 512, 2048])
+def test_h7_splitters_paper_properties(order, nb):
+    """What the paper fixes about the pivots, checked on the kernel's output
+    without the step oracle (whose sample positions restate the kernel's
+    jitter, R8): the nb - 1 splitters are non-decreasing elements of
+    the array chosen from a sample, so range buckets stay near
+    n / nb on distinct keys; a key repeated more than gamma = 2 times among the
+    sampled candidates gets an equality bucket, so
+    the heavy keys of few-unique inputs are all flagged and a flagged splitter
+    always repeats in the array."""
+    n = 300_007
+    k = gen.make(order, n, np.int32, config=25)
+    gs, ge = sr.splitters(cuda(k), nb)
+    gs, ge = np.asarray(gs.tolist(), dtype=np.int64), np.asarray(ge.tolist(), dtype=np.int64)
+    assert gs.size == nb - 1 and ge.size == nb - 1
+    assert np.all(np.diff(gs) >= 0)
+    vals, counts = np.unique(k, return_counts=True)
+    freq = dict(zip(vals.tolist(), counts.tolist()))
+    assert all(int(t) in freq for t in gs)                      # pivots are keys of the array
+    assert all(freq[int(t)] > 2 for t, f in zip(gs, ge) if f)   # an equality pivot repeats (gamma = 2)
+    if order in ("random", "nearly", "organ_pipe"):
+        # lower_bound buckets of (nearly) distinct keys: no bucket far above the mean
+        b = np.searchsorted(gs, k.astype(np.int64), side="left")
+        assert np.bincount(b, minlength=nb).max() <= 8 * n / nb + 64
+    if order == "few_unique":   # 10 values of ~n/10 keys each: every one has its equality bucket
+        assert set(gs[ge == 1].tolist()) == set(vals.tolist())
+    if order == "all_equal":
+        assert set(gs.tolist()) == set(vals.tolist()) and ge.all()
+
+
 # ---------------------------------------------------------------- H8-H10 partition level
 
 @pytest.mark.parametrize("order", ["random", "few_unique", "few100", "nearly", "all_equal", "organ_pipe", "extremes"])

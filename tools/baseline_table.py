@@ -22,6 +22,7 @@ for j in lines():
     w = cfg.get("workload")
     if w not in NAME:
         continue
+    label = NAME[w] + (" (L2 flushed)" if w == "c2" and cfg.get("l2", "").startswith("flushed") else "")
     n = cfg["n"]
     per = j["detail"]["per_order_ms_mean"]
     routes = j["detail"]["routes"]
@@ -33,7 +34,7 @@ for j in lines():
     orc = f"{n / cpu['value']:.0f}" if cpu.get("value") else ""
     dt = cfg.get("dtype", "") + (" pairs" if cfg.get("pairs") else "")
     for o, ms in per.items():
-        print(f"| {NAME[w]} | {o} | {n:,} | {dt} | {ms * 1e3:.1f} | {n / (ms * 1e3):,.0f} | {routes.get(o, '')} | | | | | {orc} | {par} |")
-    print(f"| {NAME[w]} | **step ({len(per)} orders)** | | | {j['ms_per_step'] * 1e3:.1f} | {j['value']:,.0f} | | "
+        print(f"| {label} | {o} | {n:,} | {dt} | {ms * 1e3:.1f} | {n / (ms * 1e3):,.0f} | {routes.get(o, '')} | | | | | {orc} | {par} |")
+    print(f"| {label} | **step ({len(per)} orders)** | | | {j['ms_per_step'] * 1e3:.1f} | {j['value']:,.0f} | | "
           f"{hb.get('bytes_planned_per_step', 0) / 1e6:,.0f} MB | {hb.get('frac_of_peak', '')} | {hb.get('ideal_pass_frac', '')} | "
           f"{(rf.get('traffic') or 0) / 1e6:,.0f} MB ({rf.get('kernel', '')}, {rf.get('traffic_source', {}).get('source', '') if rf.get('traffic_source') else ''}) | | {par} |")
