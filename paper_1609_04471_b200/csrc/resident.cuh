@@ -208,6 +208,23 @@ __device__ __forceinline__ void res_publish(const ResArgs<K>& a, int in_kernel) 
   a.done->seq = a.seq;
 }
 
+// The same by a whole warp (all 32 lanes call): the statistics words are copied
+// in parallel (one L2 round trip instead of one per word by a single thread).
+template <typename K>
+__device__ __forceinline__ void res_publish_warp(const ResArgs<K>& a, int in_kernel) {
+  if (!a.done) return;
+  const int lane = threadIdx.x & 31;
+  __threadfence();  // (the lane that wrote a.st)
+  __syncwarp();
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(a.st);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(&a.done->st);
+  for (int i = lane; i < (int)(sizeof(DevStats) / 8); i += 32) d[i] = __ldcg(s + i);
+  if (lane == 0) a.done->in_kernel = in_kernel;
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) a.done->seq = a.seq;
+}
+
 // Shared memory: the persistent bucket table + phase-local buffers in a union.
 template <typename K>
 struct ResSmem {
@@ -828,6 +845,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     SR_RES_CSUB(6);
     for (int q = tid; q < QS; q += NT) a.samp[(int64_t)quarter * QS + q] = sq[q];
   }
+  __shared__ int s_skip;              // (samplers) another route was published: the speculative work stops
+  __shared__ long long s_skip_route;  // ... and this is it
   if (sampler) {  // the samplers turn their sorted pieces into the level-1 splitters (R14)
     static_assert(kResSamplers == 4, "four sorted sample pieces");
     // speculatively, before the route is known (the splitters are ready when it
@@ -839,22 +858,40 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
     // (every sampler takes every step, so the counter advances by the same
     // amount in every launch; once CTA 0 has published a route other than
     // PARTITION the remaining work is skipped)
-    __shared__ int s_skip;
     if (tid == 0) s_skip = 0;
+    __syncthreads();  // (step() reads it first)
+    int steps_done = 0;  // (thread 0) this sampler's increments of the step counter in this launch
+    bool part_known = false;  // (thread 0) the published route is PARTITION: nothing more to watch
+    // a route other than PARTITION, published by CTA 0 (one more arrival), ends the samplers'
+    // work at once, also while waiting for the others; this sampler's remaining increments
+    // are added then, so that the counter still advances by 3 kResSamplers per launch, and
+    // the route is kept for the route step below
     auto step = [&](uint32_t target) {  // publish this CTA's writes, wait for the other samplers'
+      if (s_skip) return true;  // (uniform: written before the barrier that ended the last step)
       __threadfence();
       __syncthreads();
       if (tid == 0) {
         atomicAdd(a.scount, 1u);
-        uint32_t v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.scount) : "memory");
-        } while ((uint32_t)(v - a.scount_base) < target);
-        uint32_t arr;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(arr) : "l"(a.arrive) : "memory");
-        if ((uint32_t)(arr - a.arrive_base) >= (uint32_t)P + 1u &&
-            __ldcg(reinterpret_cast<const long long*>(&a.st->route)) != kRoutePartition)
-          s_skip = 1;
+        steps_done++;
+        for (;;) {
+          uint32_t v, arr;  // both counters in flight together (relaxed loads, fenced below)
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%2];\n\tld.relaxed.gpu.global.u32 %1, [%3];"
+                       : "=r"(v), "=r"(arr) : "l"(a.scount), "l"(a.arrive) : "memory");
+          if (!part_known && (uint32_t)(arr - a.arrive_base) >= (uint32_t)P + 1u) {  // CTA 0 has published the route
+            __threadfence();
+            const long long r = __ldcg(reinterpret_cast<const long long*>(&a.st->route));
+            if (r != kRoutePartition) {
+              if (steps_done < 3) atomicAdd(a.scount, (uint32_t)(3 - steps_done));
+              steps_done = 3;
+              s_skip_route = r;
+              s_skip = 1;
+              break;
+            }
+            part_known = true;
+          }
+          if ((uint32_t)(v - a.scount_base) >= target) break;
+        }
+        __threadfence();  // (acquire: the other samplers' writes, published before their increments)
       }
       __syncthreads();
       return s_skip != 0;
@@ -940,7 +977,8 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
   // samplers take the route CTA 0 publishes (one more arrival) instead of
   // resolving it themselves; the others wait for every CTA's tiles
   const uint32_t need = sampler ? (uint32_t)P + 1u : (uint32_t)P;
-  if (tid == 0) {
+  const bool have_route = sampler && s_skip;  // (uniform: s_skip is final after the sampler block's barriers)
+  if (tid == 0 && !have_route) {
     uint32_t v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.arrive) : "memory");
@@ -958,7 +996,7 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
   if (a.tstamp && c == 0 && tid == 0) a.tstamp[8 + 8 * (size_t)P + 32] = res_now();
   __shared__ int64_t s_route;
   if (sampler) {
-    if (tid == 0) s_route = __ldcg(reinterpret_cast<const long long*>(&a.st->route));
+    if (tid == 0) s_route = have_route ? s_skip_route : __ldcg(reinterpret_cast<const long long*>(&a.st->route));
   } else if (w == 0) {  // H1 resolve by one warp (CTA 0 also writes the statistics and run lists)
     const int64_t r = c == 0 ? presort_resolve_warp<K, true>(a.keys, n, sp.ts, a.G, a.lmin, a.asc, a.desc, a.st,
                                                              a.force, a.merge_ok, a.mm)
@@ -970,12 +1008,12 @@ __global__ void __launch_bounds__(kResNT, kResCtasPerSM) k_resident(const __grid
       if (c == 0) {  // the route is in a.st: tell the samplers
         __threadfence();
         atomicAdd(a.arrive, 1u);
-        // every route but the partition is decided here: sorted / reversed finish
-        // in this launch, merge / outlier / undecided continue on the host
-        if (r != kRoutePartition && !(r == kRouteOutlier && a.out_res))
-          res_publish(a, (r == kRouteSorted || r == kRouteReversed) ? 1 : 0);
       }
     }
+    // every route but the partition is decided here: sorted / reversed finish
+    // in this launch, merge / outlier / undecided continue on the host
+    if (c == 0 && r != kRoutePartition && !(r == kRouteOutlier && a.out_res))
+      res_publish_warp(a, (r == kRouteSorted || r == kRouteReversed) ? 1 : 0);
   }
   __syncthreads();
   const int64_t route = s_route;
