@@ -498,7 +498,7 @@ int64_t choose_tile(int64_t n) {  // K1 tile == level-1 chunk == L_min
 }
 // Buckets per segment: mean bucket ~kTargetBucket at level 1, ~kTargetBucket/2
 // below (those buckets are finished by one warp with 32 keys per lane).
-int choose_buckets(int64_t len, int level = 1, int key_bytes = 4) {
+int choose_buckets(int64_t len, int level = 1, int key_bytes = 4, bool keys_only = false) {
   // levels >= 2: mean 512 int32 / 256 int64 keys (measured: C5a 7.82 -> 7.71 ms
   // with 512 against 256; C5c 6.93 -> 7.10 ms, so int64 keeps 256)
   const int64_t t2 = g_tune[6] > 0 ? g_tune[6] : (key_bytes == 4 ? 2 : 1) * (kTargetBucket / 4);
@@ -509,6 +509,13 @@ int choose_buckets(int64_t len, int level = 1, int key_bytes = 4) {
   // within a few L2-resident segments
   if (level == 1 && len >= kBigLevel1) b = std::min<int64_t>(b, g_tune[1] > 0 ? g_tune[1] : kBigLevel1Buckets);
   if (level == 1 && g_tune[3] > 0) b = std::min<int64_t>(b, g_tune[3]);
+  // keys only, mid-size arrays (4M int32 / g_tune-measured int64 sizes .. 64M keys): level-1 segments of
+  // ~128K int32 / ~64K int64 keys, each split again into ~512-key buckets that the warp kernels finish.
+  // With kMaxBuckets level-1 buckets of ~8K keys half of them overflowed kCap and paid a second level
+  // of 16-32 buckets each, the rest a CTA-wide sort (tools/ab_tune.py "3=...", random keys: 16M int32
+  // 0.998 -> 0.717 ms, 32M 1.60 -> 1.19 ms, 8M 0.61 -> 0.48 ms; 16M int64 1.66 -> 1.11 ms)
+  if (level == 1 && keys_only && g_tune[3] == 0 && len >= (key_bytes == 4 ? (int64_t(4) << 20) : (int64_t(2) << 20)))
+    b = std::min<int64_t>(b, std::max<int64_t>(64, pow2ceil(ceil_div<int64_t>(len, key_bytes == 4 ? 131072 : 65536))));
   return (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(2, b));
 }
 
@@ -668,7 +675,7 @@ struct Sorter {
        // else the matrix (one scan) -- thousands of CTAs hammering 4k cursors is slower
       int64_t ent = 0;
       for (auto& p : parts)
-        ent += (2 * (int64_t)(forced_b ? forced_b : choose_buckets(p.len, level, (int)kw)) + 1) * ceil_div<int64_t>(p.len, chunk_size);
+        ent += (2 * (int64_t)(forced_b ? forced_b : choose_buckets(p.len, level, (int)kw, !HAS_V)) + 1) * ceil_div<int64_t>(p.len, chunk_size);
       L.atomic = !HAS_V && ent <= kAtomicMaxEntries;
     }
     int64_t chunk_base = 0, mat = 0, lp = 0, bins = 0;
@@ -677,7 +684,7 @@ struct Sorter {
       SegDesc d;
       d.start = parts[s].start;
       d.len = parts[s].len;
-      d.nbuckets = forced_b ? forced_b : choose_buckets(d.len, level, (int)kw);
+      d.nbuckets = forced_b ? forced_b : choose_buckets(d.len, level, (int)kw, !HAS_V);
       d.nbins = 2 * d.nbuckets + 1;
       d.nchunks = (int32_t)ceil_div<int64_t>(d.len, chunk_size);
       d.chunk_base = (int32_t)chunk_base;
