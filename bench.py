@@ -175,17 +175,24 @@ class ClockSampler:
             self.nv = None
         return self
 
-    def _run(self):
+    def sample_now(self):
+        """One sample from the calling thread (the timed loop calls it between two sorts, outside
+        their events: the sampler thread rarely gets scheduled inside a ~6 ms region)."""
         nv = self.nv
+        if nv is None:
+            return
+        try:
+            self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, attr in self.REASONS.items():
+                if r & getattr(nv, attr, 0):
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self.stop.is_set():
-            try:
-                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for name, attr in self.REASONS.items():
-                    if r & getattr(nv, attr, 0):
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            self.sample_now()
             time.sleep(0.0005)
 
     def __exit__(self, *a):
@@ -193,11 +200,21 @@ class ClockSampler:
         if self.t:
             self.t.join(timeout=1)
 
+    def absorb(self, other):
+        """Add the samples of another window of timed sorts (the flushed variant, the e2e passes)."""
+        self.extra = getattr(self, "extra", 0) + len(other.sm)
+        self.sm += other.sm
+        self.reasons |= other.reasons
+        self.max_mhz = self.max_mhz or other.max_mhz
+
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        extra = getattr(self, "extra", 0)
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "sm_mhz_min": min(self.sm)}
+                "samples": len(self.sm), "sm_mhz_min": min(self.sm),
+                "windows": f"{len(self.sm) - extra} samples during the K timed steps, {extra} during the other timed "
+                           "sorts of the run (flushed variant, e2e passes)"}
 
 
 # bench kernel names (sr_last_profile) -> ncu kernel-name prefixes
@@ -487,6 +504,8 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     with ClockSampler(dev.index) as clk:
         t_wall0 = time.perf_counter()
         for s in range(steps):
+            if not big:
+                clk.sample_now()  # (between two sorts, outside their events)
             for j, o in enumerate(orders):
                 plan, wk, wv = one_sort(o, warm + s, evs[s][j])
                 plans.append((o, plan))
@@ -574,6 +593,7 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     flushed = None
     if rotate:
         fsteps = min(steps, 5)
+        clk_f = ClockSampler(dev.index).__enter__()
         for o in orders:
             one_sort(o, 0, flushed=True)
         fev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in orders]
@@ -582,6 +602,8 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
             for j, o in enumerate(orders):
                 one_sort(o, warm + s, fev[s][j], flushed=True)
         torch.cuda.synchronize()
+        clk_f.__exit__()
+        clk.absorb(clk_f)
         fms = {o: statistics.mean(fev[s][j][0].elapsed_time(fev[s][j][1]) for s in range(fsteps))
                for j, o in enumerate(orders)}
         ftot = max_over_ranks(sum(fms.values()), dev)
@@ -592,6 +614,7 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
     # ---- e2e through the host API (pinned host buffers, copies inside the events)
     e2e = None
     if not args.no_e2e:
+        clk_e = ClockSampler(dev.index).__enter__()
         pin = {o: torch.from_numpy(host_inputs[(o, 0)]).pin_memory() for o in orders}
         hbuf = torch.empty(shape, dtype=tdt).pin_memory()
         hb = hbuf.numpy()
@@ -665,6 +688,8 @@ def measure(wl, args, sr, dev, stream, rank, ws, oracle_leg):
                    "call": "sr_sort_host_batch, the step's instances in one call (copies overlap the sorts)",
                    "per_call": {"value": e2e["value"], "ms_per_step": e2e["ms_per_step"], "call": e2e["call"]}}
             del hbufs, hvs
+        clk_e.__exit__()
+        clk.absorb(clk_e)
         del pin, hbuf
 
     # ---- per-kernel device times (profile pass over the same inputs, CUDA events on the sort stream)
